@@ -1,0 +1,557 @@
+// sm_100a Krylov solver: the reference's right-preconditioned restarted
+// GMRES (linsolve.py:107-210), its least-squares solution-extrapolation
+// initial guess (linsolve.py:213-242) and the dense complex matvec
+// (linsolve.py:73-77), as persistent cooperative kernels.
+//
+// One launch runs a whole solve: the grid stays resident, phases are
+// separated by grid-wide barriers, and every global reduction is summed in
+// a fixed order (block partials -> every block re-reduces the same
+// partials the same way), so all blocks agree bit-for-bit on every scalar
+// (Arnoldi coefficients, Givens rotations, residual estimates) and make
+// the same convergence decisions without a host round trip.  The host
+// sees one launch and one small read-back per frequency.
+//
+// The matvec streams A once per application with 16-byte loads; a warp
+// owns R rows at a time so each x-element load feeds R FMAs.  MGS is kept
+// (not CGS) for iteration-count parity: step i of the orthogonalisation
+// fuses "w -= h_i v_i" with the partial dot of step i+1, one barrier each.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "ewb_common.cuh"
+#include "ewb_krylov.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ewb {
+
+constexpr int kSolveThreads = 512;
+constexpr int kSolveWarps = kSolveThreads / 32;
+constexpr int kMaxRed = 16;  // doubles per grid reduction
+
+__device__ __forceinline__ cplx ldc(const cplx* p) {
+  double2 v = __ldcs(reinterpret_cast<const double2*>(p));  // streaming (evict-first)
+  return {v.x, v.y};
+}
+__device__ __forceinline__ cplx ldg(const cplx* p) {
+  double2 v = *reinterpret_cast<const double2*>(p);
+  return {v.x, v.y};
+}
+
+// Deterministic grid-wide sum of C doubles per thread.  `red` alternates
+// between two partial buffers so a fast block never overwrites partials a
+// slow block is still reading.
+struct GridRed {
+  double* partial;  // [2][G][kMaxRed]
+  int parity;
+};
+
+template <int C>
+__device__ void grid_sum(cg::grid_group& grid, GridRed& R, double (&v)[C]) {
+  __shared__ double s_w[kSolveWarps][kMaxRed];
+  __shared__ double s_out[kMaxRed];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    warp_sum(v[c]);
+    if (lane == 0) s_w[wid][c] = v[c];
+  }
+  __syncthreads();
+  double* part = R.partial + (size_t)R.parity * gridDim.x * kMaxRed;
+  if (threadIdx.x < C) {
+    double s = 0.0;
+    for (int w = 0; w < kSolveWarps; ++w) s += s_w[w][threadIdx.x];
+    part[(size_t)blockIdx.x * kMaxRed + threadIdx.x] = s;
+  }
+  grid.sync();
+  if (wid == 0) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double s = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) s += part[(size_t)b * kMaxRed + c];
+      warp_sum(s);
+      if (lane == 0) s_out[c] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < C; ++c) v[c] = s_out[c];
+  __syncthreads();
+  R.parity ^= 1;
+}
+
+// y[:, k] = A x[:, k] for K right-hand sides (x, y stored column after
+// column, leading dimension n).  Rows are dealt to warps R at a time.
+template <int RR, int K>
+__device__ void matvec_grid(const cplx* __restrict__ A, long long n, const cplx* x, cplx* y) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r0 = gw * RR; r0 < n; r0 += nw * RR) {
+    cplx acc[RR][K];
+#pragma unroll
+    for (int a = 0; a < RR; ++a)
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[a][k] = {0.0, 0.0};
+    const int nr = (int)min((long long)RR, n - r0);
+    if (nr == RR) {
+      const cplx* rowp = A + r0 * n;
+#pragma unroll 2
+      for (long long c = lane; c < n; c += 32) {
+        cplx xv[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) xv[k] = ldg(x + k * n + c);
+#pragma unroll
+        for (int a = 0; a < RR; ++a) {
+          cplx av = ldc(rowp + a * n + c);
+#pragma unroll
+          for (int k = 0; k < K; ++k) cfma(acc[a][k], av, xv[k]);
+        }
+      }
+    } else {
+      for (long long c = lane; c < n; c += 32) {
+        cplx xv[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) xv[k] = ldg(x + k * n + c);
+        for (int a = 0; a < nr; ++a) {
+          cplx av = ldc(A + (r0 + a) * n + c);
+#pragma unroll
+          for (int k = 0; k < K; ++k) cfma(acc[a][k], av, xv[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < RR; ++a)
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        warp_sum(acc[a][k]);
+        if (lane == 0 && a < nr) y[k * n + r0 + a] = acc[a][k];
+      }
+  }
+}
+
+// z = P^{-1} v  (3x3 blocks; identity when pinv == nullptr).  Grid-stride
+// over elements: thread e owns DOFs 3e..3e+2.
+__device__ __forceinline__ void precond_apply_elem(const cplx* pinv, long long e, const cplx* v,
+                                                   cplx* z) {
+  cplx v0 = v[3 * e], v1 = v[3 * e + 1], v2 = v[3 * e + 2];
+  const cplx* P = pinv + 9 * e;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    // numpy einsum('bij,bj->bi') order: ((P0 v0 + P1 v1) + P2 v2)
+    cplx s = P[3 * a] * v0;
+    s = s + P[3 * a + 1] * v1;
+    s = s + P[3 * a + 2] * v2;
+    z[3 * e + a] = s;
+  }
+}
+
+__device__ __forceinline__ long long gtid() {
+  return (long long)blockIdx.x * blockDim.x + threadIdx.x;
+}
+__device__ __forceinline__ long long gthreads() { return (long long)gridDim.x * blockDim.x; }
+
+// Givens state kept redundantly (and identically) in every block.
+struct GivensShared {
+  cplx cs[kMaxRestart], sn[kMaxRestart], g[kMaxRestart + 1];
+  cplx h[kMaxRestart + 1];
+};
+
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ GivensShared gs;
+  __shared__ cplx s_y[kMaxRestart];
+  const long long n = a.n;
+  const long long tid = gtid(), nth = gthreads();
+  const bool have_pc = a.pinv != nullptr;
+  GridRed R{a.partial, 0};
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+  // ||b||
+  double v1[1] = {0.0};
+  for (long long k = tid; k < n; k += nth) v1[0] += abs2(a.b[k]);
+  grid_sum(grid, R, v1);
+  const double nb = sqrt(v1[0]);
+  if (nb == 0.0) {  // linsolve.py:136-140
+    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
+    if (tid == 0) { a.out->iterations = 0; a.out->init_res = 0; a.out->final_res = 0;
+                    a.out->n_hist = 0; a.out->converged = 1; }
+    return;
+  }
+  // r = b - A x0  (skipped when x0 is all zero: linsolve.py:144)
+  double anyv[1] = {0.0};
+  if (a.has_x0)
+    for (long long k = tid; k < n; k += nth) anyv[0] += (a.x[k].re != 0.0 || a.x[k].im != 0.0);
+  else
+    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
+  grid_sum(grid, R, anyv);
+  if (anyv[0] > 0.0) {
+    matvec_grid<4, 1>(a.A, n, a.x, a.w);
+    grid.sync();
+    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
+  } else {
+    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k];
+  }
+  double rr[1] = {0.0};
+  for (long long k = tid; k < n; k += nth) rr[0] += abs2(a.r[k]);
+  grid_sum(grid, R, rr);
+  double rnorm = sqrt(rr[0]);
+  double res = rnorm / nb;
+  int n_hist = 0;
+  if (tid == 0) { a.out->init_res = res; a.hist[n_hist] = res; }
+  n_hist++;
+  int its = 0;
+  while (res > a.tol && its < a.maxiter) {
+    const int m = min(a.restart, a.maxiter - its);
+    const double beta = rnorm;
+    // V0 = r / beta ; z = P^{-1} V0
+    for (long long k = tid; k < n; k += nth) {
+      cplx v = a.r[k];
+      a.V[k] = {v.re / beta, v.im / beta};
+    }
+    if (threadIdx.x == 0) {
+      gs.g[0] = {beta, 0.0};
+      for (int k = 1; k <= m; ++k) gs.g[k] = {0.0, 0.0};
+    }
+    grid.sync();
+    int used = 0;
+    for (int j = 0; j < m; ++j) {
+      const cplx* vj = a.V + (size_t)j * n;
+      // z = P^{-1} v_j
+      if (have_pc) {
+        for (long long e = tid; e < n / 3; e += nth) precond_apply_elem(a.pinv, e, vj, a.z);
+      } else {
+        for (long long k = tid; k < n; k += nth) a.z[k] = vj[k];
+      }
+      grid.sync();
+      matvec_grid<4, 1>(a.A, n, a.z, a.w);
+      grid.sync();
+      // MGS, fused: partial <v_0, w>
+      double dv[2] = {0.0, 0.0};
+      for (long long k = tid; k < n; k += nth) {
+        cplx p = conj(a.V[k]) * a.w[k];
+        dv[0] += p.re; dv[1] += p.im;
+      }
+      for (int i = 0; i <= j; ++i) {
+        grid_sum(grid, R, dv);
+        const cplx h = {dv[0], dv[1]};
+        if (threadIdx.x == 0) gs.h[i] = h;
+        const cplx* vi = a.V + (size_t)i * n;
+        const cplx* vn = a.V + (size_t)(i + 1) * n;
+        dv[0] = dv[1] = 0.0;
+        if (i < j) {
+          for (long long k = tid; k < n; k += nth) {
+            cplx w = a.w[k] - h * vi[k];
+            a.w[k] = w;
+            cplx p = conj(vn[k]) * w;
+            dv[0] += p.re; dv[1] += p.im;
+          }
+        } else {
+          for (long long k = tid; k < n; k += nth) {
+            cplx w = a.w[k] - h * vi[k];
+            a.w[k] = w;
+            dv[0] += abs2(w);
+          }
+        }
+      }
+      double nw[1] = {dv[0]};
+      grid_sum(grid, R, nw);
+      const double hn = sqrt(nw[0]);
+      if (hn > 0.0) {
+        cplx* vn = a.V + (size_t)(j + 1) * n;
+        for (long long k = tid; k < n; k += nth) {
+          cplx w = a.w[k];
+          vn[k] = {w.re / hn, w.im / hn};
+        }
+      }
+      // Givens (linsolve.py:171-194), identical in every block
+      if (threadIdx.x == 0) {
+        gs.h[j + 1] = {hn, 0.0};
+        for (int i = 0; i < j; ++i) {
+          cplx top = gs.cs[i] * gs.h[i] + gs.sn[i] * gs.h[i + 1];
+          gs.h[i + 1] = (-conj(gs.sn[i])) * gs.h[i] + conj(gs.cs[i]) * gs.h[i + 1];
+          gs.h[i] = top;
+        }
+        double ahj = hypot(gs.h[j].re, gs.h[j].im), ahn = hypot(gs.h[j + 1].re, gs.h[j + 1].im);
+        double den = sqrt(ahj * ahj + ahn * ahn);
+        if (den == 0.0) {
+          gs.cs[j] = {1.0, 0.0}; gs.sn[j] = {0.0, 0.0};
+        } else if (gs.h[j].re == 0.0 && gs.h[j].im == 0.0) {
+          gs.cs[j] = {0.0, 0.0}; gs.sn[j] = {1.0, 0.0};
+        } else {
+          gs.cs[j] = {ahj / den, 0.0};
+          cplx ph = {gs.h[j].re / ahj, gs.h[j].im / ahj};
+          cplx t = ph * conj(gs.h[j + 1]);
+          gs.sn[j] = {t.re / den, t.im / den};
+        }
+        gs.h[j] = gs.cs[j] * gs.h[j] + gs.sn[j] * gs.h[j + 1];
+        gs.h[j + 1] = {0.0, 0.0};
+        gs.g[j + 1] = (-conj(gs.sn[j])) * gs.g[j];
+        gs.g[j] = gs.cs[j] * gs.g[j];
+        if (blockIdx.x == 0) {
+          for (int i = 0; i <= j; ++i) a.H[(size_t)i * kMaxRestart + j] = gs.h[i];
+        }
+      }
+      __syncthreads();
+      ++its;
+      used = j + 1;
+      const double est = hypot(gs.g[j + 1].re, gs.g[j + 1].im) / nb;
+      if (tid == 0 && n_hist < a.hist_cap) a.hist[n_hist] = est;
+      n_hist++;
+      grid.sync();  // V_{j+1} complete, H visible
+      if (est <= a.tol) break;
+    }
+    // back substitution (linsolve.py:196-198): warp 0 of every block
+    if (wid == 0) {
+      for (int i = used - 1; i >= 0; --i) {
+        cplx s = {0.0, 0.0};
+        for (int k = i + 1 + lane; k < used; k += 32) s = s + a.H[(size_t)i * kMaxRestart + k] * s_y[k];
+        warp_sum(s);
+        if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, a.H[(size_t)i * kMaxRestart + i]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // x += P^{-1} (V^T y)   (u in w as scratch)
+    for (long long k = tid; k < n; k += nth) {
+      cplx u = {0.0, 0.0};
+      for (int i = 0; i < used; ++i) cfma(u, a.V[(size_t)i * n + k], s_y[i]);
+      a.w[k] = u;
+    }
+    if (have_pc) {
+      grid.sync();
+      for (long long e = tid; e < n / 3; e += nth) {
+        precond_apply_elem(a.pinv, e, a.w, a.z);
+        for (int c = 0; c < 3; ++c) a.x[3 * e + c] = a.x[3 * e + c] + a.z[3 * e + c];
+      }
+    } else {
+      for (long long k = tid; k < n; k += nth) a.x[k] = a.x[k] + a.w[k];
+    }
+    grid.sync();
+    // true residual (linsolve.py:200-201)
+    matvec_grid<4, 1>(a.A, n, a.x, a.w);
+    grid.sync();
+    double q[1] = {0.0};
+    for (long long k = tid; k < n; k += nth) {
+      cplx r = a.b[k] - a.w[k];
+      a.r[k] = r;
+      q[0] += abs2(r);
+    }
+    grid_sum(grid, R, q);
+    rnorm = sqrt(q[0]);
+    res = rnorm / nb;
+  }
+  if (tid == 0) {
+    a.out->iterations = its;
+    a.out->final_res = res;
+    a.out->converged = res <= a.tol;
+    a.out->n_hist = n_hist;
+  }
+}
+
+// ---------------------------------------------------------------------
+// SEM (linsolve.py:213-242): Y = A X (one pass over A for all K columns),
+// QR of Y[:, keep] by classical Gram-Schmidt with one re-orthogonalisation
+// (|R_ii| agrees with Householder's to rounding), rank filter
+// |R_ii| >= rank_tol * max|R_ii| (<= 2 passes), x0 = X s with R s = Q^H b;
+// falls back to the newest column.
+// ---------------------------------------------------------------------
+template <int K>
+__device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  matvec_grid<2, K>(a.A, n, a.X, a.Y);
+  grid.sync();
+  __shared__ int keep[kMaxSem];
+  __shared__ cplx Rm[kMaxSem][kMaxSem];
+  __shared__ int nkeep;
+  if (threadIdx.x == 0) {
+    nkeep = a.K;
+    for (int c = 0; c < a.K; ++c) keep[c] = c;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    const int kk = nkeep;
+    // QR of Y[:, keep] -> Q (columns in a.Q), R (shared)
+    for (int c = 0; c < kk; ++c) {
+      const cplx* yc = a.Y + (size_t)keep[c] * n;
+      cplx* qc = a.Q + (size_t)c * n;
+      for (long long k = tid; k < n; k += nth) qc[k] = yc[k];
+      if (threadIdx.x == 0)
+        for (int i = 0; i < kMaxSem; ++i) Rm[i][c] = {0.0, 0.0};
+      for (int rep = 0; rep < 2 && c > 0; ++rep) {
+        double d[2 * kMaxSem];
+#pragma unroll
+        for (int i = 0; i < 2 * kMaxSem; ++i) d[i] = 0.0;
+        for (long long k = tid; k < n; k += nth) {
+          cplx qk = qc[k];
+          for (int i = 0; i < c; ++i) {
+            cplx p = conj(a.Q[(size_t)i * n + k]) * qk;
+            d[2 * i] += p.re; d[2 * i + 1] += p.im;
+          }
+        }
+        grid_sum(grid, R, d);
+        for (long long k = tid; k < n; k += nth) {
+          cplx qk = qc[k];
+          for (int i = 0; i < c; ++i) qk = qk - cplx{d[2 * i], d[2 * i + 1]} * a.Q[(size_t)i * n + k];
+          qc[k] = qk;
+        }
+        if (threadIdx.x == 0)
+          for (int i = 0; i < c; ++i) Rm[i][c] = Rm[i][c] + cplx{d[2 * i], d[2 * i + 1]};
+        grid.sync();
+      }
+      double nn[1] = {0.0};
+      for (long long k = tid; k < n; k += nth) nn[0] += abs2(qc[k]);
+      grid_sum(grid, R, nn);
+      const double rcc = sqrt(nn[0]);
+      if (threadIdx.x == 0) Rm[c][c] = {rcc, 0.0};
+      if (rcc > 0.0) {  // an exactly dependent column keeps q = 0 (as Householder's R_cc = 0)
+        for (long long k = tid; k < n; k += nth) {
+          cplx q = qc[k];
+          qc[k] = {q.re / rcc, q.im / rcc};
+        }
+      }
+      grid.sync();
+    }
+    __syncthreads();
+    double dmax = 0.0;
+    for (int c = 0; c < kk; ++c) dmax = fmax(dmax, fabs(Rm[c][c].re));
+    bool good[kMaxSem];
+    bool all_good = true;
+    int ng = 0;
+    for (int c = 0; c < kk; ++c) {
+      double dg = fabs(Rm[c][c].re);
+      good[c] = dmax > 0 ? dg >= a.rank_tol * dmax : dg > 0;
+      all_good = all_good && good[c];
+      ng += good[c];
+    }
+    if (all_good) {
+      // s = R^{-1} Q^H b
+      double d[2 * kMaxSem];
+#pragma unroll
+      for (int i = 0; i < 2 * kMaxSem; ++i) d[i] = 0.0;
+      for (long long k = tid; k < n; k += nth) {
+        cplx bk = a.b[k];
+        for (int i = 0; i < kk; ++i) {
+          cplx p = conj(a.Q[(size_t)i * n + k]) * bk;
+          d[2 * i] += p.re; d[2 * i + 1] += p.im;
+        }
+      }
+      grid_sum(grid, R, d);
+      cplx s[kMaxSem];
+      for (int i = kk - 1; i >= 0; --i) {
+        cplx t = {d[2 * i], d[2 * i + 1]};
+        for (int k2 = i + 1; k2 < kk; ++k2) t = t - Rm[i][k2] * s[k2];
+        s[i] = cdiv(t, Rm[i][i]);
+      }
+      for (long long k = tid; k < n; k += nth) {
+        cplx x = {0.0, 0.0};
+        for (int i = 0; i < kk; ++i) cfma(x, a.X[(size_t)keep[i] * n + k], s[i]);
+        a.x0[k] = x;
+      }
+      if (tid == 0) { a.out->kept = kk; a.out->fallback = 0; }
+      return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int w = 0;
+      for (int c = 0; c < kk; ++c)
+        if (good[c]) keep[w++] = keep[c];
+      nkeep = w;
+    }
+    __syncthreads();
+    if (ng == 0) break;
+  }
+  for (long long k = tid; k < n; k += nth) a.x0[k] = a.X[k];
+  if (tid == 0) { a.out->kept = 0; a.out->fallback = 1; }
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 1) k_sem(SemArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  GridRed R{a.partial, 0};
+  switch (a.K) {
+    case 1: sem_body<1>(grid, R, a); break;
+    case 2: sem_body<2>(grid, R, a); break;
+    case 3: sem_body<3>(grid, R, a); break;
+    default: sem_body<4>(grid, R, a); break;
+  }
+}
+
+// Plain batched GEMV y_b = A_b x_b (one launch, `batch` systems of size n).
+template <int RR>
+__global__ void __launch_bounds__(512) k_gemv_batched(const cplx* A, const cplx* x, cplx* y,
+                                                      long long n, int batch) {
+  // blockIdx.y = system
+  const cplx* Ab = A + (size_t)blockIdx.y * n * n;
+  const cplx* xb = x + (size_t)blockIdx.y * n;
+  cplx* yb = y + (size_t)blockIdx.y * n;
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r0 = gw * RR; r0 < n; r0 += nw * RR) {
+    cplx acc[RR];
+#pragma unroll
+    for (int a = 0; a < RR; ++a) acc[a] = {0.0, 0.0};
+    const int nr = (int)min((long long)RR, n - r0);
+#pragma unroll 2
+    for (long long c = lane; c < n; c += 32) {
+      cplx xv = ldg(xb + c);
+#pragma unroll
+      for (int a = 0; a < RR; ++a)
+        if (a < nr) cfma(acc[a], ldc(Ab + (r0 + a) * n + c), xv);
+    }
+#pragma unroll
+    for (int a = 0; a < RR; ++a) {
+      warp_sum(acc[a]);
+      if (lane == 0 && a < nr) yb[r0 + a] = acc[a];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------
+static int g_coop_blocks = 0;
+
+static int coop_grid(const void* fn) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kSolveThreads, 0);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+int solver_grid_blocks() {
+  if (g_coop_blocks == 0) {
+    int a = coop_grid((const void*)k_gmres), b = coop_grid((const void*)k_sem);
+    g_coop_blocks = a < b ? a : b;
+  }
+  return g_coop_blocks;
+}
+
+cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
+  int G = solver_grid_blocks();
+  void* params[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)k_gmres, dim3(G), dim3(kSolveThreads), params, 0,
+                                     s);
+}
+
+cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
+  int G = solver_grid_blocks();
+  void* params[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)k_sem, dim3(G), dim3(kSolveThreads), params, 0, s);
+}
+
+cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long n, int batch,
+                                cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long warps_needed = (n + 3) / 4;
+  long long blocks = (warps_needed + 15) / 16;
+  long long cap = (long long)sms * 4 / (batch > 0 ? batch : 1);
+  if (cap < 1) cap = 1;
+  if (blocks > cap) blocks = cap;
+  k_gemv_batched<4><<<dim3((unsigned)blocks, batch), 512, 0, s>>>(A, x, y, n, batch);
+  return cudaGetLastError();
+}
+
+}  // namespace ewb
