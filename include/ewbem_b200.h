@@ -43,7 +43,7 @@ typedef struct ewb_gmres_result {
   int32_t iterations;
   int32_t n_hist;      /* entries written to the residual history */
   int32_t converged;
-  int32_t pad;
+  int32_t matvecs;    /* passes over A: iterations + true residuals + r0 */
   double init_residual;
   double final_residual;
 } ewb_gmres_result;
@@ -55,6 +55,10 @@ typedef struct ewb_sem_result {
 
 int ewb_abi_version(void);
 const char* ewb_last_error(void);
+
+/* Number of kernels this library has launched since load (all entry points);
+ * the benchmark reports the delta across its timed region. */
+int64_t ewb_launch_count(void);
 
 /* Per-mesh context: replaces Assembler.__init__ + _prepare_geometry +
  * static_offdiag_rowsums (assembly.py:112-216).  Uploads the element

@@ -532,6 +532,61 @@ def sampled_row_operator(vertices, triangles, med, rows, omega, vectors_t, vecto
     return tv.reshape(-1, K), uv.reshape(-1, K), rsum
 
 
+def column_sample_seconds(vertices, triangles, med, cols, omega, n_radial=8, n_angular=16):
+    """CPU seconds the reference algorithm spends on the columns ``cols``.
+
+    Runs, for the sampled columns only, exactly the per-column work of
+    DenseOracle: bucket/pair-geometry prep (assembly.py:142-171), the static
+    integrals (assembly.py:197-203) and one dynamic assembly at ``omega``
+    (assembly.py:233-246).  Used by bench.py to extrapolate a full-sweep CPU
+    time (per-column cost x n_e) without holding the O(n_e^2) pair data.
+    Returns dict(prep=, static=, dynamic=) seconds for the sample.
+    """
+    g = element_geometry(vertices, triangles)
+    xc = g["centroids"]
+    far, mid = rule_g3(), rule_g7()
+    near_cache = {}
+    t0 = time.perf_counter()
+    tier = tiers_for_rows(xc, g["diameters"], np.arange(len(triangles)), np.asarray(cols))
+    data = []
+    for jj, j in enumerate(cols):
+        vj = g["corners"][j]
+        groups = []
+        for tid, rule in ((0, far), (1, mid)):
+            rows = np.flatnonzero(tier[:, jj] == tid)
+            rows = rows[rows != j]
+            if rows.size:
+                groups.append((rows, rule))
+        nr = np.flatnonzero(tier[:, jj] == 2)
+        nr = nr[nr != j]
+        if nr.size:
+            lv = near_level(surface_distance(xc[nr], vj) / g["diameters"][j])
+            for l in np.unique(lv):
+                if l not in near_cache:
+                    near_cache[l] = rule_refine(rule_g7(), int(l))
+                groups.append((nr[lv == l], near_cache[l]))
+        buckets = []
+        for rows, (bary, wts) in groups:
+            r, d, dn = pair_geom(xc[rows], bary @ vj, g["normals"][j])
+            buckets.append((rows, wts * g["areas"][j], r, d, dn))
+        ys, ws = self_points(vj, n_radial, n_angular)
+        r, d, dn = pair_geom(xc[j][None, :], ys, g["normals"][j])
+        data.append((j, buckets, (ws, r, d, dn)))
+    t1 = time.perf_counter()
+    for j, buckets, _ in data:
+        for rows, w, r, d, dn in buckets:
+            blocks_static(r, d, dn, w, g["normals"][j], med)
+    t2 = time.perf_counter()
+    for j, buckets, (ws, r, d, dn) in data:
+        nj = g["normals"][j]
+        for rows, w, rr, dd, ddn in buckets:
+            blocks_dynamic(rr, dd, ddn, w, nj, med, omega)
+        blocks_dynamic(r, d, dn, ws, nj, med, omega)
+        blocks_static(r, d, dn, ws, nj, med)
+    t3 = time.perf_counter()
+    return dict(prep=t1 - t0, static=t2 - t1, dynamic=t3 - t2)
+
+
 # ----------------------------------------------------------------------
 # boundary conditions                              [assembly.py:263-305]
 # ----------------------------------------------------------------------

@@ -18,7 +18,7 @@ LIB_PATH = PKG_DIR / LIB_NAME
 
 # Every symbol include/ewbem_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
-    "ewb_abi_version", "ewb_last_error", "ewb_ctx_create", "ewb_ctx_destroy",
+    "ewb_abi_version", "ewb_last_error", "ewb_launch_count", "ewb_ctx_create", "ewb_ctx_destroy",
     "ewb_ctx_counts", "ewb_static_rowsums", "ewb_static_tu", "ewb_assemble_tu",
     "ewb_assemble_system", "ewb_ctx_flags", "ewb_apply_bcs", "ewb_blockdiag_inverse",
     "ewb_gemv_batched", "ewb_gmres_workspace_bytes", "ewb_gmres",
@@ -41,7 +41,7 @@ class NativeError(RuntimeError):
 
 class GmresResult(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("n_hist", ctypes.c_int32),
-                ("converged", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("converged", ctypes.c_int32), ("matvecs", ctypes.c_int32),
                 ("init_residual", ctypes.c_double), ("final_residual", ctypes.c_double)]
 
 
@@ -55,6 +55,7 @@ D = ctypes.c_double
 _SIGS = {
     "ewb_abi_version": (I32, []),
     "ewb_last_error": (ctypes.c_char_p, []),
+    "ewb_launch_count": (I64, []),
     "ewb_ctx_create": (I32, [P, P, P, P, P, I64, D, D, D, P, P, P, P, P, P, ctypes.POINTER(P)]),
     "ewb_ctx_destroy": (I32, [P]),
     "ewb_ctx_counts": (I32, [P, P]),

@@ -664,10 +664,10 @@ cudaError_t setup_context(Context& c, const double* centroids, const double* nor
   g.yfar = yfar;
   g.ymid = ymid;
   g.self_pts = selfp;
-  k_field_points<<<blocks_for(n, 128), 128, 0, s>>>(g, rules + rule_off[0], rules + rule_off[1],
+  EWB_NOTE k_field_points<<<blocks_for(n, 128), 128, 0, s>>>(g, rules + rule_off[0], rules + rule_off[1],
                                                     yfar, ymid);
-  k_self_rule<<<blocks_for((long long)n * 48, 128), 128, 0, s>>>(g, gl, gl + 16, selfp);
-  k_near_count<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_cnt, far_cnt, mid_cnt);
+  EWB_NOTE k_self_rule<<<blocks_for((long long)n * 48, 128), 128, 0, s>>>(g, gl, gl + 16, selfp);
+  EWB_NOTE k_near_count<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_cnt, far_cnt, mid_cnt);
   err = cudaGetLastError();
   if (err) return err;
   std::vector<int> cnt(n);
@@ -692,7 +692,7 @@ cudaError_t setup_context(Context& c, const double* centroids, const double* nor
   if (err) return err;
   cudaMemcpyAsync(near_ptr, ptr.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, s);
   g.near_ptr = near_ptr; g.near_j = near_j; g.near_row = near_row; g.near_lvl = near_lvl;
-  k_near_fill<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_ptr, near_j, near_row,
+  EWB_NOTE k_near_fill<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_ptr, near_j, near_row,
                                                                  near_lvl);
   // near level census
   std::vector<int> lv(c.n_near);
@@ -722,22 +722,22 @@ cudaError_t launch_static_pass(Context& c, double* t_out, double* u_out, cudaStr
   const int n = c.n_e;
   long long warps = (long long)n * c.n_tiles;
   if (t_out) {
-    k_farmid<false, OUT_TU | OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+    EWB_NOTE k_farmid<false, OUT_TU | OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
     if (c.n_near)
-      k_near<false, OUT_TU | OUT_ROWSUM><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(
+      EWB_NOTE k_near<false, OUT_TU | OUT_ROWSUM><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(
           c.g, ph, o, c.n_near);
   } else {
-    k_farmid<false, OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+    EWB_NOTE k_farmid<false, OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
     if (c.n_near)
-      k_near<false, OUT_ROWSUM><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(
+      EWB_NOTE k_near<false, OUT_ROWSUM><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(
           c.g, ph, o, c.n_near);
   }
-  k_self_static<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, c.u_sta_self,
+  EWB_NOTE k_self_static<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, c.u_sta_self,
                                                                    c.t_sta_self);
-  k_rowsum_finalize<<<blocks_for((long long)n * 9, 128), 128, 0, s>>>(
+  EWB_NOTE k_rowsum_finalize<<<blocks_for((long long)n * 9, 128), 128, 0, s>>>(
       c.g, c.spart, c.snear, c.t_sta_self, c.rowsums, c.diag_base, c.n_tiles);
   if (t_out)
-    k_static_diag<<<blocks_for((long long)n * 9, 128), 128, 0, s>>>(n, c.rowsums, c.u_sta_self,
+    EWB_NOTE k_static_diag<<<blocks_for((long long)n * 9, 128), 128, 0, s>>>(n, c.rowsums, c.u_sta_self,
                                                                     t_out, u_out);
   return cudaGetLastError();
 }
@@ -749,11 +749,11 @@ cudaError_t launch_assemble_tu(Context& c, double ore, double oim, cplx* T, cplx
   o.T = T; o.U = U; o.flags = c.flags;
   const int n = c.n_e;
   long long warps = (long long)n * c.n_tiles;
-  k_farmid<true, OUT_TU><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+  EWB_NOTE k_farmid<true, OUT_TU><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
   if (c.n_near)
-    k_near<true, OUT_TU><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
+    EWB_NOTE k_near<true, OUT_TU><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
                                                                                  c.n_near);
-  k_self_dyn<OUT_TU><<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, o, c.diag_base,
+  EWB_NOTE k_self_dyn<OUT_TU><<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, o, c.diag_base,
                                                                        c.n_tiles);
   return cudaGetLastError();
 }
@@ -767,25 +767,25 @@ cudaError_t launch_assemble_system(Context& c, double ore, double oim, const uin
   o.bpart = c.bpart; o.bnear = c.bnear; o.flags = c.flags;
   const int n = c.n_e;
   long long warps = (long long)n * c.n_tiles;
-  k_farmid<true, OUT_SYS><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+  EWB_NOTE k_farmid<true, OUT_SYS><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
   if (c.n_near)
-    k_near<true, OUT_SYS><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
+    EWB_NOTE k_near<true, OUT_SYS><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
                                                                                    c.n_near);
-  k_self_dyn<OUT_SYS><<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, o, c.diag_base,
+  EWB_NOTE k_self_dyn<OUT_SYS><<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, o, c.diag_base,
                                                                         c.n_tiles);
   return cudaGetLastError();
 }
 
 cudaError_t launch_apply_bcs(const cplx* T, const cplx* U, const uint8_t* kinds, const cplx* p,
                              long long n, cplx* A, cplx* b, cudaStream_t s) {
-  k_apply_bcs_cols<<<blocks_for(n * n, 256), 256, 0, s>>>(T, U, kinds, n, A);
-  k_apply_bcs_rhs<<<blocks_for(n * 32, 128), 128, 0, s>>>(T, U, kinds, p, n, b);
+  EWB_NOTE k_apply_bcs_cols<<<blocks_for(n * n, 256), 256, 0, s>>>(T, U, kinds, n, A);
+  EWB_NOTE k_apply_bcs_rhs<<<blocks_for(n * 32, 128), 128, 0, s>>>(T, U, kinds, p, n, b);
   return cudaGetLastError();
 }
 
 cudaError_t launch_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int* singular,
                                      cudaStream_t s) {
-  k_blockdiag_inverse<<<blocks_for(n / 3, 128), 128, 0, s>>>(A, n, pinv, singular);
+  EWB_NOTE k_blockdiag_inverse<<<blocks_for(n / 3, 128), 128, 0, s>>>(A, n, pinv, singular);
   return cudaGetLastError();
 }
 

@@ -2,6 +2,7 @@
 // the thread-local error string live here; kernels live in the other files.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -23,6 +24,9 @@ struct ewb_ctx {
 };
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void ewb::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -44,6 +48,8 @@ extern "C" {
 int ewb_abi_version(void) { return EWB_ABI_VERSION; }
 
 const char* ewb_last_error(void) { return g_err.c_str(); }
+
+int64_t ewb_launch_count(void) { return g_launches.load(); }
 
 int ewb_ctx_create(const double* centroids, const double* normals, const double* areas,
                    const double* diameters, const double* corners, int64_t n_elements,

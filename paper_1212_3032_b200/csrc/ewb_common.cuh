@@ -22,6 +22,12 @@
 
 namespace ewb {
 
+// Every kernel launch of the library is counted (ewb_launch_count) so the
+// benchmark can report exactly how many of OUR kernels ran in its timed
+// region.  Usage:  EWB_NOTE kernel<<<...>>>(...);
+void note_launch();
+#define EWB_NOTE ::ewb::note_launch(),
+
 constexpr double kSeriesSwitch = 0.35;   // kernels.py:36 (strict <)
 constexpr double kFarRatio = 4.0;        // quadrature.py:206 far_threshold
 constexpr double kNearRatio = 1.5;       // quadrature.py:207 near_threshold

@@ -175,9 +175,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
   if (nb == 0.0) {  // linsolve.py:136-140
     for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
     if (tid == 0) { a.out->iterations = 0; a.out->init_res = 0; a.out->final_res = 0;
-                    a.out->n_hist = 0; a.out->converged = 1; }
+                    a.out->n_hist = 0; a.out->converged = 1; a.out->matvecs = 0; }
     return;
   }
+  int n_mv = 0;
   // r = b - A x0  (skipped when x0 is all zero: linsolve.py:144)
   double anyv[1] = {0.0};
   if (a.has_x0)
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
   grid_sum(grid, R, anyv);
   if (anyv[0] > 0.0) {
     matvec_grid<4, 1>(a.A, n, a.x, a.w);
+    ++n_mv;
     grid.sync();
     for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
   } else {
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
       }
       grid.sync();
       matvec_grid<4, 1>(a.A, n, a.z, a.w);
+      ++n_mv;
       grid.sync();
       // MGS, fused: partial <v_0, w>
       double dv[2] = {0.0, 0.0};
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
     grid.sync();
     // true residual (linsolve.py:200-201)
     matvec_grid<4, 1>(a.A, n, a.x, a.w);
+    ++n_mv;
     grid.sync();
     double q[1] = {0.0};
     for (long long k = tid; k < n; k += nth) {
@@ -346,6 +350,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
     a.out->final_res = res;
     a.out->converged = res <= a.tol;
     a.out->n_hist = n_hist;
+    a.out->matvecs = n_mv;
   }
 }
 
@@ -530,6 +535,7 @@ int solver_grid_blocks() {
 cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
+  note_launch();
   return cudaLaunchCooperativeKernel((const void*)k_gmres, dim3(G), dim3(kSolveThreads), params, 0,
                                      s);
 }
@@ -537,6 +543,7 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
+  note_launch();
   return cudaLaunchCooperativeKernel((const void*)k_sem, dim3(G), dim3(kSolveThreads), params, 0, s);
 }
 
@@ -550,7 +557,7 @@ cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long
   long long cap = (long long)sms * 4 / (batch > 0 ? batch : 1);
   if (cap < 1) cap = 1;
   if (blocks > cap) blocks = cap;
-  k_gemv_batched<4><<<dim3((unsigned)blocks, batch), 512, 0, s>>>(A, x, y, n, batch);
+  EWB_NOTE k_gemv_batched<4><<<dim3((unsigned)blocks, batch), 512, 0, s>>>(A, x, y, n, batch);
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ struct GmresOut {
   int iterations;
   int n_hist;
   int converged;
-  int pad;
+  int matvecs;   // dense passes over A (iterations + restarts + r0)
   double init_res;
   double final_res;
 };

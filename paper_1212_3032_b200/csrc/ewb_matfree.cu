@@ -301,10 +301,10 @@ template <int K, bool USE_U>
 static cudaError_t mf_launch(Context& c, Phys<true> ph, MfArgs m, cudaStream_t s) {
   const int n = c.n_e;
   dim3 grid((n + 127) / 128, m.nchunk);
-  k_mf_farmid<K, USE_U><<<grid, 128, 0, s>>>(c.g, ph, m);
+  EWB_NOTE k_mf_farmid<K, USE_U><<<grid, 128, 0, s>>>(c.g, ph, m);
   if (c.n_near)
-    k_mf_near<K, USE_U><<<(c.n_near * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m, c.n_near);
-  k_mf_self<K, USE_U><<<(n * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m);
+    EWB_NOTE k_mf_near<K, USE_U><<<(c.n_near * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m, c.n_near);
+  EWB_NOTE k_mf_self<K, USE_U><<<(n * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m);
   return cudaGetLastError();
 }
 
@@ -490,7 +490,7 @@ cudaError_t launch_pair_blocks(const double* x, long long P, const double* tri, 
   cudaError_t e = upload_series(s);
   if (e) return e;
   dim3 grid((unsigned)((P * M + 127) / 128), F);
-  k_pair_blocks<<<grid, 128, 0, s>>>(x, P, tri, M, fcs_dev, b7, w7, u, t);
+  EWB_NOTE k_pair_blocks<<<grid, 128, 0, s>>>(x, P, tri, M, fcs_dev, b7, w7, u, t);
   return cudaGetLastError();
 }
 
@@ -502,9 +502,9 @@ cudaError_t launch_pair_reduce(const double* x, long long P, const double* tri, 
   if (e) return e;
   long long chunk = (M + nchunk - 1) / nchunk;
   dim3 grid((unsigned)((P + 127) / 128), F, nchunk);
-  k_pair_reduce<<<grid, 128, 0, s>>>(x, P, tri, M, xv, fcs_dev, b7, w7, chunk, part);
+  EWB_NOTE k_pair_reduce<<<grid, 128, 0, s>>>(x, P, tri, M, xv, fcs_dev, b7, w7, chunk, part);
   long long tot = (long long)F * P * 6;
-  k_pair_reduce_final<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, nchunk, F, P, yu, yt);
+  EWB_NOTE k_pair_reduce_final<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, nchunk, F, P, yu, yt);
   return cudaGetLastError();
 }
 
@@ -537,12 +537,12 @@ cudaError_t fp64_peak_probe(long long iters, int blocks_per_sm, double* tflops, 
   if (e) return e;
   const int threads = 256;
   const int blocks = sms * blocks_per_sm;
-  k_dfma_probe<<<blocks, threads, 0, s>>>(iters / 8 + 1, sink);  // warm-up
+  EWB_NOTE k_dfma_probe<<<blocks, threads, 0, s>>>(iters / 8 + 1, sink);  // warm-up
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
-  k_dfma_probe<<<blocks, threads, 0, s>>>(iters, sink);
+  EWB_NOTE k_dfma_probe<<<blocks, threads, 0, s>>>(iters, sink);
   cudaEventRecord(e1, s);
   e = cudaEventSynchronize(e1);
   float t = 0.f;

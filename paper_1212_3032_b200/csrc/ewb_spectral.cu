@@ -63,7 +63,7 @@ cudaError_t launch_window_idft(const cplx* half, long long n_half, long long D, 
   const int N = (int)(2 * (n_half - 1));
   int threads = N < 256 ? ((N + 31) / 32) * 32 : 256;
   size_t smem = (size_t)2 * N * sizeof(cplx) + 2 * 8 * sizeof(double) * 8;
-  k_window_idft<<<(unsigned)D, threads, smem, s>>>(half, n_half, D, win, tw, eta_dt, out, residue);
+  EWB_NOTE k_window_idft<<<(unsigned)D, threads, smem, s>>>(half, n_half, D, win, tw, eta_dt, out, residue);
   return cudaGetLastError();
 }
 

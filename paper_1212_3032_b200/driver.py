@@ -3,19 +3,19 @@
 ``run_sweep(cfg) -> SweepResult`` keeps the reference's sequencing exactly
 (ascending k, SEM history pushed after each solve, probes, NaN poisoning of
 every history when any solve fails, manifest) while every per-frequency
-array stays in HBM:
+array stays in HBM.  The device loop lives in :class:`DeviceSweep`:
 
     per k:  ewb_assemble_system   (assembly + BCs + b + P^{-1}, no T/U)
             ewb_sem_guess         (if history: Y = A X, QR, x0)
             ewb_gmres             (the whole restarted solve, one launch)
-            one 64-byte read-back (flags + iteration count + residuals)
+            one small read-back   (fault flags + iteration count + residuals)
     end:    ewb_window_idft       (conjugate fill + window + IDFT for the
                                    probe columns, or all DOFs)
 
 With SEM off and torch.distributed initialised with world > 1, the
 frequencies are dealt round-robin to the ranks (the reference's fork pool,
-driver.py:113-122, as replicas over NVLink-connected GPUs) and the
-per-frequency results are all-gathered once at the end.
+driver.py:113-122, as replicas on separate GPUs) and the per-frequency
+results are all-gathered once at the end.
 """
 
 from __future__ import annotations
@@ -32,7 +32,7 @@ import numpy as np
 from . import _lib
 from .assembly import DIRICHLET, NEUMANN, Assembler
 from .config import SweepConfig
-from .linsolve import SolveStats, _SEM_WS, _WS, gmres_device, sem_device
+from .linsolve import SolveStats, _WS, _fill_stats, block_diag_precond, gmres_device, sem_device
 from .transform import (check_residue, eta_from_kappa, forward_mft, frequency_grid,
                         windowed_inverse_device)
 
@@ -75,9 +75,9 @@ def _dist():
 
 
 def gather_frequency_results(local: dict, n_freq: int, width: int, dist=None):
-    """All-gather {k: (values (width,) complex, stats tuple)} from every rank.
+    """All-gather {k: (values (width,) complex, stats 6-tuple)} from every rank.
 
-    Returns (values (n_freq, width) complex ndarray, stats list indexed by k).
+    Returns (values (n_freq, width) complex ndarray, meta (n_freq, 6)).
     Host-side bookkeeping, exercised with the gloo backend in the tests.
     """
     import torch
@@ -99,7 +99,7 @@ def gather_frequency_results(local: dict, n_freq: int, width: int, dist=None):
         dist.all_gather(parts, t)
         total = sum(p.cpu().numpy() for p in parts)
         w2 = 2 * width
-        vals = total[:, :w2].copy().view(complex)
+        vals = np.ascontiguousarray(total[:, :w2]).view(complex)
         meta = total[:, w2:w2 + 6]
         owned = total[:, -1]
     if not np.all(owned == 1):
@@ -107,134 +107,186 @@ def gather_frequency_results(local: dict, n_freq: int, width: int, dist=None):
     return vals, meta
 
 
+class DeviceSweep:
+    """The per-frequency loop with every array resident in HBM.
+
+    Construction uploads the per-run inputs (BC kinds, the prescribed
+    spectra of every frequency); ``run()`` performs the sweep and returns
+    device tensors.  ``timing=True`` brackets the assembly and solver
+    launches of every frequency with CUDA events (phase split for the
+    roofline report).
+    """
+
+    def __init__(self, cfg: SweepConfig, assembler: Assembler | None = None,
+                 frequencies: list | None = None):
+        import torch
+
+        _lib.require_cuda()
+        self.cfg = cfg
+        self.eta = eta_from_kappa(cfg.kappa, cfg.period)
+        self.omegas = frequency_grid(cfg.period, cfg.n_omega, self.eta)
+        self.n_freq = len(self.omegas)
+        self.h2d_bytes = 0
+        spectra = np.stack([forward_mft(s, cfg.period, cfg.n_omega, self.eta).values[:self.n_freq]
+                            for s in cfg.signals])
+        self.asm = assembler or Assembler(cfg.mesh, cfg.material)
+        if assembler is None:
+            m = cfg.mesh
+            self.h2d_bytes += 8 * (m.centroids.size + m.normals.size + m.areas.size
+                                   + m.diameters.size + 9 * m.n_elements)
+        n = cfg.mesh.n_dofs
+        self.n = n
+        self.kinds = np.ascontiguousarray(cfg.bcs.flat_kind(), dtype=np.uint8)
+        sig = cfg.bcs.flat_signal().astype(np.int64)
+        spec_t = np.ascontiguousarray(spectra.T)                    # (n_freq, n_signals)
+        spec_dev = torch.from_numpy(spec_t).cuda()
+        sig_dev = torch.from_numpy(sig).cuda()
+        self.h2d_bytes += spec_t.nbytes + sig.nbytes + self.kinds.nbytes
+        self.P = spec_dev[:, sig_dev].contiguous()                  # (n_freq, n) prescribed
+        self.frequencies = list(range(self.n_freq)) if frequencies is None else list(frequencies)
+        self.sol = torch.zeros((self.n_freq, n), dtype=torch.complex128, device="cuda")
+        self.x = torch.zeros(n, dtype=torch.complex128, device="cuda")
+        self.hist = torch.zeros((cfg.sem_depth, n), dtype=torch.complex128, device="cuda")
+        self.system = None
+        self.d2h_bytes = 0
+
+    def run(self, timing: bool = False):
+        """Sweep the owned frequencies; returns {k: SolveStats}."""
+        import torch
+
+        cfg = self.cfg
+        asm = self.asm
+        stats = {}
+        ev = []
+        n_hist = 0
+        K = cfg.sem_depth
+        self.hist.zero_()
+        self.phase = {"assembly_ms": 0.0, "solve_ms": 0.0, "matvecs": 0, "solves": 0}
+        for k in self.frequencies:
+            omega = complex(self.omegas[k])
+            try:
+                if timing:
+                    e_a = torch.cuda.Event(enable_timing=True)
+                    e_a.record()
+                sysm = asm.assemble_system(omega, cfg.bcs, self.P[k],
+                                           out=self.system if omega != 0 else None, check=False)
+                if sysm.pinv is None:   # omega == 0: static path (kappa = 0 sweeps)
+                    sysm.pinv = block_diag_precond(sysm.A).pinv
+                else:
+                    self.system = sysm
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                use_sem = cfg.sem_enabled and n_hist > 0
+                if use_sem:
+                    sem_device(sysm.A, sysm.b, self.hist[:n_hist], 1e-10, self.x)
+                st = SolveStats()
+                gmres_device(sysm.A, sysm.b, self.x, use_sem, cfg.tol, cfg.restart, cfg.maxiter,
+                             sysm.pinv, stats=st, sync=False)
+                e1.record()
+                nf, sg = ctypes.c_int32(), ctypes.c_int32()
+                _lib.check(asm._lib.ewb_ctx_flags(asm.ctx, ctypes.byref(nf), ctypes.byref(sg),
+                                                  _lib.stream_handle()))
+                if nf.value:
+                    raise FloatingPointError(f"non-finite entries assembled at omega = {omega}")
+                if sg.value:
+                    log.warning("%d singular 3x3 diagonal blocks; identity fallback", sg.value)
+                _fill_stats(st, _WS.result(), _WS.hist_buf(1))
+                self.d2h_bytes += 8 + 32 + 8 * len(st.residual_history)
+            except SweepError:
+                raise
+            except Exception as exc:
+                raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
+            st.k = k
+            st.omega = omega
+            stats[k] = st
+            ev.append((k, e_a if timing else None, e0, e1, use_sem))
+            self.sol[k] = self.x
+            if cfg.sem_enabled:
+                self.hist[1:] = self.hist[:-1].clone()
+                self.hist[0] = self.x
+                n_hist = min(n_hist + 1, K)
+            if not st.converged:
+                log.warning("GMRES stalled at residual %.3e after %d iterations",
+                            st.final_residual, st.iterations)
+        torch.cuda.synchronize()
+        for k, ea, e0, e1, use_sem in ev:
+            stats[k].seconds = e0.elapsed_time(e1) * 1e-3
+            if timing:
+                self.phase["assembly_ms"] += ea.elapsed_time(e0)
+                self.phase["solve_ms"] += e0.elapsed_time(e1)
+            # passes over A: the solver's own count + SEM's single Y = A X pass
+            self.phase["matvecs"] += stats[k].matvecs + (1 if use_sem else 0)
+            self.phase["solves"] += 1
+        return stats
+
+    def probe_half(self, probes):
+        import torch
+
+        cols = []
+        for p in probes:
+            unknown = (self.kinds[p.dof] == NEUMANN) if p.quantity == "displacement" else \
+                (self.kinds[p.dof] == DIRICHLET)
+            cols.append(self.sol[:, p.dof] if unknown else self.P[:, p.dof])
+        if not cols:
+            return torch.zeros((self.n_freq, 0), dtype=torch.complex128, device="cuda")
+        return torch.stack(cols, dim=1).contiguous()
+
+    def displacement_field(self):
+        """u for every DOF at every frequency: (n_freq, n) device."""
+        import torch
+
+        neu = torch.from_numpy(self.kinds == NEUMANN).cuda()
+        return torch.where(neu[None, :], self.sol, self.P)
+
+
 def run_sweep(cfg: SweepConfig, full_field: bool = False, assembler: Assembler | None = None,
-              distributed: bool = True) -> SweepResult:
+              distributed: bool = True, _sweep_out: list | None = None) -> SweepResult:
     """Run the transient analysis described by ``cfg`` on the GPU."""
     import torch
 
     t_begin = time.perf_counter()
-    _lib.require_cuda()
-    eta = eta_from_kappa(cfg.kappa, cfg.period)
-    omegas = frequency_grid(cfg.period, cfg.n_omega, eta)
-    n_freq = len(omegas)
-    log.info("sweep: %d elements, %d frequencies, eta=%.4g 1/s", cfg.mesh.n_elements, n_freq, eta)
-    spectra = np.stack([forward_mft(s, cfg.period, cfg.n_omega, eta).values[:n_freq]
-                        for s in cfg.signals])
-    asm = assembler or Assembler(cfg.mesh, cfg.material)
-    n = cfg.mesh.n_dofs
-    kinds = np.ascontiguousarray(cfg.bcs.flat_kind(), dtype=np.uint8)
-    sig = cfg.bcs.flat_signal()
-    # prescribed values for every k, on the device: P[k, d] = spectra[sig[d], k]
-    spec_dev = torch.from_numpy(np.ascontiguousarray(spectra.T)).cuda()      # (n_freq, n_sig)
-    P = spec_dev[:, torch.from_numpy(sig.astype(np.int64)).cuda()].contiguous()  # (n_freq, n)
-
     dist = _dist() if distributed else None
     world = dist.get_world_size() if dist else 1
     rank = dist.get_rank() if dist else 0
     parallel = world > 1 and not cfg.sem_enabled
     if world > 1 and cfg.sem_enabled:
         log.info("solution extrapolation is sequential; every rank runs the whole sweep")
-    my_k = shard_frequencies(n_freq, rank, world) if parallel else list(range(n_freq))
-
-    sol = torch.zeros((n_freq, n), dtype=torch.complex128, device="cuda")
-    x = torch.zeros(n, dtype=torch.complex128, device="cuda")
-    K = cfg.sem_depth
-    hist = torch.zeros((K, n), dtype=torch.complex128, device="cuda")
-    n_hist = 0
-    system = None
-    stats_local = {}
-    res_host = torch.empty(64, dtype=torch.uint8).pin_memory()
-    ev = []
-    for k in my_k:
-        omega = complex(omegas[k])
-        try:
-            system = asm.assemble_system(omega, cfg.bcs, P[k], out=system if omega != 0 else None,
-                                         check=False)
-            if system.pinv is None:   # omega == 0 static path (kappa = 0)
-                from .linsolve import block_diag_precond
-
-                system.pinv = block_diag_precond(system.A).pinv
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            use_sem = cfg.sem_enabled and n_hist > 0
-            if use_sem:
-                sem_device(system.A, system.b, hist[:n_hist], 1e-10, x)
-            st = SolveStats()
-            gmres_device(system.A, system.b, x, use_sem, cfg.tol, cfg.restart, cfg.maxiter,
-                         system.pinv, stats=st, sync=False)
-            e1.record()
-            # one read-back per frequency: fault flags + solver record
-            nf = ctypes.c_int32()
-            sg = ctypes.c_int32()
-            _lib.check(asm._lib.ewb_ctx_flags(asm.ctx, ctypes.byref(nf), ctypes.byref(sg),
-                                              _lib.stream_handle()))
-            if nf.value:
-                raise FloatingPointError(f"non-finite entries assembled at omega = {omega}")
-            if sg.value:
-                log.warning("%d singular 3x3 diagonal blocks; identity fallback", sg.value)
-            from .linsolve import _fill_stats
-
-            _fill_stats(st, _WS.result(), _WS.hist_buf(1))
-        except SweepError:
-            raise
-        except Exception as exc:
-            raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
-        st.k = k
-        st.omega = omega
-        stats_local[k] = st
-        ev.append((k, e0, e1))
-        sol[k] = x
-        if cfg.sem_enabled:
-            hist[1:] = hist[:-1].clone()
-            hist[0] = x
-            n_hist = min(n_hist + 1, K)
-        if not st.converged:
-            log.warning("GMRES stalled at residual %.3e after %d iterations",
-                        st.final_residual, st.iterations)
-        log.debug("k=%3d iters=%4d res=%.2e", k, st.iterations, st.final_residual)
-    torch.cuda.synchronize()
-    for k, e0, e1 in ev:
-        stats_local[k].seconds = e0.elapsed_time(e1) * 1e-3
-
-    # probe spectra: u = a (Neumann) else prescribed; t = a (Dirichlet) else prescribed
+    eta = eta_from_kappa(cfg.kappa, cfg.period)
+    n_freq = cfg.n_omega // 2 + 1
+    mine = shard_frequencies(n_freq, rank, world) if parallel else None
+    ds = DeviceSweep(cfg, assembler, mine)
+    log.info("sweep: %d elements, %d frequencies, eta=%.4g 1/s", cfg.mesh.n_elements, n_freq, eta)
+    stats_local = ds.run()
     probes = list(cfg.probes)
-    cols = []
-    for p in probes:
-        unknown = (kinds[p.dof] == NEUMANN) if p.quantity == "displacement" else \
-            (kinds[p.dof] == DIRICHLET)
-        cols.append((p.dof, bool(unknown)))
-    probe_half = torch.stack([sol[:, d] if unk else P[:, d] for d, unk in cols], dim=1) \
-        if cols else torch.zeros((n_freq, 0), dtype=torch.complex128, device="cuda")
-
+    probe_half = ds.probe_half(probes)
     stats_list = [None] * n_freq
     if parallel:
         local = {k: (probe_half[k].cpu().numpy(),
                      (stats_local[k].iterations, stats_local[k].init_residual,
                       stats_local[k].final_residual, stats_local[k].seconds,
-                      float(stats_local[k].converged), 0.0)) for k in my_k}
+                      float(stats_local[k].converged), 0.0)) for k in ds.frequencies}
         vals, meta = gather_frequency_results(local, n_freq, len(probes), dist)
         probe_half = torch.from_numpy(vals).cuda()
         for k in range(n_freq):
             it, i0, f0, sec, conv, _ = meta[k]
-            stats_list[k] = SolveStats(k=k, omega=complex(omegas[k]), iterations=int(it),
+            stats_list[k] = SolveStats(k=k, omega=complex(ds.omegas[k]), iterations=int(it),
                                        init_residual=float(i0), final_residual=float(f0),
                                        seconds=float(sec), converged=bool(conv))
     else:
-        for k in my_k:
+        for k in ds.frequencies:
             stats_list[k] = stats_local[k]
-
     failed = [s.k for s in stats_list if not s.converged]
     if failed:
         log.error("non-converged frequencies: %s", failed)
-    dt = cfg.period / cfg.n_omega
-    times = np.arange(cfg.n_omega) * dt
+    times = np.arange(cfg.n_omega) * (cfg.period / cfg.n_omega)
     histories, half_spectra = {}, {}
     if probes:
         series, residue = windowed_inverse_device(probe_half, cfg.window, eta, cfg.period)
         series_h = series.cpu().numpy()
         residue_h = residue.cpu().numpy()
         half_h = probe_half.cpu().numpy()
+        ds.d2h_bytes += series_h.nbytes + residue_h.nbytes + half_h.nbytes
         for i, p in enumerate(probes):
             half_spectra[p.name] = half_h[:, i].copy()
             check_residue(float(residue_h[i]))
@@ -242,11 +294,11 @@ def run_sweep(cfg: SweepConfig, full_field: bool = False, assembler: Assembler |
             histories[p.name] = np.full_like(s, np.nan) if failed else s
     field_hist = None
     if full_field:
-        # u for every DOF (displacement field), all on the device
-        neu = torch.from_numpy(kinds == NEUMANN).cuda()
-        u_half = torch.where(neu[None, :], sol, P)
-        field_hist, _ = windowed_inverse_device(u_half, cfg.window, eta, cfg.period)
+        field_hist, _ = windowed_inverse_device(ds.displacement_field(), cfg.window, eta,
+                                                cfg.period)
     manifest = build_manifest(cfg, eta, time.perf_counter() - t_begin, failed)
+    if _sweep_out is not None:
+        _sweep_out.append(ds)
     return SweepResult(times=times, histories=histories, half_spectra=half_spectra,
                        stats=stats_list, manifest=manifest, failed_frequencies=failed,
                        full_field=field_hist)

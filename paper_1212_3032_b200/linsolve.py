@@ -46,6 +46,7 @@ class SolveStats:
     seconds: float = 0.0
     converged: bool = True
     residual_history: list = field(default_factory=list, repr=False)
+    matvecs: int = 0   # device extra: passes over A inside the solve
 
     CSV_HEADER = "k,omega_re,omega_im,iterations,init_residual,final_residual,seconds"
 
@@ -188,6 +189,7 @@ def _fill_stats(st: SolveStats, res, hist):
     st.init_residual = out.init_residual
     st.final_residual = out.final_residual
     st.converged = bool(out.converged)
+    st.matvecs = out.matvecs
     nh = min(out.n_hist, hist.numel())
     st.residual_history = hist[:nh].cpu().tolist() if nh else []
     return st

@@ -305,6 +305,36 @@ def section_cfg1_sweep():
     save("cfg1_sweep", **out)
 
 
+def section_cfg1_solutions():
+    """cfg1 per-frequency solutions a_k, (b_k norm) and SEM initial residuals.
+
+    The loop restates run_sweep's sequential branch (driver.py:123-153) with
+    the reference's own functions so the per-k solution vectors can be kept:
+    a GPU solve fed the reference's history must reproduce each count.
+    """
+    cfg = cfg1_reference_config()
+    eta = R_tr.eta_from_kappa(cfg.kappa, cfg.period)
+    omegas = R_tr.frequency_grid(cfg.period, cfg.n_omega, eta)
+    spectra = np.stack([R_tr.forward_mft(s, cfg.period, cfg.n_omega, eta).values[:len(omegas)]
+                        for s in cfg.signals])
+    asm = R_asm.Assembler(cfg.mesh, cfg.material)
+    asm.static_offdiag_rowsums()
+    hist = R_lin.SolutionHistory(cfg.sem_depth)
+    xs, its, init = [], [], []
+    for k in range(len(omegas)):
+        t, u = asm.assemble_tu(omegas[k])
+        p = spectra[cfg.bcs.flat_signal(), k]
+        sysm = R_asm.apply_bcs(t, u, cfg.bcs, p)
+        x0 = R_lin.sem_initial_guess(hist, sysm.A, sysm.b) if len(hist) else None
+        x, st = R_lin.gmres(sysm.A, sysm.b, x0=x0, tol=cfg.tol, restart=cfg.restart,
+                            maxiter=cfg.maxiter, precond=R_lin.block_diag_precond(sysm.A))
+        hist.push(x)
+        xs.append(x)
+        its.append(st.iterations)
+        init.append(st.init_residual)
+    save("cfg1_solutions", x=np.array(xs), its=np.array(its), init=np.array(init))
+
+
 def section_cfg2_head():
     """cfg2 sphere (ico4 cavity, 15360 DOF): first 3 frequencies of the sweep.
 
@@ -356,6 +386,7 @@ def section_cfg2_head():
 SECTIONS = dict(small=section_small, cfg1_rows=section_cfg1_rows, tiers=section_tiers,
                 linsolve=section_linsolve, transform=section_transform,
                 sweeps=section_sweeps, cfg1_sweep=section_cfg1_sweep,
+                cfg1_solutions=section_cfg1_solutions,
                 cfg2_head=section_cfg2_head)
 
 if __name__ == "__main__":
