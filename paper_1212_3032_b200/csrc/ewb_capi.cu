@@ -191,7 +191,8 @@ int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart) {
   int64_t cpl = 16;
   int64_t G = ewb::solver_grid_blocks();
   return cpl * (3 * n + (int64_t)(restart + 1) * n +
-                (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart) +
+                2 * (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart +
+                2 * G * (2 * ewb::kMaxRestart + 2)) +
          8 * 2 * G * 16 + 256 * 8;
 }
 
@@ -218,7 +219,14 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   g.z = base + 2 * n;
   g.V = base + 3 * n;
   g.H = g.V + (int64_t)(restart + 1) * n;
-  g.partial = (double*)(g.H + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart);
+  g.Gram = g.H + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
+  g.dpart = g.Gram + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
+  g.partial = (double*)(g.dpart + 2 * (int64_t)ewb::solver_grid_blocks() *
+                                      (2 * ewb::kMaxRestart + 2));
+  {
+    const char* env = getenv("EWB_GMRES_ORTHO");
+    g.ortho = env ? atoi(env) : 0;
+  }
   g.hist = hist;
   g.out = (ewb::GmresOut*)result;
   g.n = n;

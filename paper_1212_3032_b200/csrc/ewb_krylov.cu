@@ -130,6 +130,180 @@ __device__ void matvec_grid(const cplx* __restrict__ A, long long n, const cplx*
   }
 }
 
+// ---------------------------------------------------------------------
+// TMA (cp.async.bulk) matvec.  Row groups of kRR rows are dealt to CTAs
+// round-robin; each CTA streams its groups through a kNS-stage ring of
+// shared-memory tiles (kRR rows x kTC columns = 32 KB), one bulk copy per
+// row segment, completion tracked by a transaction-count mbarrier per
+// stage.  Thread t owns column t % kTC of every tile for kRR/2 rows; the
+// per-row sums are reduced across the CTA at the end of each row group.
+// Up to kNS x 32 KB = 192 KB per SM are in flight with no register cost.
+// ---------------------------------------------------------------------
+#ifndef EWB_RING_RR
+#define EWB_RING_RR 16
+#endif
+#ifndef EWB_RING_TC
+#define EWB_RING_TC 256
+#endif
+#ifndef EWB_RING_NS
+#define EWB_RING_NS 3
+#endif
+constexpr int kRR = EWB_RING_RR;
+constexpr int kTC = EWB_RING_TC;
+constexpr int kNS = EWB_RING_NS;
+constexpr int kStageElems = kRR * kTC;
+constexpr int kRingBytes = kNS * kStageElems * 16;
+constexpr int kSlices = kSolveThreads / kTC;     // row slices per tile
+constexpr int kRpt = kRR / kSlices;              // rows per thread
+static_assert(kSolveThreads % kTC == 0 && kRR % kSlices == 0, "tile geometry");
+
+struct Ring {
+  cplx* buf;            // dynamic shared memory, kNS stages
+  uint64_t* bar;        // kNS mbarriers (static shared)
+  unsigned pos;         // stages consumed so far by this CTA (uniform)
+  uint64_t policy;      // L2 cache policy for A
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void ring_init(Ring& R, bool evict_first) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNS; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&R.bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(R.policy));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(R.policy));
+  R.pos = 0;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cplx* A, long long n,
+                                           long long row0, int nrows, long long c0, int tc) {
+  const int b = pos % kNS;
+  const uint32_t bar = smem_u32(&R.bar[b]);
+  const uint32_t bytes = (uint32_t)(nrows * tc * 16);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  for (int r = 0; r < nrows; ++r) {
+    const uint32_t dst = smem_u32(R.buf + (size_t)b * kStageElems + r * kTC);
+    const cplx* src = A + (row0 + r) * n + c0;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(tc * 16), "r"(bar), "l"(R.policy)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void ring_wait(const Ring& R, unsigned pos) {
+  const uint32_t bar = smem_u32(&R.bar[pos % kNS]);
+  const uint32_t parity = (pos / kNS) & 1u;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// y[k] = A x[k] for K vectors (x, y: vector k at +k n), all CTAs cooperate;
+// the caller separates phases with grid.sync().
+template <int K>
+__device__ void matvec_tma(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
+                           cplx* y) {
+  __shared__ cplx s_red[kSolveWarps][kRpt][K];
+  const long long ngroups = (n + kRR - 1) / kRR;
+  const int ntile = (int)((n + kTC - 1) / kTC);
+  const long long mine = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long S = mine * ntile;
+  auto coords = [&](long long s, long long& row0, int& nrows, long long& c0, int& tc) {
+    const long long gi = s / ntile;
+    const int t = (int)(s % ntile);
+    row0 = (blockIdx.x + gi * gridDim.x) * kRR;
+    nrows = (int)min((long long)kRR, n - row0);
+    c0 = (long long)t * kTC;
+    tc = (int)min((long long)kTC, n - c0);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (long long s = 0; s < S && s < kNS; ++s) {
+      long long row0, c0;
+      int nrows, tc;
+      coords(s, row0, nrows, c0, tc);
+      ring_issue(R, R.pos + (unsigned)s, A, n, row0, nrows, c0, tc);
+    }
+  }
+  const int col = threadIdx.x % kTC, slice = threadIdx.x / kTC;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  cplx acc[kRpt][K];
+#pragma unroll
+  for (int r = 0; r < kRpt; ++r)
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
+  for (long long s = 0; s < S; ++s) {
+    long long row0, c0;
+    int nrows, tc;
+    coords(s, row0, nrows, c0, tc);
+    const unsigned pos = R.pos + (unsigned)s;
+    ring_wait(R, pos);
+    if (col < tc) {
+      cplx xv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) xv[k] = ldg(x + k * n + c0 + col);
+      const cplx* tile = R.buf + (size_t)(pos % kNS) * kStageElems;
+#pragma unroll
+      for (int r = 0; r < kRpt; ++r) {
+        const int row = slice * kRpt + r;
+        if (row < nrows) {
+          double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + col);
+          cplx av = {a2.x, a2.y};
+#pragma unroll
+          for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[k]);
+        }
+      }
+    }
+    __syncthreads();  // every consumer is done with this stage's buffer
+    if (threadIdx.x == 0 && s + kNS < S) {
+      long long r2, c2;
+      int n2, t2;
+      coords(s + kNS, r2, n2, c2, t2);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      ring_issue(R, pos + kNS, A, n, r2, n2, c2, t2);
+    }
+    if (c0 + tc >= n) {  // last tile of the row group: reduce and store
+#pragma unroll
+      for (int r = 0; r < kRpt; ++r)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          warp_sum(acc[r][k]);
+          if (lane == 0) s_red[wid][r][k] = acc[r][k];
+          acc[r][k] = {0.0, 0.0};
+        }
+      __syncthreads();
+      if (threadIdx.x < kRR * K) {
+        const int row = threadIdx.x / K, k = threadIdx.x % K;
+        const int h = row / kRpt, r = row % kRpt;
+        constexpr int wps = kSolveWarps / kSlices;  // warps per row slice
+        cplx sum = {0.0, 0.0};
+        for (int w = 0; w < wps; ++w) sum = sum + s_red[h * wps + w][r][k];
+        if (row < nrows) y[k * n + row0 + row] = sum;
+      }
+      __syncthreads();
+    }
+  }
+  R.pos += (unsigned)S;
+}
+
 // z = P^{-1} v  (3x3 blocks; identity when pinv == nullptr).  Grid-stride
 // over elements: thread e owns DOFs 3e..3e+2.
 __device__ __forceinline__ void precond_apply_elem(const cplx* pinv, long long e, const cplx* v,
@@ -157,8 +331,14 @@ struct GivensShared {
   cplx h[kMaxRestart + 1];
 };
 
-__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
+// Classic sequential MGS (one grid barrier per projection) — kept as the
+// GmresArgs::ortho == 1 variant for A/B parity checks.
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_mgs(GmresArgs a) {
   cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
+  ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
   __shared__ GivensShared gs;
   __shared__ cplx s_y[kMaxRestart];
   const long long n = a.n;
@@ -187,7 +367,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
     for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
   grid_sum(grid, R, anyv);
   if (anyv[0] > 0.0) {
-    matvec_grid<4, 1>(a.A, n, a.x, a.w);
+    matvec_tma<1>(ring, a.A, n, a.x, a.w);
     ++n_mv;
     grid.sync();
     for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
@@ -226,7 +406,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
         for (long long k = tid; k < n; k += nth) a.z[k] = vj[k];
       }
       grid.sync();
-      matvec_grid<4, 1>(a.A, n, a.z, a.w);
+      matvec_tma<1>(ring, a.A, n, a.z, a.w);
       ++n_mv;
       grid.sync();
       // MGS, fused: partial <v_0, w>
@@ -332,7 +512,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
     }
     grid.sync();
     // true residual (linsolve.py:200-201)
-    matvec_grid<4, 1>(a.A, n, a.x, a.w);
+    matvec_tma<1>(ring, a.A, n, a.x, a.w);
     ++n_mv;
     grid.sync();
     double q[1] = {0.0};
@@ -355,6 +535,275 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
 }
 
 // ---------------------------------------------------------------------
+// One-reduction MGS-GMRES (default).  The reference's MGS computes
+//   h_i = <v_i, w - sum_{l<i} h_l v_l> = d_i - sum_{l<i} <v_i, v_l> h_l,
+// d_i = <v_i, w>, i.e. h = (I + L)^{-1} d with L the strictly lower part of
+// the Gram matrix V^H V.  Row j of L (<v_j, v_l>, l < j) is reduced together
+// with d in ONE grid reduction, the unit-triangular solve runs redundantly
+// (and identically) in every CTA, and w -= h_0 v_0 -= h_1 v_1 ... (the MGS
+// update order) plus |w|^2 take the second reduction.  Same algorithm and
+// coefficients as MGS up to floating-point association — no approximation —
+// with 4 grid barriers per Arnoldi step instead of j + 5.
+// ---------------------------------------------------------------------
+constexpr int kMaxDots = 2 * kMaxRestart + 2;
+
+// CTA-partial dots over this CTA's DOF slice [k0, k1):
+//   t < nd        : <V_t, w>
+//   nd <= t < nd+ng: <v_j, V_{t-nd}>
+__device__ void slice_dots(const cplx* V, long long n, const cplx* w, int nd, int ng, int j,
+                           long long k0, long long k1, cplx* part) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t = wid; t < nd + ng; t += kSolveWarps) {
+    const cplx* p = t < nd ? V + (size_t)t * n : V + (size_t)j * n;
+    const cplx* q = t < nd ? w : V + (size_t)(t - nd) * n;
+    cplx s = {0.0, 0.0};
+    for (long long k = k0 + lane; k < k1; k += 32) cfma(s, conj(p[k]), q[k]);
+    warp_sum(s);
+    if (lane == 0) part[(size_t)blockIdx.x * kMaxDots + t] = s;
+  }
+}
+
+// Every CTA reduces the CTA partials in the same fixed order -> s_out.
+__device__ void reduce_slices(const cplx* part, int cnt, cplx* s_out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int t = wid; t < cnt; t += kSolveWarps) {
+    cplx s = {0.0, 0.0};
+    for (int b = lane; b < (int)gridDim.x; b += 32) s = s + part[(size_t)b * kMaxDots + t];
+    warp_sum(s);
+    if (lane == 0) s_out[t] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void precond_regs(const cplx* pinv, long long e, const cplx v[3],
+                                             cplx* z) {
+  const cplx* P = pinv + 9 * e;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    cplx s = P[3 * r] * v[0];
+    s = s + P[3 * r + 1] * v[1];
+    s = s + P[3 * r + 2] * v[2];
+    z[3 * e + r] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  __shared__ GivensShared gs;
+  __shared__ cplx s_y[kMaxRestart];
+  __shared__ cplx s_dots[kMaxDots];
+  __shared__ cplx s_h[kMaxRestart + 1];
+  __shared__ double s_est;
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
+  ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
+  const long long n = a.n;
+  const long long tid = gtid(), nth = gthreads();
+  const bool pc = a.pinv != nullptr;
+  const int ucnt = pc ? 3 : 1;
+  const long long nunits = pc ? n / 3 : n;
+  const long long k0 = (long long)blockIdx.x * n / gridDim.x;
+  const long long k1 = (long long)(blockIdx.x + 1) * n / gridDim.x;
+  GridRed R{a.partial, 0};
+  int dpar = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+
+  // ||b|| and "x0 has a nonzero entry", one reduction
+  double v2[2] = {0.0, 0.0};
+  for (long long k = tid; k < n; k += nth) {
+    v2[0] += abs2(a.b[k]);
+    if (a.has_x0) v2[1] += (a.x[k].re != 0.0 || a.x[k].im != 0.0);
+    else a.x[k] = {0.0, 0.0};
+  }
+  grid_sum(grid, R, v2);
+  const double nb = sqrt(v2[0]);
+  if (nb == 0.0) {  // linsolve.py:136-140
+    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
+    if (tid == 0) { a.out->iterations = 0; a.out->init_res = 0; a.out->final_res = 0;
+                    a.out->n_hist = 0; a.out->converged = 1; a.out->matvecs = 0; }
+    return;
+  }
+  int n_mv = 0;
+  if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
+    matvec_tma<1>(ring, a.A, n, a.x, a.w);
+    ++n_mv;
+    grid.sync();
+    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
+  } else {
+    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k];
+  }
+  double rr[1] = {0.0};
+  for (long long k = tid; k < n; k += nth) rr[0] += abs2(a.r[k]);
+  grid_sum(grid, R, rr);
+  double rnorm = sqrt(rr[0]);
+  double res = rnorm / nb;
+  int n_hist = 0;
+  if (tid == 0) { a.out->init_res = res; a.hist[0] = res; }
+  n_hist++;
+  int its = 0;
+  while (res > a.tol && its < a.maxiter) {
+    const int m = min(a.restart, a.maxiter - its);
+    const double beta = rnorm;
+    // V0 = r / beta and z = P^{-1} V0, per unit (element or DOF)
+    for (long long u = tid; u < nunits; u += nth) {
+      cplx v[3];
+      for (int c = 0; c < ucnt; ++c) {
+        const long long k = u * ucnt + c;
+        v[c] = {a.r[k].re / beta, a.r[k].im / beta};
+        a.V[k] = v[c];
+      }
+      if (pc) precond_regs(a.pinv, u, v, a.z);
+      else a.z[u] = v[0];
+    }
+    if (threadIdx.x == 0) {
+      gs.g[0] = {beta, 0.0};
+      for (int k = 1; k <= m; ++k) gs.g[k] = {0.0, 0.0};
+    }
+    grid.sync();
+    int used = 0;
+    for (int j = 0; j < m; ++j) {
+      matvec_tma<1>(ring, a.A, n, a.z, a.w);   // w = A P^{-1} v_j
+      ++n_mv;
+      grid.sync();
+      // reduction 1: d_i = <v_i, w> (i <= j) and Gram row j: <v_j, v_l> (l < j)
+      cplx* part = a.dpart + (size_t)dpar * gridDim.x * kMaxDots;
+      dpar ^= 1;
+      slice_dots(a.V, n, a.w, j + 1, j, j, k0, k1, part);
+      grid.sync();
+      reduce_slices(part, 2 * j + 1, s_dots);
+      // h = (I + L)^{-1} d  (warp 0, identical in every CTA)
+      if (wid == 0) {
+        for (int i = 0; i <= j; ++i) {
+          cplx s = {0.0, 0.0};
+          for (int l = lane; l < i; l += 32) {
+            const cplx g = i == j ? s_dots[j + 1 + l] : a.Gram[(size_t)i * kMaxRestart + l];
+            s = s + g * s_h[l];
+          }
+          warp_sum(s);
+          if (lane == 0) s_h[i] = s_dots[i] - s;
+          __syncwarp();
+        }
+        if (blockIdx.x == 0)
+          for (int l = lane; l < j; l += 32) a.Gram[(size_t)j * kMaxRestart + l] = s_dots[j + 1 + l];
+      }
+      __syncthreads();
+      // w <- (((w - h0 v0) - h1 v1) ... - hj vj)  and |w|^2 (reduction 2)
+      double q[1] = {0.0};
+      for (long long k = tid; k < n; k += nth) {
+        cplx wk = a.w[k];
+        for (int i = 0; i <= j; ++i) wk = wk - s_h[i] * a.V[(size_t)i * n + k];
+        a.w[k] = wk;
+        q[0] += abs2(wk);
+      }
+      grid_sum(grid, R, q);
+      const double hn = sqrt(q[0]);
+      // Givens (linsolve.py:171-194), identical in every CTA
+      if (threadIdx.x == 0) {
+        for (int i = 0; i <= j; ++i) gs.h[i] = s_h[i];
+        gs.h[j + 1] = {hn, 0.0};
+        for (int i = 0; i < j; ++i) {
+          cplx top = gs.cs[i] * gs.h[i] + gs.sn[i] * gs.h[i + 1];
+          gs.h[i + 1] = (-conj(gs.sn[i])) * gs.h[i] + conj(gs.cs[i]) * gs.h[i + 1];
+          gs.h[i] = top;
+        }
+        double ahj = hypot(gs.h[j].re, gs.h[j].im), ahn = hypot(gs.h[j + 1].re, gs.h[j + 1].im);
+        double den = sqrt(ahj * ahj + ahn * ahn);
+        if (den == 0.0) {
+          gs.cs[j] = {1.0, 0.0}; gs.sn[j] = {0.0, 0.0};
+        } else if (gs.h[j].re == 0.0 && gs.h[j].im == 0.0) {
+          gs.cs[j] = {0.0, 0.0}; gs.sn[j] = {1.0, 0.0};
+        } else {
+          gs.cs[j] = {ahj / den, 0.0};
+          cplx ph = {gs.h[j].re / ahj, gs.h[j].im / ahj};
+          cplx t = ph * conj(gs.h[j + 1]);
+          gs.sn[j] = {t.re / den, t.im / den};
+        }
+        gs.h[j] = gs.cs[j] * gs.h[j] + gs.sn[j] * gs.h[j + 1];
+        gs.h[j + 1] = {0.0, 0.0};
+        gs.g[j + 1] = (-conj(gs.sn[j])) * gs.g[j];
+        gs.g[j] = gs.cs[j] * gs.g[j];
+        s_est = hypot(gs.g[j + 1].re, gs.g[j + 1].im) / nb;
+        if (blockIdx.x == 0)
+          for (int i = 0; i <= j; ++i) a.H[(size_t)i * kMaxRestart + j] = gs.h[i];
+      }
+      __syncthreads();
+      ++its;
+      used = j + 1;
+      const double est = s_est;
+      if (tid == 0 && n_hist < a.hist_cap) a.hist[n_hist] = est;
+      n_hist++;
+      if (est <= a.tol) {
+        grid.sync();  // H visible to every CTA before the back substitution
+        break;
+      }
+      // v_{j+1} = w / h_{j+1,j} and z = P^{-1} v_{j+1}
+      if (hn > 0.0) {
+        cplx* vn = a.V + (size_t)(j + 1) * n;
+        for (long long u = tid; u < nunits; u += nth) {
+          cplx v[3];
+          for (int c = 0; c < ucnt; ++c) {
+            const long long k = u * ucnt + c;
+            v[c] = {a.w[k].re / hn, a.w[k].im / hn};
+            vn[k] = v[c];
+          }
+          if (pc) precond_regs(a.pinv, u, v, a.z);
+          else a.z[u] = v[0];
+        }
+      }
+      grid.sync();
+    }
+    // back substitution (linsolve.py:196-198): warp 0 of every CTA
+    if (wid == 0) {
+      for (int i = used - 1; i >= 0; --i) {
+        cplx s = {0.0, 0.0};
+        for (int k = i + 1 + lane; k < used; k += 32) s = s + a.H[(size_t)i * kMaxRestart + k] * s_y[k];
+        warp_sum(s);
+        if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, a.H[(size_t)i * kMaxRestart + i]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // x += P^{-1} (V^T y), per unit
+    for (long long u = tid; u < nunits; u += nth) {
+      cplx uv[3];
+      for (int c = 0; c < ucnt; ++c) {
+        const long long k = u * ucnt + c;
+        cplx s = {0.0, 0.0};
+        for (int i = 0; i < used; ++i) cfma(s, a.V[(size_t)i * n + k], s_y[i]);
+        uv[c] = s;
+      }
+      if (pc) {
+        precond_regs(a.pinv, u, uv, a.z);
+        for (int c = 0; c < 3; ++c) a.x[3 * u + c] = a.x[3 * u + c] + a.z[3 * u + c];
+      } else {
+        a.x[u] = a.x[u] + uv[0];
+      }
+    }
+    grid.sync();
+    matvec_tma<1>(ring, a.A, n, a.x, a.w);  // true residual (linsolve.py:200-201)
+    ++n_mv;
+    grid.sync();
+    double q2[1] = {0.0};
+    for (long long k = tid; k < n; k += nth) {
+      cplx r = a.b[k] - a.w[k];
+      a.r[k] = r;
+      q2[0] += abs2(r);
+    }
+    grid_sum(grid, R, q2);
+    rnorm = sqrt(q2[0]);
+    res = rnorm / nb;
+  }
+  if (tid == 0) {
+    a.out->iterations = its;
+    a.out->final_res = res;
+    a.out->converged = res <= a.tol;
+    a.out->n_hist = n_hist;
+    a.out->matvecs = n_mv;
+  }
+}
+
+// ---------------------------------------------------------------------
 // SEM (linsolve.py:213-242): Y = A X (one pass over A for all K columns),
 // QR of Y[:, keep] by classical Gram-Schmidt with one re-orthogonalisation
 // (|R_ii| agrees with Householder's to rounding), rank filter
@@ -364,7 +813,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
 template <int K>
 __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
   const long long n = a.n, tid = gtid(), nth = gthreads();
-  matvec_grid<2, K>(a.A, n, a.X, a.Y);
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
+  ring_init(ring, 16.0 * (double)n * (double)n > 96e6);
+  matvec_tma<K>(ring, a.A, n, a.X, a.Y);
   grid.sync();
   __shared__ int keep[kMaxSem];
   __shared__ cplx Rm[kMaxSem][kMaxSem];
@@ -481,6 +934,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_sem(SemArgs a) {
   }
 }
 
+// Batched GEMV y_b = A_b x_b through the TMA ring (regular launch; system
+// blockIdx.y, row groups dealt over blockIdx.x).
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gemv_tma(const cplx* A, const cplx* x,
+                                                               cplx* y, long long n) {
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
+  ring_init(ring, true);
+  const size_t sys = blockIdx.y;
+  matvec_tma<1>(ring, A + sys * n * n, n, x + sys * n, y + sys * n);
+}
+
 // Plain batched GEMV y_b = A_b x_b (one launch, `batch` systems of size n).
 template <int RR>
 __global__ void __launch_bounds__(512) k_gemv_batched(const cplx* A, const cplx* x, cplx* y,
@@ -519,7 +984,8 @@ static int coop_grid(const void* fn) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kSolveThreads, 0);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kSolveThreads, kRingBytes);
   if (per < 1) per = 1;
   return sms * per;
 }
@@ -527,7 +993,9 @@ static int coop_grid(const void* fn) {
 int solver_grid_blocks() {
   if (g_coop_blocks == 0) {
     int a = coop_grid((const void*)k_gmres), b = coop_grid((const void*)k_sem);
+    int c = coop_grid((const void*)k_gmres_mgs);
     g_coop_blocks = a < b ? a : b;
+    g_coop_blocks = c < g_coop_blocks ? c : g_coop_blocks;
   }
   return g_coop_blocks;
 }
@@ -536,15 +1004,16 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
   note_launch();
-  return cudaLaunchCooperativeKernel((const void*)k_gmres, dim3(G), dim3(kSolveThreads), params, 0,
-                                     s);
+  const void* fn = args.ortho == 1 ? (const void*)k_gmres_mgs : (const void*)k_gmres;
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kSolveThreads), params, kRingBytes, s);
 }
 
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
   note_launch();
-  return cudaLaunchCooperativeKernel((const void*)k_sem, dim3(G), dim3(kSolveThreads), params, 0, s);
+  return cudaLaunchCooperativeKernel((const void*)k_sem, dim3(G), dim3(kSolveThreads), params,
+                                     kRingBytes, s);
 }
 
 cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long n, int batch,
@@ -552,12 +1021,15 @@ cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  long long warps_needed = (n + 3) / 4;
-  long long blocks = (warps_needed + 15) / 16;
-  long long cap = (long long)sms * 4 / (batch > 0 ? batch : 1);
-  if (cap < 1) cap = 1;
-  if (blocks > cap) blocks = cap;
-  EWB_NOTE k_gemv_batched<4><<<dim3((unsigned)blocks, batch), 512, 0, s>>>(A, x, y, n, batch);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_gemv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRingBytes);
+    attr = true;
+  }
+  long long groups = (n + kRR - 1) / kRR;
+  long long blocks = groups < sms ? groups : sms;
+  EWB_NOTE k_gemv_tma<<<dim3((unsigned)blocks, batch), kSolveThreads, kRingBytes, s>>>(A, x, y, n);
   return cudaGetLastError();
 }
 

@@ -29,11 +29,14 @@ struct GmresArgs {
   cplx* z;              // scratch (n)
   cplx* V;              // scratch ((restart+1) n)
   cplx* H;              // scratch ((kMaxRestart+1) kMaxRestart)
+  cplx* Gram;           // scratch ((kMaxRestart+1) kMaxRestart): <v_i, v_l>, l < i
+  cplx* dpart;          // scratch (2 * grid * (2 kMaxRestart + 2)) batched-dot partials
   double* partial;      // scratch (2 * grid * 16)
   double* hist;         // residual history (hist_cap)
   GmresOut* out;
   long long n;
   int restart, maxiter, has_x0, hist_cap;
+  int ortho;            // 0: one-reduction MGS (default), 1: sequential MGS
   double tol;
 };
 
