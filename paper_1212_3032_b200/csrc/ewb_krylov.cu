@@ -672,12 +672,19 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
       slice_dots(a.V, n, a.w, j + 1, j, j, k0, k1, part);
       grid.sync();
       reduce_slices(part, 2 * j + 1, s_dots);
-      // h = (I + L)^{-1} d  (warp 0, identical in every CTA)
+      // h = (I + L)^{-1} d  (warp 0, identical in every CTA).  The Gram rows
+      // i < j are first staged (packed, one parallel round trip) into the
+      // idle TMA ring — the matvec is complete, nothing is in flight.
+      cplx* gsm = ring.buf;
+      for (int i = 1; i < j; ++i)
+        for (int l = threadIdx.x; l < i; l += blockDim.x)
+          gsm[i * (i - 1) / 2 + l] = a.Gram[(size_t)i * kMaxRestart + l];
+      __syncthreads();
       if (wid == 0) {
         for (int i = 0; i <= j; ++i) {
           cplx s = {0.0, 0.0};
           for (int l = lane; l < i; l += 32) {
-            const cplx g = i == j ? s_dots[j + 1 + l] : a.Gram[(size_t)i * kMaxRestart + l];
+            const cplx g = i == j ? s_dots[j + 1 + l] : gsm[i * (i - 1) / 2 + l];
             s = s + g * s_h[l];
           }
           warp_sum(s);
@@ -753,17 +760,26 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
       }
       grid.sync();
     }
-    // back substitution (linsolve.py:196-198): warp 0 of every CTA
-    if (wid == 0) {
-      for (int i = used - 1; i >= 0; --i) {
-        cplx s = {0.0, 0.0};
-        for (int k = i + 1 + lane; k < used; k += 32) s = s + a.H[(size_t)i * kMaxRestart + k] * s_y[k];
-        warp_sum(s);
-        if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, a.H[(size_t)i * kMaxRestart + i]);
-        __syncwarp();
+    // back substitution (linsolve.py:196-198): warp 0 of every CTA, with
+    // the upper triangle of H staged (packed) into the idle ring first.
+    {
+      cplx* hsm = ring.buf;
+      for (int i = 0; i < used; ++i)
+        for (int k = i + threadIdx.x; k < used; k += blockDim.x)
+          hsm[i * used - i * (i - 1) / 2 + (k - i)] = a.H[(size_t)i * kMaxRestart + k];
+      __syncthreads();
+      if (wid == 0) {
+        for (int i = used - 1; i >= 0; --i) {
+          const cplx* row = hsm + i * used - i * (i - 1) / 2 - i;
+          cplx s = {0.0, 0.0};
+          for (int k = i + 1 + lane; k < used; k += 32) s = s + row[k] * s_y[k];
+          warp_sum(s);
+          if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, row[i]);
+          __syncwarp();
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
     // x += P^{-1} (V^T y), per unit
     for (long long u = tid; u < nunits; u += nth) {
       cplx uv[3];
