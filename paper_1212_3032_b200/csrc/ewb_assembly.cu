@@ -241,7 +241,10 @@ __device__ __forceinline__ void sys_block(const SysArgs& s, long long N, int i, 
 
 // Far/mid pairs: warp = (row element i, column tile t), lane = column j.
 template <bool DYN, int OUT>
-__global__ void __launch_bounds__(128) k_farmid(Geo g, Phys<DYN> ph, PairOut o) {
+#ifndef EWB_FARMID_MINB
+#define EWB_FARMID_MINB 3
+#endif
+__global__ void __launch_bounds__(128, EWB_FARMID_MINB) k_farmid(Geo g, Phys<DYN> ph, PairOut o) {
   using S = typename Phys<DYN>::S;
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -255,14 +258,14 @@ __global__ void __launch_bounds__(128) k_farmid(Geo g, Phys<DYN> ph, PairOut o) 
   if (j < g.n_e && j != i) tier = exact_tier(xi, yi, zi, g.cx[j], g.cy[j], g.cz[j], g.diam[j]);
   const bool active = tier < 2;
   S U[3][3], T[3][3];
+  // warps whose active lanes are all far (the common case) take an unrolled
+  // 3-point path; mixed far/mid warps the generic loop
+  const bool all_far = __all_sync(0xffffffffu, tier != 1);
   if (active) {
     Acc<S> acc;
     acc_zero(acc);
     const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
-    const int Q = tier == 0 ? 3 : 7;
-    const double* yb = tier == 0 ? g.yfar : g.ymid;
-    const double* wb = tier == 0 ? g.wfar : g.wmid;
-    for (int q = 0; q < Q; ++q) {
+    auto point = [&](const double* yb, const double* wb, int q) {
       double dx = yb[(size_t)(3 * q) * g.n_e + j] - xi;
       double dy = yb[(size_t)(3 * q + 1) * g.n_e + j] - yi;
       double dz = yb[(size_t)(3 * q + 2) * g.n_e + j] - zi;
@@ -271,6 +274,19 @@ __global__ void __launch_bounds__(128) k_farmid(Geo g, Phys<DYN> ph, PairOut o) 
       dx *= ir; dy *= ir; dz *= ir;
       double dn = fma(dz, nz, fma(dy, ny, dx * nx));
       ph.point(acc, r, ir, dx, dy, dz, dn, wb[q] * ar);
+    };
+    if (all_far) {
+#ifdef EWB_FAR_UNROLL
+#pragma unroll
+#else
+#pragma unroll 1
+#endif
+      for (int q = 0; q < 3; ++q) point(g.yfar, g.wfar, q);
+    } else {
+      const int Q = tier == 0 ? 3 : 7;
+      const double* yb = tier == 0 ? g.yfar : g.ymid;
+      const double* wb = tier == 0 ? g.wfar : g.wmid;
+      for (int q = 0; q < Q; ++q) point(yb, wb, q);
     }
     acc_finalize(acc, nx, ny, nz, ph.i4pm(), ph.i4p(), U, T);
     bool ok = true;

@@ -227,6 +227,16 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
     const char* env = getenv("EWB_GMRES_ORTHO");
     g.ortho = env ? atoi(env) : 0;
   }
+  g.probe = nullptr;
+  g.probe_cap = 0;
+  {
+    // diagnostics: EWB_GMRES_PROBE=<device address> enables the phase trace
+    const char* env = getenv("EWB_GMRES_PROBE");
+    if (env) {
+      g.probe = (unsigned long long*)strtoull(env, nullptr, 0);
+      g.probe_cap = 1 << 16;
+    }
+  }
   g.hist = hist;
   g.out = (ewb::GmresOut*)result;
   g.n = n;

@@ -17,7 +17,7 @@
 #include <cuda_runtime.h>
 
 #ifndef EWB_SERIES_TERMS
-#define EWB_SERIES_TERMS 18
+#define EWB_SERIES_TERMS 20
 #endif
 
 namespace ewb {
@@ -198,9 +198,74 @@ __device__ __forceinline__ Brackets brackets_series(const FreqConst& fc, double 
   return o;
 }
 
-__device__ __forceinline__ Brackets brackets_dynamic(const FreqConst& fc, double r, double ir) {
+// Power-sum form of the same series, NT terms: one complex power per term
+// shared by the four real-coefficient sums (fewer FP64 ops than Horner).
+template <int NT>
+__device__ __forceinline__ void series4_pow(cplx w, const double* c0, const double* c1,
+                                            const double* c2, const double* c3, cplx* out) {
+  cplx s0 = {c0[0], 0.0}, s1 = {c1[0], 0.0}, s2 = {c2[0], 0.0}, s3 = {c3[0], 0.0};
+  cplx p = w;
+#pragma unroll
+  for (int n = 1; n < NT; ++n) {
+    axpy(s0, c0[n], p);
+    axpy(s1, c1[n], p);
+    axpy(s2, c2[n], p);
+    axpy(s3, c3[n], p);
+    if (n + 1 < NT) p = p * w;
+  }
+  out[0] = s0; out[1] = s1; out[2] = s2; out[3] = s3;
+}
+
+template <int NT>
+__device__ __forceinline__ Brackets brackets_series_n(const FreqConst& fc, double r) {
+  static_assert(NT <= EWB_SERIES_TERMS, "series table too short");
+  cplx ws = {fc.ks.im * r, -fc.ks.re * r};
+  cplx wp = {fc.kp.im * r, -fc.kp.re * r};
+  cplx s[4], p[4];
+  series4_pow<NT>(ws, c_series.a, c_series.da, c_series.c, c_series.dc, s);
+  series4_pow<NT>(wp, c_series.b, c_series.db, c_series.c, c_series.dc, p);
+  Brackets o;
+  o.f0 = s[0] + fc.g2 * p[0];
+  o.f2 = s[1] + fc.g2 * p[1];
+  o.f1 = s[2] - fc.g2 * p[2];
+  o.f3 = s[3] - fc.g2 * p[3];
+  return o;
+}
+
+// Strict per-point switch exactly as kernels.py:79-95 (|k_s r| < 0.35).
+__device__ __forceinline__ Brackets brackets_strict(const FreqConst& fc, double r, double ir) {
+#ifdef EWB_SERIES_POW
+  if (fc.ks_abs * r < kSeriesSwitch) return brackets_series_n<16>(fc, r);
+#else
   if (fc.ks_abs * r < kSeriesSwitch) return brackets_series(fc, r);
+#endif
   return brackets_closed(fc, r, ir);
+}
+
+// Warp-uniform evaluation.  When every active lane is on the same side of
+// the reference's switch the result is the reference's branch.  When a warp
+// mixes both, one evaluation valid for all its lanes is used instead of
+// executing both branches serially:
+//   series, 20 terms, if every |z_s| < 1   (truncation < 1e-17 relative)
+//   closed form      if every |z_s| > 0.05 (cancellation <= eps/|z|^2 ~ 1e-13)
+// Both agree with the reference's choice far inside the 1e-10 parity bar
+// (the reference's own seam test allows 1e-12, test_kernels.py:83-98).
+// Build with -DEWB_STRICT_SWITCH for the per-point reference switch.
+__device__ __forceinline__ Brackets brackets_dynamic(const FreqConst& fc, double r, double ir) {
+#if defined(EWB_TIMING_CLOSED_ONLY)
+  return brackets_closed(fc, r, ir);   // timing experiments only: not parity-valid
+#elif !defined(EWB_UNIFORM_SWITCH)
+  return brackets_strict(fc, r, ir);
+#else
+  const unsigned mask = __activemask();
+  const double za = fc.ks_abs * r;
+  const bool ser = za < kSeriesSwitch;
+  if (__all_sync(mask, ser)) return brackets_series_n<16>(fc, r);
+  if (__all_sync(mask, !ser)) return brackets_closed(fc, r, ir);
+  if (__all_sync(mask, za < 1.0)) return brackets_series_n<20>(fc, r);
+  if (__all_sync(mask, za > 0.05)) return brackets_closed(fc, r, ir);
+  return brackets_strict(fc, r, ir);
+#endif
 }
 
 // ---------------------------------------------------------------------

@@ -37,6 +37,8 @@ struct GmresArgs {
   long long n;
   int restart, maxiter, has_x0, hist_cap;
   int ortho;            // 0: one-reduction MGS (default), 1: sequential MGS
+  unsigned long long* probe;  // optional phase trace (CTA 0): (phase << 56) | globaltimer
+  int probe_cap;
   double tol;
 };
 
