@@ -50,7 +50,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg1", "cfg3", "cfg4"))
+    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg1", "cfg3", "cfg4", "cfg5"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args(argv)
 

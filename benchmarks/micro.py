@@ -18,6 +18,7 @@ import ctypes
 import json
 import math
 import statistics
+import time
 
 import numpy as np
 
@@ -172,6 +173,76 @@ def run_cfg4(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_cfg5(args, rank, world, local_rank):
+    """cfg5: ico6 cavity, 81,920 el / 245,760 DOF, matrix-free (966 GB dense).
+
+    value = element pairs per second of one matrix-free operator application
+    (6.7e9 pairs, 2.04e10 quadrature points); the first two frequencies of the
+    SEM sweep (the reference's own check range) are solved and timed too."""
+    import torch
+
+    import bench
+    from paper_1212_3032_b200 import _lib
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.matfree import MatrixFreeOperator
+    from paper_1212_3032_b200.workloads import cfg5
+
+    lib = _lib.require_cuda()
+    torch.cuda.set_device(local_rank)
+    peak64 = bench.fp64_peak()
+    cfg = cfg5()
+    t0 = time.perf_counter()
+    ds = DeviceSweep(cfg, frequencies=[0, 1])
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    pc = ds.asm.pair_counts()
+    pairs = pc["far"] + pc["mid"] + pc["near"] + pc["n_elements"]
+    pe = ds.asm.point_evals()
+    flops = 397.0 * pe + 72.0 * pairs            # SURVEY §8(d) matrix-free count
+    op = MatrixFreeOperator(ds.asm, complex(ds.omegas[1]))
+    v = torch.randn((1, ds.n), dtype=torch.complex128, device="cuda")
+    for _ in range(max(1, args.warmup)):
+        op.apply_multi(v)
+    torch.cuda.synchronize()
+    sampler = bench.ClockSampler(local_rank)
+    l0 = lib.ewb_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        op.apply_multi(v)
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = lib.ewb_launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    ds.matrix_free = True
+    t1 = time.perf_counter()
+    stats = ds.run()
+    first2 = time.perf_counter() - t1
+    tf = flops / (ms * 1e-3) / 1e12
+    line = {
+        "metric": "element-pair kernel evals/s", "value": pairs / (ms * 1e-3),
+        "unit": "pair-evals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (deterministic ico6 cavity, unit step pressure)",
+        "config": {"workload": "cfg5: flipped icosphere L6, 81920 el / 245760 DOF, matrix-free "
+                               "operator application (one step = one A v over all 6.7e9 pairs)",
+                   "l2": "compute-bound"},
+        "roofline": {"bound": "fp64", "achieved": tf, "peak": peak64, "unit": "TFLOP/s",
+                     "frac": tf / peak64, "traffic": None, "algorithmic_flops_per_launch": flops,
+                     "peak_source": "measured DFMA probe"},
+        "gpu_launches": launches, "clocks": clocks,
+        "metrics": {"setup_s": setup_s, "point_evals_per_application": pe,
+                    "point_evals_per_s": pe / (ms * 1e-3), "pairs": pc,
+                    "first_two_frequencies_s": first2,
+                    "first_two": {k: dict(iterations=s.iterations, applications=s.matvecs,
+                                          init_residual=s.init_residual,
+                                          final_residual=s.final_residual)
+                                  for k, s in stats.items()}},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main(args, rank, world, local_rank):
     if rank != 0:
         return
@@ -179,3 +250,5 @@ def main(args, rank, world, local_rank):
         run_cfg3(args, rank, world, local_rank)
     elif args.workload == "cfg4":
         run_cfg4(args, rank, world, local_rank)
+    elif args.workload == "cfg5":
+        run_cfg5(args, rank, world, local_rank)

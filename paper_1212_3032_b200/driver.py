@@ -150,10 +150,69 @@ class DeviceSweep:
         self.system = None
         self.d2h_bytes = 0
 
+    def run_matrix_free(self):
+        """Matrix-free sweep (north-star item 2): the operator is recomputed in
+        every application, nothing of size N^2 is stored.  Per frequency the
+        right-hand side, the SEM product Y = A X and the block preconditioner
+        come from ONE pass over all element pairs (ewb_matfree_apply with K+1
+        vectors); GMRES then applies the operator once per iteration."""
+        import torch
+
+        from .krylov_host import gmres_operator, sem_operator
+        from .linsolve import BlockDiagPreconditioner
+        from .matfree import MatrixFreeOperator
+
+        cfg = self.cfg
+        stats = {}
+        n_hist = 0
+        K = cfg.sem_depth
+        self.hist.zero_()
+        self.phase = {"applications": 0, "solves": 0, "seconds": 0.0}
+        for k in self.frequencies:
+            omega = complex(self.omegas[k])
+            t0 = time.perf_counter()
+            try:
+                if omega == 0:
+                    raise ValueError("omega == 0 (kappa = 0) needs the dense static path")
+                op = MatrixFreeOperator(self.asm, omega, cfg.bcs)
+                use_sem = cfg.sem_enabled and n_hist > 0
+                hist = self.hist[:n_hist] if use_sem else None
+                b, Y = op.rhs_and_apply(self.P[k], hist, want_pinv=True)
+                pc = BlockDiagPreconditioner(op.pinv)
+                x0 = sem_operator(op, b, hist, 1e-10, Y=Y) if use_sem else None
+                x, st = gmres_operator(op, b, x0, cfg.tol, cfg.restart, cfg.maxiter, pc)
+                nf, sg = ctypes.c_int32(), ctypes.c_int32()
+                _lib.check(self.asm._lib.ewb_ctx_flags(self.asm.ctx, ctypes.byref(nf),
+                                                       ctypes.byref(sg), _lib.stream_handle()))
+                if nf.value:
+                    raise FloatingPointError(f"non-finite operator entries at omega = {omega}")
+            except SweepError:
+                raise
+            except Exception as exc:
+                raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
+            torch.cuda.synchronize()
+            st.k, st.omega = k, omega
+            st.seconds = time.perf_counter() - t0
+            st.matvecs = op.applications
+            stats[k] = st
+            self.phase["applications"] += op.applications
+            self.phase["solves"] += 1
+            self.phase["seconds"] += st.seconds
+            self.sol[k] = x
+            if cfg.sem_enabled:
+                self.hist[1:] = self.hist[:-1].clone()
+                self.hist[0] = x
+                n_hist = min(n_hist + 1, K)
+            log.info("k=%d its=%d applications=%d %.2fs", k, st.iterations, op.applications,
+                     st.seconds)
+        return stats
+
     def run(self, timing: bool = False):
         """Sweep the owned frequencies; returns {k: SolveStats}."""
         import torch
 
+        if getattr(self, "matrix_free", False):
+            return self.run_matrix_free()
         cfg = self.cfg
         asm = self.asm
         stats = {}
@@ -241,8 +300,13 @@ class DeviceSweep:
 
 
 def run_sweep(cfg: SweepConfig, full_field: bool = False, assembler: Assembler | None = None,
-              distributed: bool = True, _sweep_out: list | None = None) -> SweepResult:
-    """Run the transient analysis described by ``cfg`` on the GPU."""
+              distributed: bool = True, _sweep_out: list | None = None,
+              matrix_free: bool | None = None) -> SweepResult:
+    """Run the transient analysis described by ``cfg`` on the GPU.
+
+    ``matrix_free=None`` picks the matrix-free operator automatically when the
+    dense (N, N) complex matrix would not fit comfortably in HBM (> 40 % of
+    the free device memory)."""
     import torch
 
     t_begin = time.perf_counter()
@@ -256,6 +320,10 @@ def run_sweep(cfg: SweepConfig, full_field: bool = False, assembler: Assembler |
     n_freq = cfg.n_omega // 2 + 1
     mine = shard_frequencies(n_freq, rank, world) if parallel else None
     ds = DeviceSweep(cfg, assembler, mine)
+    if matrix_free is None:
+        free, _ = torch.cuda.mem_get_info()
+        matrix_free = 16.0 * cfg.mesh.n_dofs ** 2 > 0.4 * free
+    ds.matrix_free = bool(matrix_free)
     log.info("sweep: %d elements, %d frequencies, eta=%.4g 1/s", cfg.mesh.n_elements, n_freq, eta)
     stats_local = ds.run()
     probes = list(cfg.probes)
