@@ -82,6 +82,12 @@ int ewb_ctx_create(const double* centroids_host, const double* normals_host,
                    const int32_t* rule_q_host, void* stream, ewb_ctx** out);
 int ewb_ctx_destroy(ewb_ctx* ctx);
 
+/* Exterior-problem diagonal (NOT a reference mode, parity
+ * unpinned): on != 0 adds +I to every T diagonal block (c + PV int T = I, an
+ * unbounded medium) instead of the reference's interior identity
+ * (assembly.py:243-246).  Default off. */
+int ewb_ctx_set_exterior(ewb_ctx* ctx, int32_t on, void* stream);
+
 /* counts_host[8] = n_e, far pairs, mid pairs, near pairs, near L1..L4. */
 int ewb_ctx_counts(const ewb_ctx* ctx, int64_t* counts_host);
 

@@ -19,7 +19,8 @@ LIB_PATH = PKG_DIR / LIB_NAME
 # Every symbol include/ewbem_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = (
     "ewb_abi_version", "ewb_last_error", "ewb_launch_count", "ewb_ctx_create", "ewb_ctx_destroy",
-    "ewb_ctx_counts", "ewb_static_rowsums", "ewb_static_tu", "ewb_assemble_tu",
+    "ewb_ctx_set_exterior", "ewb_ctx_counts", "ewb_static_rowsums", "ewb_static_tu",
+    "ewb_assemble_tu",
     "ewb_assemble_system", "ewb_ctx_flags", "ewb_apply_bcs", "ewb_blockdiag_inverse",
     "ewb_gemv_batched", "ewb_gmres_workspace_bytes", "ewb_gmres",
     "ewb_sem_workspace_bytes", "ewb_sem_guess", "ewb_window_idft",
@@ -59,6 +60,7 @@ _SIGS = {
     "ewb_ctx_create": (I32, [P, P, P, P, P, I64, D, D, D, P, P, P, P, P, P, ctypes.POINTER(P)]),
     "ewb_ctx_destroy": (I32, [P]),
     "ewb_ctx_counts": (I32, [P, P]),
+    "ewb_ctx_set_exterior": (I32, [P, I32, P]),
     "ewb_static_rowsums": (I32, [P, P, P]),
     "ewb_static_tu": (I32, [P, P, P, P]),
     "ewb_assemble_tu": (I32, [P, D, D, P, P, P]),

@@ -109,7 +109,10 @@ class Assembler:
     """Device-resident per-mesh context + per-frequency assembly (assembly.py:103-254)."""
 
     def __init__(self, mesh: TriangleMesh, material: Material,
-                 quadrature: QuadratureSet | None = None):
+                 quadrature: QuadratureSet | None = None, exterior: bool = False):
+        """``exterior=True`` (not a reference mode; parity unpinned) puts +I on
+        every dynamic T diagonal block: c + PV int T = I for an unbounded
+        medium instead of the reference's interior identity."""
         lib = _lib.require_cuda()
         self.mesh = mesh
         self.material = material
@@ -133,6 +136,9 @@ class Assembler:
         self._ctx = out
         self._lib = lib
         self._static_tu = None
+        self.exterior = bool(exterior)
+        if self.exterior:
+            _lib.check(lib.ewb_ctx_set_exterior(self._ctx, 1, _lib.stream_handle()))
 
     def close(self):
         if getattr(self, "_ctx", None):

@@ -425,6 +425,16 @@ __global__ void k_rowsum_finalize(Geo g, const double* spart, const double* snea
   diag_base[tid] = -s - t_self[tid];
 }
 
+// Exterior-problem diagonal: the reference enforces the
+// interior identity c + PV int T = 0 (assembly.py:243-246); an unbounded
+// medium needs c + PV int T = I, i.e. +I on every T diagonal block.  No
+// reference mode exists, so this option's parity is unpinned.
+__global__ void k_diag_shift(int n_e, double* diag_base, double shift) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_e) return;
+  for (int a = 0; a < 3; ++a) diag_base[9 * e + 4 * a] += shift;
+}
+
 // Static diagonal for omega = 0 (assembly.py:207-216): T_ee = -rowsum, U_ee = U_sta_self.
 __global__ void k_static_diag(int n_e, const double* rowsums, const double* u_self, double* T,
                               double* U) {
@@ -802,6 +812,15 @@ cudaError_t launch_apply_bcs(const cplx* T, const cplx* U, const uint8_t* kinds,
 cudaError_t launch_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int* singular,
                                      cudaStream_t s) {
   EWB_NOTE k_blockdiag_inverse<<<blocks_for(n / 3, 128), 128, 0, s>>>(A, n, pinv, singular);
+  return cudaGetLastError();
+}
+
+cudaError_t set_exterior(Context& c, int on, cudaStream_t s) {
+  on = on ? 1 : 0;
+  if (on == c.exterior) return cudaSuccess;
+  EWB_NOTE k_diag_shift<<<blocks_for(c.n_e, 128), 128, 0, s>>>(c.n_e, c.diag_base,
+                                                                on ? 1.0 : -1.0);
+  c.exterior = on;
   return cudaGetLastError();
 }
 

@@ -90,6 +90,12 @@ int ewb_ctx_destroy(ewb_ctx* ctx) {
   return EWB_OK;
 }
 
+int ewb_ctx_set_exterior(ewb_ctx* ctx, int32_t on, void* stream) {
+  if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_set_exterior: null argument");
+  EWB_CUDA(ewb::set_exterior(ctx->c, on, S(stream)), "ewb_ctx_set_exterior");
+  return EWB_OK;
+}
+
 int ewb_ctx_counts(const ewb_ctx* ctx, int64_t* counts) {
   if (!ctx || !counts) return fail(EWB_ERR_INVALID, "ewb_ctx_counts: null argument");
   counts[0] = ctx->c.n_e;

@@ -99,6 +99,7 @@ struct Context {
   long long n_far = 0, n_mid = 0;    // off-diagonal pair counts per tier
   long long n_near_lvl[kMaxNearLevel + 1] = {0, 0, 0, 0, 0};
   double lam = 0, mu = 0, rho = 0;
+  int exterior = 0;                  // 1: c + PV int T = I diagonal
   Geo g{};
   // owned device buffers
   std::vector<void*> owned;
@@ -133,5 +134,6 @@ cudaError_t launch_apply_bcs(const cplx* T, const cplx* U, const uint8_t* kinds,
                              const cplx* p, long long n, cplx* A, cplx* b, cudaStream_t s);
 cudaError_t launch_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int* singular,
                                      cudaStream_t s);
+cudaError_t set_exterior(Context& c, int on, cudaStream_t s);
 
 }  // namespace ewb
