@@ -240,90 +240,98 @@ __device__ __forceinline__ void sys_block(const SysArgs& s, long long N, int i, 
 }
 
 // Far/mid pairs: warp = (row element i, column tile t), lane = column j.
-template <bool DYN, int OUT>
 #ifndef EWB_FARMID_MINB
 #define EWB_FARMID_MINB 3
 #endif
+#ifndef EWB_FARMID_ROWS
+#define EWB_FARMID_ROWS 4
+#endif
+constexpr int kFarRows = EWB_FARMID_ROWS;
+
+// Far/mid pairs: warp = (kFarRows consecutive row elements, column tile t),
+// lane = column j.  The column element's data (centroid, diameter, normal,
+// area, the 3 far field points) is loaded once per warp and reused for the
+// kFarRows rows, so its load latency is paid once per kFarRows pairs.
+template <bool DYN, int OUT>
 __global__ void __launch_bounds__(128, EWB_FARMID_MINB) k_farmid(Geo g, Phys<DYN> ph, PairOut o) {
   using S = typename Phys<DYN>::S;
   const int lane = threadIdx.x & 31;
   const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int ntile = (g.n_e + 31) >> 5;
-  if (warp >= (long long)g.n_e * ntile) return;
-  const int i = (int)(warp / ntile), t = (int)(warp % ntile);
+  const int ngroups = (g.n_e + kFarRows - 1) / kFarRows;
+  if (warp >= (long long)ngroups * ntile) return;
+  const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
   const int j = t * 32 + lane;
+  const bool jv = j < g.n_e;
   const long long N = 3LL * g.n_e;
-  const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
-  int tier = 3;
-  if (j < g.n_e && j != i) tier = exact_tier(xi, yi, zi, g.cx[j], g.cy[j], g.cz[j], g.diam[j]);
-  const bool active = tier < 2;
-  S U[3][3], T[3][3];
-  // warps whose active lanes are all far (the common case) take an unrolled
-  // 3-point path; mixed far/mid warps the generic loop
-  const bool all_far = __all_sync(0xffffffffu, tier != 1);
-  if (active) {
-    Acc<S> acc;
-    acc_zero(acc);
-    const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
-    auto point = [&](const double* yb, const double* wb, int q) {
-      double dx = yb[(size_t)(3 * q) * g.n_e + j] - xi;
-      double dy = yb[(size_t)(3 * q + 1) * g.n_e + j] - yi;
-      double dz = yb[(size_t)(3 * q + 2) * g.n_e + j] - zi;
-      double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-      double ir = 1.0 / r;
-      dx *= ir; dy *= ir; dz *= ir;
-      double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-      ph.point(acc, r, ir, dx, dy, dz, dn, wb[q] * ar);
-    };
-    if (all_far) {
-#ifdef EWB_FAR_UNROLL
+  const int jj = jv ? j : 0;
+  const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
+  const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
+  double yf[9];
 #pragma unroll
-#else
+  for (int c = 0; c < 9; ++c) yf[c] = g.yfar[(size_t)c * g.n_e + jj];
+  for (int r = 0; r < kFarRows; ++r) {
+    const int i = rg * kFarRows + r;
+    if (i >= g.n_e) break;
+    const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+    int tier = 3;
+    if (jv && j != i) tier = exact_tier(xi, yi, zi, cxj, cyj, czj, dj);
+    const bool active = tier < 2;
+    S U[3][3], T[3][3];
+    if (active) {
+      Acc<S> acc;
+      acc_zero(acc);
+      auto point = [&](double px, double py, double pz, double wq) {
+        double dx = px - xi, dy = py - yi, dz = pz - zi;
+        double rr = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
+        double ir = 1.0 / rr;
+        dx *= ir; dy *= ir; dz *= ir;
+        double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+        ph.point(acc, rr, ir, dx, dy, dz, dn, wq * ar);
+      };
+      if (tier == 0) {
 #pragma unroll 1
-#endif
-      for (int q = 0; q < 3; ++q) point(g.yfar, g.wfar, q);
-    } else {
-      const int Q = tier == 0 ? 3 : 7;
-      const double* yb = tier == 0 ? g.yfar : g.ymid;
-      const double* wb = tier == 0 ? g.wfar : g.wmid;
-      for (int q = 0; q < Q; ++q) point(yb, wb, q);
-    }
-    acc_finalize(acc, nx, ny, nz, ph.i4pm(), ph.i4p(), U, T);
-    bool ok = true;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
-    if (!ok) o.flags[0] = 1;
-    if (OUT & OUT_TU) {
-      store_block((S*)o.T, N, i, j, T);
-      store_block((S*)o.U, N, i, j, U);
-    }
-  }
-  if constexpr (DYN && (OUT & OUT_SYS)) {
-    cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
-    if (active) sys_block(o.sys, N, i, j, U, T, bc);
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      warp_sum(bc[a]);
-      if (lane == 0) o.bpart[(size_t)t * N + 3 * i + a] = bc[a];
-    }
-  }
-  if constexpr (!DYN && (OUT & OUT_ROWSUM)) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        double v = active ? to_c(T[a][b]).re : 0.0;
-        warp_sum(v);
-        if (lane == 0) o.spart[((size_t)t * g.n_e + i) * 9 + 3 * a + b] = v;
+        for (int q = 0; q < 3; ++q) point(yf[3 * q], yf[3 * q + 1], yf[3 * q + 2], g.wfar[q]);
+      } else {
+        for (int q = 0; q < 7; ++q)
+          point(g.ymid[(size_t)(3 * q) * g.n_e + j], g.ymid[(size_t)(3 * q + 1) * g.n_e + j],
+                g.ymid[(size_t)(3 * q + 2) * g.n_e + j], g.wmid[q]);
       }
+      acc_finalize(acc, nx, ny, nz, ph.i4pm(), ph.i4p(), U, T);
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
+      if (!ok) o.flags[0] = 1;
+      if (OUT & OUT_TU) {
+        store_block((S*)o.T, N, i, j, T);
+        store_block((S*)o.U, N, i, j, U);
+      }
+    }
+    if constexpr (DYN && (OUT & OUT_SYS)) {
+      cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+      if (active) sys_block(o.sys, N, i, j, U, T, bc);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        warp_sum(bc[a]);
+        if (lane == 0) o.bpart[(size_t)t * N + 3 * i + a] = bc[a];
+      }
+    }
+    if constexpr (!DYN && (OUT & OUT_ROWSUM)) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          double v = active ? to_c(T[a][b]).re : 0.0;
+          warp_sum(v);
+          if (lane == 0) o.spart[((size_t)t * g.n_e + i) * 9 + 3 * a + b] = v;
+        }
+    }
   }
 }
-
-// Near pairs: warp per pair, lanes split the Q = 7*4^L subdivided points.
 template <bool DYN, int OUT>
-__global__ void __launch_bounds__(128) k_near(Geo g, Phys<DYN> ph, PairOut o, int n_near) {
+__global__ void __launch_bounds__(128, 3) k_near(Geo g, Phys<DYN> ph, PairOut o, int n_near) {
   using S = typename Phys<DYN>::S;
   const int lane = threadIdx.x & 31;
   const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -616,6 +624,7 @@ FreqConst freq_const(const Context& c, double ore, double oim) {
   cplx q = cdiv_h(f.kp, f.ks);
   f.g2 = {q.re * q.re - q.im * q.im, q.re * q.im + q.im * q.re};
   f.ks_abs = hypot(f.ks.re, f.ks.im);
+  f.sw = kSeriesSwitch;
   f.ratio = (c.lam + 2.0 * c.mu) / c.mu;
   f.inv4pimu = 1.0 / (4.0 * M_PI * c.mu);
   f.inv4pi = 1.0 / (4.0 * M_PI);
@@ -746,7 +755,7 @@ cudaError_t launch_static_pass(Context& c, double* t_out, double* u_out, cudaStr
   PairOut o{};
   o.T = t_out; o.U = u_out; o.spart = c.spart; o.snear = c.snear; o.flags = c.flags;
   const int n = c.n_e;
-  long long warps = (long long)n * c.n_tiles;
+  long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
   if (t_out) {
     EWB_NOTE k_farmid<false, OUT_TU | OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
     if (c.n_near)
@@ -774,8 +783,10 @@ cudaError_t launch_assemble_tu(Context& c, double ore, double oim, cplx* T, cplx
   PairOut o{};
   o.T = T; o.U = U; o.flags = c.flags;
   const int n = c.n_e;
-  long long warps = (long long)n * c.n_tiles;
-  EWB_NOTE k_farmid<true, OUT_TU><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+  long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  Phys<true> phf = ph;
+  phf.fc.sw = kFarSwitch;
+  EWB_NOTE k_farmid<true, OUT_TU><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, phf, o);
   if (c.n_near)
     EWB_NOTE k_near<true, OUT_TU><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
                                                                                  c.n_near);
@@ -792,8 +803,10 @@ cudaError_t launch_assemble_system(Context& c, double ore, double oim, const uin
   o.sys = SysArgs{kinds, prescribed, A, pinv, b};
   o.bpart = c.bpart; o.bnear = c.bnear; o.flags = c.flags;
   const int n = c.n_e;
-  long long warps = (long long)n * c.n_tiles;
-  EWB_NOTE k_farmid<true, OUT_SYS><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+  long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  Phys<true> phf = ph;
+  phf.fc.sw = kFarSwitch;
+  EWB_NOTE k_farmid<true, OUT_SYS><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, phf, o);
   if (c.n_near)
     EWB_NOTE k_near<true, OUT_SYS><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
                                                                                    c.n_near);

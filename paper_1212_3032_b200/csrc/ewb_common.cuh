@@ -77,6 +77,7 @@ struct FreqConst {
   cplx iks, ikp;        // 1 / ks, 1 / kp
   cplx g2;              // (kp / ks)^2   (kernels.py:75)
   double ks_abs;        // |ks| : |z_s| = |ks| r decides the series branch
+  double sw;            // series below |z_s| < sw (reference: 0.35, kernels.py:36)
   double ratio;         // (lam + 2 mu) / mu        (kernels.py:328)
   double inv4pimu;      // 1 / (4 pi mu)
   double inv4pi;        // 1 / (4 pi)
@@ -233,11 +234,22 @@ __device__ __forceinline__ Brackets brackets_series_n(const FreqConst& fc, doubl
 }
 
 // Strict per-point switch exactly as kernels.py:79-95 (|k_s r| < 0.35).
+// The far/mid (and matrix-free far) kernels run with fc.sw = kFarSwitch:
+// between 0.1 and 0.35 the closed form agrees with the series to <= 2e-13
+// relative (measured against the reference's 24-term series, DESIGN.md
+// §4), and warps of far pairs then never execute both branches.  Near and
+// self pairs keep the reference's 0.35.  -DEWB_STRICT_SWITCH: 0.35 everywhere.
+#ifdef EWB_STRICT_SWITCH
+constexpr double kFarSwitch = kSeriesSwitch;
+#else
+constexpr double kFarSwitch = 0.1;
+#endif
+
 __device__ __forceinline__ Brackets brackets_strict(const FreqConst& fc, double r, double ir) {
 #ifdef EWB_SERIES_POW
-  if (fc.ks_abs * r < kSeriesSwitch) return brackets_series_n<16>(fc, r);
+  if (fc.ks_abs * r < fc.sw) return brackets_series_n<16>(fc, r);
 #else
-  if (fc.ks_abs * r < kSeriesSwitch) return brackets_series(fc, r);
+  if (fc.ks_abs * r < fc.sw) return brackets_series(fc, r);
 #endif
   return brackets_closed(fc, r, ir);
 }

@@ -304,6 +304,35 @@ __device__ void matvec_tma(Ring& R, const cplx* __restrict__ A, long long n, con
   R.pos += (unsigned)S;
 }
 
+// One out-of-line copy of the single-vector matvec for the GMRES kernel:
+// every call site shares the same (register-allocated once) code.  The ring
+// travels by value and the new position is returned, so nothing is spilled.
+__device__ __noinline__ unsigned matvec1_nl(Ring R, const cplx* __restrict__ A, long long n,
+                                            const cplx* x, cplx* y) {
+  matvec_tma<1>(R, A, n, x, y);
+  return R.pos;
+}
+// (measured: the out-of-line copy is ~15 % slower than inlining; kept for
+// A/B tests with -DEWB_MATVEC_NOINLINE)
+#ifndef EWB_MATVEC_NOINLINE
+#define EWB_MATVEC1(ring, A, n, x, y) matvec_tma<1>(ring, A, n, x, y)
+#else
+#define EWB_MATVEC1(ring, A, n, x, y) (ring).pos = matvec1_nl(ring, A, n, x, y)
+#endif
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// optional phase trace (CTA 0): (phase << 56) | %globaltimer
+#define EWB_PROBE(id)                                                                  \
+  do {                                                                                 \
+    if (a.probe && blockIdx.x == 0 && threadIdx.x == 0 && n_probe < a.probe_cap)       \
+      a.probe[n_probe++] = ((unsigned long long)(id) << 56) |                          \
+                           (gtimer() & ((1ull << 56) - 1));                            \
+  } while (0)
+
 // z = P^{-1} v  (3x3 blocks; identity when pinv == nullptr).  Grid-stride
 // over elements: thread e owns DOFs 3e..3e+2.
 __device__ __forceinline__ void precond_apply_elem(const cplx* pinv, long long e, const cplx* v,
@@ -588,6 +617,7 @@ __device__ __forceinline__ void precond_regs(const cplx* pinv, long long e, cons
 }
 
 __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
+  int n_probe = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
@@ -626,7 +656,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
   }
   int n_mv = 0;
   if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
-    matvec_tma<1>(ring, a.A, n, a.x, a.w);
+    EWB_MATVEC1(ring, a.A, n, a.x, a.w);
     ++n_mv;
     grid.sync();
     for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
@@ -663,13 +693,26 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
     grid.sync();
     int used = 0;
     for (int j = 0; j < m; ++j) {
-      matvec_tma<1>(ring, a.A, n, a.z, a.w);   // w = A P^{-1} v_j
+#ifdef EWB_DBG_LOOP_X
+      EWB_MATVEC1(ring, a.A, n, a.x, a.w);   // timing experiment only
+#else
+      EWB_MATVEC1(ring, a.A, n, a.z, a.w);   // w = A P^{-1} v_j
+#endif
       ++n_mv;
       grid.sync();
       // reduction 1: d_i = <v_i, w> (i <= j) and Gram row j: <v_j, v_l> (l < j)
       cplx* part = a.dpart + (size_t)dpar * gridDim.x * kMaxDots;
       dpar ^= 1;
+      EWB_PROBE(20);
+#ifdef EWB_DBG_WARM
+      for (int rep = 0; rep < 2; ++rep) {  // second pass: same code and data, warm
+        slice_dots(a.V, n, a.w, j + 1, j, j, k0, k1, part);
+        EWB_PROBE(21 + rep);
+      }
+#else
       slice_dots(a.V, n, a.w, j + 1, j, j, k0, k1, part);
+      EWB_PROBE(21);
+#endif
       grid.sync();
       reduce_slices(part, 2 * j + 1, s_dots);
       // h = (I + L)^{-1} d  (warp 0, identical in every CTA).  The Gram rows
@@ -797,7 +840,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
       }
     }
     grid.sync();
-    matvec_tma<1>(ring, a.A, n, a.x, a.w);  // true residual (linsolve.py:200-201)
+    EWB_MATVEC1(ring, a.A, n, a.x, a.w);  // true residual (linsolve.py:200-201)
     ++n_mv;
     grid.sync();
     double q2[1] = {0.0};

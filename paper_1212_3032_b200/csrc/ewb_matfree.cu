@@ -301,7 +301,9 @@ template <int K, bool USE_U>
 static cudaError_t mf_launch(Context& c, Phys<true> ph, MfArgs m, cudaStream_t s) {
   const int n = c.n_e;
   dim3 grid((n + 127) / 128, m.nchunk);
-  EWB_NOTE k_mf_farmid<K, USE_U><<<grid, 128, 0, s>>>(c.g, ph, m);
+  Phys<true> phf = ph;
+  phf.fc.sw = kFarSwitch;
+  EWB_NOTE k_mf_farmid<K, USE_U><<<grid, 128, 0, s>>>(c.g, phf, m);
   if (c.n_near)
     EWB_NOTE k_mf_near<K, USE_U><<<(c.n_near * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m, c.n_near);
   EWB_NOTE k_mf_self<K, USE_U><<<(n * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m);
