@@ -283,8 +283,9 @@ __global__ void __launch_bounds__(128, EWB_FARMID_MINB) k_farmid(Geo g, Phys<DYN
       acc_zero(acc);
       auto point = [&](double px, double py, double pz, double wq) {
         double dx = px - xi, dy = py - yi, dz = pz - zi;
-        double rr = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-        double ir = 1.0 / rr;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ir = rsqrt(r2);
+        double rr = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
         double dn = fma(dz, nz, fma(dy, ny, dx * nx));
         ph.point(acc, rr, ir, dx, dy, dz, dn, wq * ar);
@@ -352,8 +353,9 @@ __global__ void __launch_bounds__(128, 3) k_near(Geo g, Phys<DYN> ph, PairOut o,
     double dx = fma(b2, v[6], fma(b1, v[3], b0 * v[0])) - xi;
     double dy = fma(b2, v[7], fma(b1, v[4], b0 * v[1])) - yi;
     double dz = fma(b2, v[8], fma(b1, v[5], b0 * v[2])) - zi;
-    double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-    double ir = 1.0 / r;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
     dx *= ir; dy *= ir; dz *= ir;
     double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     ph.point(acc, r, ir, dx, dy, dz, dn, wq[q] * ar);
@@ -393,8 +395,9 @@ __device__ __forceinline__ void self_accumulate(const Geo& g, const Phys<DYN>& p
   for (int q = lane; q < kSelfQ; q += 32) {
     double4 y = sp[q];
     double dx = y.x - xi, dy = y.y - yi, dz = y.z - zi;
-    double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-    double ir = 1.0 / r;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
     dx *= ir; dy *= ir; dz *= ir;
     double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     ph.point(acc, r, ir, dx, dy, dz, dn, y.w);

@@ -78,7 +78,10 @@ struct MfArgs {
 };
 
 template <int K, bool USE_U>
-__global__ void __launch_bounds__(128) k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
+#ifndef EWB_MF_MINB
+#define EWB_MF_MINB 3
+#endif
+__global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
   __shared__ double s_geo[kMfTile][8];        // cx cy cz diam nx ny nz area
   __shared__ double s_y[kMfTile][30];         // 3 far + 7 mid points
   __shared__ cplx s_vt[kMfTile][K][3];
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(128) k_mf_farmid(Geo g, Phys<true> ph, MfArgs 
     for (int jj = 0; jj < tc; ++jj) {
       const int j = t0 + jj;
       if (j == i) continue;
-      const int tier = exact_tier(xi, yi, zi, s_geo[jj][0], s_geo[jj][1], s_geo[jj][2],
+      const int tier = exact_tier_fast(xi, yi, zi, s_geo[jj][0], s_geo[jj][1], s_geo[jj][2],
                                   s_geo[jj][3]);
       if (tier == 2) continue;
       const double nx = s_geo[jj][4], ny = s_geo[jj][5], nz = s_geo[jj][6], ar = s_geo[jj][7];
@@ -135,8 +138,9 @@ __global__ void __launch_bounds__(128) k_mf_farmid(Geo g, Phys<true> ph, MfArgs 
       acc_zero(acc);
       for (int q = 0; q < Q; ++q) {
         double dx = yq[3 * q] - xi, dy = yq[3 * q + 1] - yi, dz = yq[3 * q + 2] - zi;
-        double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-        double ir = 1.0 / r;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ir = rsqrt(r2);
+        double r = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
         double dn = fma(dz, nz, fma(dy, ny, dx * nx));
         ph.point(acc, r, ir, dx, dy, dz, dn, wq[q] * ar);
@@ -177,8 +181,9 @@ __global__ void __launch_bounds__(128) k_mf_near(Geo g, Phys<true> ph, MfArgs m,
     double dx = fma(b2, v[6], fma(b1, v[3], b0 * v[0])) - xi;
     double dy = fma(b2, v[7], fma(b1, v[4], b0 * v[1])) - yi;
     double dz = fma(b2, v[8], fma(b1, v[5], b0 * v[2])) - zi;
-    double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-    double ir = 1.0 / r;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
     dx *= ir; dy *= ir; dz *= ir;
     double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     ph.point(acc, r, ir, dx, dy, dz, dn, wq[q] * ar);
@@ -243,8 +248,9 @@ __global__ void __launch_bounds__(128) k_mf_self(Geo g, Phys<true> ph, MfArgs m)
   for (int q = lane; q < kSelfQ; q += 32) {
     double4 yq = sp[q];
     double dx = yq.x - xi, dy = yq.y - yi, dz = yq.z - zi;
-    double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-    double ir = 1.0 / r;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
     dx *= ir; dy *= ir; dz *= ir;
     double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     ph.point(acc, r, ir, dx, dy, dz, dn, yq.w);
@@ -397,8 +403,9 @@ __global__ void k_pair_blocks(const double* x, long long P, const double* tri, l
     double dx = fma(b2, v[6], fma(b1, v[3], b0 * v[0])) - xi;
     double dy = fma(b2, v[7], fma(b1, v[4], b0 * v[1])) - yi;
     double dz = fma(b2, v[8], fma(b1, v[5], b0 * v[2])) - zi;
-    double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-    double ir = 1.0 / r;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
     dx *= ir; dy *= ir; dz *= ir;
     double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     point_dynamic(acc, fc, r, ir, dx, dy, dz, dn, w7[q] * ar);
@@ -459,8 +466,9 @@ __global__ void __launch_bounds__(128) k_pair_reduce(const double* x, long long 
 #pragma unroll 1
       for (int q = 0; q < 7; ++q) {
         double dx = s_y[jj][3 * q] - xi, dy = s_y[jj][3 * q + 1] - yi, dz = s_y[jj][3 * q + 2] - zi;
-        double r = sqrt(fma(dz, dz, fma(dy, dy, dx * dx)));
-        double ir = 1.0 / r;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ir = rsqrt(r2);
+        double r = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
         double dn = fma(dz, nz, fma(dy, ny, dx * nx));
         point_dynamic(acc, fc, r, ir, dx, dy, dz, dn, w7r[q] * ar);
