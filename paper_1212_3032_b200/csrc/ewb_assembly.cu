@@ -360,26 +360,50 @@ __global__ void __launch_bounds__(128, 3) k_near(Geo g, Phys<DYN> ph, PairOut o,
     double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     ph.point(acc, r, ir, dx, dy, dz, dn, wq[q] * ar);
   }
-  acc_warp_sum(acc);
-  if (lane != 0) return;
-  S U[3][3], T[3][3];
-  acc_finalize(acc, nx, ny, nz, ph.i4pm(), ph.i4p(), U, T);
-  bool ok = true;
-  for (int a = 0; a < 3; ++a)
-    for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
-  if (!ok) o.flags[0] = 1;
+  // butterfly reduction: every lane holds the totals, then lanes 0..8 each
+  // finalise one block entry (a, c) in parallel (kernels.py:336-356)
+  acc_warp_allsum(acc);
+  const int a = lane / 3, c = lane % 3;
+  S u_ac, t_ac;
+  {
+    const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+    const double n[3] = {nx, ny, nz};
+    const int ac = lane < 9 ? sym[a][c] : 0;
+    const int aa = lane < 9 ? a : 0, cc = lane < 9 ? c : 0;
+    S pu = acc.P[ac];
+    u_ac = aa == cc ? acc.su - pu : -pu;
+    u_ac = ph.i4pm() * u_ac;
+    S t = acc.B[ac];
+    madd(t, n[aa], acc.va[cc]);
+    madd(t, n[cc], acc.vc[aa]);
+    if (aa == cc) t = t + acc.sa;
+    t_ac = ph.i4p() * t;
+  }
+  const bool ok = lane >= 9 || (finite(u_ac) && finite(t_ac));
+  if (!__all_sync(0xffffffffu, ok) && lane == 0) o.flags[0] = 1;
   if (OUT & OUT_TU) {
-    store_block((S*)o.T, N, i, j, T);
-    store_block((S*)o.U, N, i, j, U);
+    if (lane < 9) {
+      ((S*)o.T)[(size_t)(3 * i + a) * N + 3 * j + c] = t_ac;
+      ((S*)o.U)[(size_t)(3 * i + a) * N + 3 * j + c] = u_ac;
+    }
   }
   if constexpr (DYN && (OUT & OUT_SYS)) {
-    cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
-    sys_block(o.sys, N, i, j, U, T, bc);
-    for (int a = 0; a < 3; ++a) o.bnear[(size_t)3 * p + a] = bc[a];
+    // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
+    // Dirichlet column A = -U, b -= T p;  b summed over c = 0, 1, 2 in order
+    cplx bt = {0.0, 0.0};
+    if (lane < 9) {
+      const size_t col = 3 * (size_t)j + c;
+      const bool dir = o.sys.kinds[col] == kDirichlet;
+      const cplx pv = o.sys.p[col];
+      o.sys.A[(size_t)(3 * i + a) * N + col] = dir ? -u_ac : t_ac;
+      bt = dir ? -(t_ac * pv) : u_ac * pv;
+    }
+    const cplx b1 = {__shfl_down_sync(0xffffffffu, bt.re, 1), __shfl_down_sync(0xffffffffu, bt.im, 1)};
+    const cplx b2 = {__shfl_down_sync(0xffffffffu, bt.re, 2), __shfl_down_sync(0xffffffffu, bt.im, 2)};
+    if (lane < 9 && c == 0) o.bnear[(size_t)3 * p + a] = (cplx{0.0, 0.0} + bt + b1) + b2;
   }
   if constexpr (!DYN && (OUT & OUT_ROWSUM)) {
-    for (int a = 0; a < 3; ++a)
-      for (int b = 0; b < 3; ++b) o.snear[(size_t)9 * p + 3 * a + b] = to_c(T[a][b]).re;
+    if (lane < 9) o.snear[(size_t)9 * p + 3 * a + c] = to_c(t_ac).re;
   }
 }
 

@@ -390,6 +390,22 @@ __device__ __forceinline__ void warp_sum(double& v) {
 }
 __device__ __forceinline__ void warp_sum(cplx& v) { warp_sum(v.re); warp_sum(v.im); }
 
+__device__ __forceinline__ void warp_allsum(double& v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+}
+__device__ __forceinline__ void warp_allsum(cplx& v) { warp_allsum(v.re); warp_allsum(v.im); }
+
+// Butterfly variant: every lane ends with the (bitwise identical) totals.
+template <typename S>
+__device__ __forceinline__ void acc_warp_allsum(Acc<S>& A) {
+  warp_allsum(A.su); warp_allsum(A.sa);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { warp_allsum(A.P[k]); warp_allsum(A.B[k]); }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { warp_allsum(A.va[k]); warp_allsum(A.vc[k]); }
+}
+
 template <typename S>
 __device__ __forceinline__ void acc_warp_sum(Acc<S>& A) {
   warp_sum(A.su); warp_sum(A.sa);
