@@ -872,12 +872,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
 template <int K>
 __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
   const long long n = a.n, tid = gtid(), nth = gthreads();
-  extern __shared__ __align__(128) unsigned char ring_smem[];
-  __shared__ uint64_t ring_bar[kNS];
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
-  ring_init(ring, 16.0 * (double)n * (double)n > 96e6);
-  matvec_tma<K>(ring, a.A, n, a.X, a.Y);
-  grid.sync();
+  // Y = A X was produced by k_multi_gemv (its own launch: the K-vector
+  // matvec needs more registers than this cooperative kernel can give it)
   __shared__ int keep[kMaxSem];
   __shared__ cplx Rm[kMaxSem][kMaxSem];
   __shared__ int nkeep;
@@ -1067,7 +1063,47 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kSolveThreads), params, kRingBytes, s);
 }
 
+// Y = A X for K <= 4 columns in one TMA-streamed pass (SEM's products,
+// linsolve.py:228).  Regular launch, 1 CTA/SM, full register budget.
+template <int K>
+__global__ void __launch_bounds__(kSolveThreads, 1) k_multi_gemv(const cplx* A, const cplx* X,
+                                                                 cplx* Y, long long n) {
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
+  ring_init(ring, 16.0 * (double)n * (double)n > 96e6);
+  matvec_tma<K>(ring, A, n, X, Y);
+}
+
+template <int K>
+static cudaError_t launch_multi_gemv(const cplx* A, const cplx* X, cplx* Y, long long n,
+                                     cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)k_multi_gemv<K>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBytes);
+    attr = true;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long groups = (n + kRR - 1) / kRR;
+  unsigned blocks = (unsigned)(groups < sms ? groups : sms);
+  EWB_NOTE k_multi_gemv<K><<<blocks, kSolveThreads, kRingBytes, s>>>(A, X, Y, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
+  // Measured: the K-vector matvec spills beyond K = 2 under the 128-register
+  // cap of a 512-thread CTA (K=4 in one pass: 2.04 ms at n=15360), so the
+  // columns go two at a time.
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < args.K && e == cudaSuccess; c += 2) {
+    const long long off = (long long)c * args.n;
+    if (args.K - c >= 2) e = launch_multi_gemv<2>(args.A, args.X + off, args.Y + off, args.n, s);
+    else e = launch_multi_gemv<1>(args.A, args.X + off, args.Y + off, args.n, s);
+  }
+  if (e != cudaSuccess) return e;
   int G = solver_grid_blocks();
   void* params[] = {&args};
   note_launch();
