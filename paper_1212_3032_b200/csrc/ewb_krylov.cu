@@ -750,13 +750,17 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
       const double hn = sqrt(q[0]);
       // Givens (linsolve.py:171-194), identical in every CTA
       if (threadIdx.x == 0) {
-        for (int i = 0; i <= j; ++i) gs.h[i] = s_h[i];
-        gs.h[j + 1] = {hn, 0.0};
+        // apply the previous rotations; only `carry` (the running h_i) is
+        // on the dependency chain
+        cplx carry = s_h[0];
+#pragma unroll 4
         for (int i = 0; i < j; ++i) {
-          cplx top = gs.cs[i] * gs.h[i] + gs.sn[i] * gs.h[i + 1];
-          gs.h[i + 1] = (-conj(gs.sn[i])) * gs.h[i] + conj(gs.cs[i]) * gs.h[i + 1];
-          gs.h[i] = top;
+          const cplx c = gs.cs[i], sn = gs.sn[i], hn1 = s_h[i + 1];
+          gs.h[i] = c * carry + sn * hn1;
+          carry = (-conj(sn)) * carry + conj(c) * hn1;
         }
+        gs.h[j] = carry;
+        gs.h[j + 1] = {hn, 0.0};
         double ahj = hypot(gs.h[j].re, gs.h[j].im), ahn = hypot(gs.h[j + 1].re, gs.h[j + 1].im);
         double den = sqrt(ahj * ahj + ahn * ahn);
         if (den == 0.0) {
@@ -851,6 +855,612 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
     }
     grid_sum(grid, R, q2);
     rnorm = sqrt(q2[0]);
+    res = rnorm / nb;
+  }
+  if (tid == 0) {
+    a.out->iterations = its;
+    a.out->final_res = res;
+    a.out->converged = res <= a.tol;
+    a.out->n_hist = n_hist;
+    a.out->matvecs = n_mv;
+  }
+}
+
+// ---------------------------------------------------------------------
+// Balanced row-block matvec with a per-block epilogue.
+//
+// CTA b owns the contiguous rows [b n / G, (b+1) n / G) (at most one row of
+// imbalance, where the round-robin 16-row groups above leave up to 8 %),
+// cut into ceil(R / kRR) near-equal blocks.  Each block streams through the
+// same TMA ring; x is read one stage ahead so its L2 latency overlaps the
+// current stage.  When a block's last column tile is consumed its per-row
+// sums land in s_sum[row][k] and epi(row0, nrows, s_sum) runs on all
+// threads (CTA-uniform), so vector work on the block's rows (scaling,
+// residuals, partial dot products) happens while the next stages are
+// already in flight.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& r1) {
+  r0 = (long long)blockIdx.x * n / gridDim.x;
+  r1 = (long long)(blockIdx.x + 1) * n / gridDim.x;
+}
+
+template <int K, typename Epi>
+__device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
+                            long long r0, long long r1, Epi&& epi) {
+  __shared__ cplx s_red[kSolveWarps][kRpt][K];
+  __shared__ cplx s_sum[kRR][K];
+  const long long rows = r1 - r0;
+  if (rows <= 0) return;
+  const int nblk = (int)((rows + kRR - 1) / kRR);
+  const int ntile = (int)((n + kTC - 1) / kTC);
+  const int S = nblk * ntile;
+  const int last_tc = (int)(n - (long long)(ntile - 1) * kTC);
+  // block q covers rows [r0 + q rows / nblk, r0 + (q+1) rows / nblk); stage
+  // s = q ntile + t.  Coordinates advance incrementally (no 64-bit division
+  // per stage).
+  auto block_rows = [&](int q, long long& row0, int& nrows) {
+    row0 = r0 + (long long)q * rows / nblk;
+    nrows = (int)(r0 + (long long)(q + 1) * rows / nblk - row0);
+  };
+  // producer state (thread 0): next stage to issue
+  int pq = 0, pt = 0;
+  long long prow0 = 0;
+  int pnrows = 0;
+  auto issue_next = [&](unsigned pos) {
+    if (pt == 0) block_rows(pq, prow0, pnrows);
+    const int tc = pt == ntile - 1 ? last_tc : kTC;
+    ring_issue(R, pos, A, n, prow0, pnrows, (long long)pt * kTC, tc);
+    if (++pt == ntile) { pt = 0; ++pq; }
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int s = 0; s < S && s < kNS; ++s) issue_next(R.pos + (unsigned)s);
+  }
+  const int col = threadIdx.x % kTC, slice = threadIdx.x / kTC;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  cplx acc[kRpt][K];
+#pragma unroll
+  for (int r = 0; r < kRpt; ++r)
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
+  cplx xn[K];  // x for the stage being consumed (prefetched one stage ahead)
+#pragma unroll
+  for (int k = 0; k < K; ++k) xn[k] = col < n ? ldg(x + k * n + col) : cplx{0.0, 0.0};
+  int q = 0, t = 0;
+  long long row0;
+  int nrows;
+  block_rows(0, row0, nrows);
+  for (int s = 0; s < S; ++s) {
+    const long long c0 = (long long)t * kTC;
+    const int tc = t == ntile - 1 ? last_tc : kTC;
+    cplx xv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) xv[k] = xn[k];
+    {  // prefetch the next stage's x
+      const long long cn = (t == ntile - 1 ? 0 : c0 + kTC) + col;
+#pragma unroll
+      for (int k = 0; k < K; ++k) xn[k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
+    }
+    const unsigned pos = R.pos + (unsigned)s;
+    ring_wait(R, pos);
+    if (col < tc) {
+      const cplx* tile = R.buf + (size_t)(pos % kNS) * kStageElems;
+#pragma unroll
+      for (int r = 0; r < kRpt; ++r) {
+        const int row = slice * kRpt + r;
+        if (row < nrows) {
+          double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + col);
+          cplx av = {a2.x, a2.y};
+#pragma unroll
+          for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[k]);
+        }
+      }
+    }
+    __syncthreads();  // every consumer is done with this stage's buffer
+    if (threadIdx.x == 0 && s + kNS < S) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_next(pos + kNS);
+    }
+    if (t == ntile - 1) {  // last tile of the block: reduce, then the epilogue
+#pragma unroll
+      for (int r = 0; r < kRpt; ++r)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          warp_sum(acc[r][k]);
+          if (lane == 0) s_red[wid][r][k] = acc[r][k];
+          acc[r][k] = {0.0, 0.0};
+        }
+      __syncthreads();
+      if (threadIdx.x < kRR * K) {
+        const int row = threadIdx.x / K, k = threadIdx.x % K;
+        const int h = row / kRpt, r = row % kRpt;
+        constexpr int wps = kSolveWarps / kSlices;  // warps per row slice
+        cplx sum = {0.0, 0.0};
+        for (int w = 0; w < wps; ++w) sum = sum + s_red[h * wps + w][r][k];
+        s_sum[row][k] = sum;
+      }
+      __syncthreads();
+      epi(row0, nrows, s_sum);
+      __syncthreads();
+      t = 0;
+      if (++q < nblk) block_rows(q, row0, nrows);
+    } else {
+      ++t;
+    }
+  }
+  R.pos += (unsigned)S;
+}
+
+// Fixed-order reduction of `cnt` CTA partials (layout part[b * stride + t]):
+// 8 threads per value, thread `sub` summing CTAs sub, sub + 8, ... with all
+// of its loads issued before the first add (one L2 round trip per round
+// instead of one per CTA), then a 3-step shuffle.  Identical in every CTA.
+constexpr int kRedPer = 20;  // partial loads per thread: grids up to 160 CTAs
+
+__device__ void reduce_parts(const cplx* part, int stride, int cnt, cplx* out) {
+  const int sub = threadIdx.x & 7;
+  const int G = gridDim.x;
+  for (int base = 0; base < cnt; base += kSolveThreads / 8) {
+    const int t = base + (threadIdx.x >> 3);
+    cplx s = {0.0, 0.0};
+    if (t < cnt) {
+      if (G <= 8 * kRedPer) {
+        cplx v[kRedPer];
+#pragma unroll
+        for (int i = 0; i < kRedPer; ++i) {
+          const int b = sub + 8 * i;
+          v[i] = b < G ? part[(size_t)b * stride + t] : cplx{0.0, 0.0};
+        }
+#pragma unroll
+        for (int i = 0; i < kRedPer; ++i) s = s + v[i];
+      } else {
+        for (int b = sub; b < G; b += 8) s = s + part[(size_t)b * stride + t];
+      }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
+      s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
+    }
+    if (sub == 0 && t < cnt) out[t] = s;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------
+// GMRES with the Arnoldi vector work fused around the matvec (default,
+// GmresArgs::ortho == 0).  Same algorithm as k_gmres (one-reduction MGS,
+// linsolve.py:150-170 up to association), restructured so that an Arnoldi
+// step costs one pass over A plus two grid barriers:
+//
+//   matvec   w = (A z') / h_{j,j-1} over the CTA's own rows; each finished
+//            row block immediately adds <V_t, w>, t <= j, to CTA partials
+//   S1       grid barrier
+//   reduce   d_t and Gram row j (fixed order, every CTA); h = (I + L)^{-1} d
+//            as d - L (d - L d), exact to O(|L|^3) with |L| the basis's loss
+//            of orthogonality (~1e-15)
+//   update   u = w - sum_i h_i V_i over own rows (+ the <= 2 rows completing
+//            the last owned element), |u|^2 and <u, V_l> partials (the next
+//            Gram row), z' = P^{-1} u for owned elements
+//   S2       grid barrier
+//   Givens   h_{j+1,j} = |u| (fixed-order reduce), rotations, residual
+//            estimate; V_{j+1} = u / h_{j+1,j} written by the owning CTA
+//
+// The basis vector is normalised lazily: the next matvec runs on the
+// unnormalised z' and scales its rows, so the norm reduction shares the
+// barrier with the update instead of costing one of its own.
+// ---------------------------------------------------------------------
+constexpr int kNormSlot = kMaxDots - 1;
+constexpr int kGrp = kRR <= 16 ? 16 : 32;  // lanes per epilogue dot
+
+// sum over aligned groups of G lanes (result in every lane of the group)
+template <int G>
+__device__ __forceinline__ void group_sum(cplx& v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
+    v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
+  }
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_f(GmresArgs a) {
+  int n_probe = 0;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  __shared__ GivensShared gs;
+  __shared__ cplx s_y[kMaxRestart];
+  __shared__ cplx s_dots[kMaxDots];
+  __shared__ cplx s_h[kMaxRestart + 1];
+  __shared__ cplx s_h1[kMaxRestart + 1];
+  __shared__ cplx s_dacc[kMaxRestart + 1];
+  __shared__ cplx s_wblk[kRR];
+  __shared__ double s_nrm[kSolveWarps];
+  __shared__ double s_est;
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
+  ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
+  const long long n = a.n;
+  const long long tid = gtid(), nth = gthreads();
+  const bool pc = a.pinv != nullptr;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long k0, k1;
+  cta_rows(n, k0, k1);
+  // rows whose u this CTA computes: own rows plus the tail of the last
+  // element it owns (element e is owned by the CTA owning row 3e)
+  const long long e0 = pc ? (k0 + 2) / 3 : k0, e1 = pc ? (k1 + 2) / 3 : k1;
+  const long long ka = k0, kb = pc ? max(k1, 3 * e1) : k1;
+  const int RU = (int)(kb - ka);
+  GridRed R{a.partial, 0};
+  int dpar = 0;
+  auto part_buf = [&](int p) { return a.dpart + (size_t)p * gridDim.x * kMaxDots; };
+
+  // CTA-sum of one double per thread -> part[kNormSlot].re of buffer p
+  auto cta_norm_partial = [&](double q, int p) {
+    warp_sum(q);
+    if (lane == 0) s_nrm[wid] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kSolveWarps; ++w) s += s_nrm[w];
+      part_buf(p)[(size_t)blockIdx.x * kMaxDots + kNormSlot] = {s, 0.0};
+    }
+  };
+  // every CTA: sum of the kNormSlot partials of buffer p (fixed order)
+  auto grid_norm = [&](int p) -> double {
+    const cplx* part = part_buf(p);
+    if (wid == 0) {
+      double v[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int b = lane + 32 * i;
+        v[i] = b < (int)gridDim.x ? part[(size_t)b * kMaxDots + kNormSlot].re : 0.0;
+      }
+      double s = (((v[0] + v[1]) + v[2]) + v[3]) + v[4];
+      for (int b = lane + 160; b < (int)gridDim.x; b += 32) s += part[(size_t)b * kMaxDots + kNormSlot].re;
+      warp_sum(s);
+      if (lane == 0) s_est = s;
+    }
+    __syncthreads();
+    const double v = s_est;
+    __syncthreads();
+    return v;
+  };
+  // r = b - A x over own rows (a.r), |r|^2 partial into buffer p; ends with
+  // a grid barrier, returns |r|
+  auto residual = [&](int p) -> double {
+    double q = 0.0;
+    matvec_rows<1>(ring, a.A, n, a.x, k0, k1, [&](long long row0, int nr, cplx (*sum)[1]) {
+      if (threadIdx.x < nr) {
+        const cplx r = a.b[row0 + threadIdx.x] - sum[threadIdx.x][0];
+        a.r[row0 + threadIdx.x] = r;
+        q += abs2(r);
+      }
+    });
+    cta_norm_partial(q, p);
+    grid.sync();
+    return sqrt(grid_norm(p));
+  };
+
+  // ||b|| and "x0 has a nonzero entry", one reduction
+  double v2[2] = {0.0, 0.0};
+  for (long long k = tid; k < n; k += nth) {
+    v2[0] += abs2(a.b[k]);
+    if (a.has_x0) v2[1] += (a.x[k].re != 0.0 || a.x[k].im != 0.0);
+    else a.x[k] = {0.0, 0.0};
+  }
+  grid_sum(grid, R, v2);
+  const double nb = sqrt(v2[0]);
+  if (nb == 0.0) {  // linsolve.py:136-140
+    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
+    if (tid == 0) { a.out->iterations = 0; a.out->init_res = 0; a.out->final_res = 0;
+                    a.out->n_hist = 0; a.out->converged = 1; a.out->matvecs = 0; }
+    return;
+  }
+  int n_mv = 0;
+  double rnorm;
+  if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
+    rnorm = residual(dpar);
+    dpar ^= 1;
+    ++n_mv;
+  } else {
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) a.r[k] = a.b[k];
+    rnorm = nb;
+    grid.sync();
+  }
+  double res = rnorm / nb;
+  int n_hist = 0;
+  if (tid == 0) { a.out->init_res = res; a.hist[0] = res; }
+  n_hist++;
+  int its = 0;
+  cplx* const scr = ring.buf;  // idle ring = scratch between matvecs
+  while (res > a.tol && its < a.maxiter) {
+    const int m = min(a.restart, a.maxiter - its);
+    // cycle start: u = r, h = beta; z' = P^{-1} r for owned elements
+    const double beta = rnorm;
+    if (pc) {
+      for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        cplx v[3] = {a.r[3 * e], a.r[3 * e + 1], a.r[3 * e + 2]};
+        precond_regs(a.pinv, e, v, a.z);
+      }
+    } else {
+      for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) a.z[k] = a.r[k];
+    }
+    if (threadIdx.x == 0) {
+      gs.g[0] = {beta, 0.0};
+      for (int k = 1; k <= m; ++k) gs.g[k] = {0.0, 0.0};
+    }
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+      a.V[k] = {a.r[k].re / beta, a.r[k].im / beta};
+    grid.sync();
+    double hprev = beta;
+    int used = 0;
+    for (int j = 0;; ++j) {
+      // ---- matvec + <V_t, w> partials ------------------------------------
+      const double sc = 1.0 / hprev;
+      for (int t = threadIdx.x; t <= j; t += blockDim.x) s_dacc[t] = {0.0, 0.0};
+      __syncthreads();
+      EWB_PROBE(2);
+      matvec_rows<1>(ring, a.A, n, a.z, k0, k1, [&](long long row0, int nr, cplx (*sum)[1]) {
+        if (threadIdx.x < nr) {
+          const cplx w = sum[threadIdx.x][0] * sc;
+          a.w[row0 + threadIdx.x] = w;
+          s_wblk[threadIdx.x] = w;
+        }
+        __syncthreads();
+        // kGrp lanes per dot (one row each), kSolveThreads / kGrp dots per round
+        const int sub = threadIdx.x % kGrp;
+        for (int t0 = 0; t0 <= j; t0 += 2 * (kSolveThreads / kGrp)) {
+          const int ta = t0 + threadIdx.x / kGrp, tb = ta + kSolveThreads / kGrp;
+          const bool ok = sub < nr;
+          cplx va = ok && ta <= j ? a.V[(size_t)ta * n + row0 + sub] : cplx{0.0, 0.0};
+          cplx vb = ok && tb <= j ? a.V[(size_t)tb * n + row0 + sub] : cplx{0.0, 0.0};
+          const cplx wv = ok ? s_wblk[sub] : cplx{0.0, 0.0};
+          cplx sa = conj(va) * wv, sb = conj(vb) * wv;
+          group_sum<kGrp>(sa);
+          group_sum<kGrp>(sb);
+          if (sub == 0) {
+            if (ta <= j) s_dacc[ta] = s_dacc[ta] + sa;
+            if (tb <= j) s_dacc[tb] = s_dacc[tb] + sb;
+          }
+        }
+      });
+      ++n_mv;
+      cplx* part = part_buf(dpar);
+      for (int t = threadIdx.x; t <= j; t += blockDim.x)
+        part[(size_t)blockIdx.x * kMaxDots + t] = s_dacc[t];
+      EWB_PROBE(3);
+      if (a.probe && threadIdx.x == 0 && j < 100 && its == j)  // per-CTA matvec finish (cycle 0)
+        a.probe[32768 + j * gridDim.x + blockIdx.x] = gtimer();
+      // Gram rows 1..j-1 (written in earlier steps) staged into the idle
+      // ring while other CTAs finish their matvec
+      cplx* gsm = scr;
+      {
+        const int tri = j * (j - 1) / 2;
+        for (int q = threadIdx.x; q < tri; q += blockDim.x) {
+          // packed index q -> (i, l), i >= 1, l < i
+          int i = (int)((1.0 + sqrt(1.0 + 8.0 * q)) * 0.5);
+          while (i * (i - 1) / 2 > q) --i;
+          while ((i + 1) * i / 2 <= q) ++i;
+          const int l = q - i * (i - 1) / 2;
+          gsm[q] = a.Gram[(size_t)i * kMaxRestart + l];
+        }
+      }
+      grid.sync();  // S1
+      EWB_PROBE(4);
+      // ---- d_t and Gram row j; h = (I + L)^{-1} d --------------------------
+      {
+        // reduce-scatter (CTA b sums value t = b mod G over the CTA partials
+        // in a fixed order) + barrier + all-gather: every partial is read
+        // once instead of once per CTA
+        cplx* fin = reinterpret_cast<cplx*>(a.partial);
+        const int cnt = 2 * j + 1;
+#ifdef EWB_DBG_WARM
+        for (int rep = 0; rep < 2; ++rep) {
+        if (rep) EWB_PROBE(15);
+#endif
+        for (int t = blockIdx.x + wid * gridDim.x; t < cnt; t += kSolveWarps * gridDim.x) {
+          cplx v[5];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            const int b = lane + 32 * i;
+            v[i] = b < (int)gridDim.x ? part[(size_t)b * kMaxDots + t] : cplx{0.0, 0.0};
+          }
+          cplx sum = (((v[0] + v[1]) + v[2]) + v[3]) + v[4];
+          for (int b = lane + 160; b < (int)gridDim.x; b += 32) sum = sum + part[(size_t)b * kMaxDots + t];
+          warp_sum(sum);
+          if (lane == 0) fin[t] = t > j ? sum * sc : sum;  // <u, V_l> / h = <v_j, V_l>
+        }
+#ifdef EWB_DBG_WARM
+        __syncthreads();
+        }
+#endif
+        EWB_PROBE(11);
+        grid.sync();  // S1b
+        EWB_PROBE(12);
+        for (int t = threadIdx.x; t < cnt; t += blockDim.x) s_dots[t] = fin[t];
+        __syncthreads();
+        EWB_PROBE(8);
+        if (blockIdx.x == 0)
+          for (int l = threadIdx.x; l < j; l += blockDim.x)
+            a.Gram[(size_t)j * kMaxRestart + l] = s_dots[j + 1 + l];
+        // h = d - L (d - L d): two Jacobi sweeps, warp per row
+        for (int sweep = 0; sweep < 2; ++sweep) {
+          const cplx* hin = sweep == 0 ? s_dots : s_h1;
+          cplx* hout = sweep == 0 ? s_h1 : s_h;
+          for (int i = wid; i <= j; i += kSolveWarps) {
+            cplx s = {0.0, 0.0};
+            for (int l = lane; l < i; l += 32) {
+              const cplx g = i == j ? s_dots[j + 1 + l] : gsm[i * (i - 1) / 2 + l];
+              s = s + g * hin[l];
+            }
+            warp_sum(s);
+            if (lane == 0) hout[i] = s_dots[i] - s;
+          }
+          __syncthreads();
+          EWB_PROBE(9 + sweep);
+        }
+      }
+      EWB_PROBE(5);
+      // ---- update: u = w - sum_i h_i V_i over [ka, kb) --------------------
+      {
+        const int nv = j + 1;
+        const int nc = max(1, min(nv, kSolveThreads / max(RU, 1)));
+        cplx* pu = scr;            // [nc][RU] chunk partials
+        cplx* su = scr + nc * RU;  // [RU] u
+        for (int p = threadIdx.x; p < nc * RU; p += blockDim.x) {
+          const int r = p % RU, c = p / RU;
+          const int i0 = c * nv / nc, i1 = (c + 1) * nv / nc;
+          cplx s = {0.0, 0.0};
+#pragma unroll 8
+          for (int i = i0; i < i1; ++i) cfma(s, s_h[i], a.V[(size_t)i * n + ka + r]);
+          pu[p] = s;
+        }
+        __syncthreads();
+        double q = 0.0;
+        for (int r = threadIdx.x; r < RU; r += blockDim.x) {
+          cplx u = a.w[ka + r];
+          for (int c = 0; c < nc; ++c) u = u - pu[c * RU + r];
+          su[r] = u;
+          if (ka + r < k1) {
+            a.r[ka + r] = u;
+            q += abs2(u);
+          }
+        }
+        __syncthreads();
+        if (pc) {
+          for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+            const cplx* u = su + (3 * e - ka);
+            cplx v[3] = {u[0], u[1], u[2]};
+            precond_regs(a.pinv, e, v, a.z);
+          }
+        } else {
+          for (int r = threadIdx.x; r < RU; r += blockDim.x) a.z[ka + r] = su[r];
+        }
+        // next Gram row: <u, V_l>, l <= j, over own rows
+        cplx* pn = part_buf(dpar ^ 1);
+        const int own = (int)(k1 - k0);
+        {
+          const int sub = threadIdx.x & 15;
+          for (int l0 = 0; l0 <= j; l0 += kSolveThreads / 16) {  // warp-uniform trip count
+            const int l = l0 + (threadIdx.x >> 4);
+            cplx s = {0.0, 0.0};
+            if (l <= j) {
+#pragma unroll 8
+              for (int r = sub; r < own; r += 16) cfma(s, conj(su[r]), a.V[(size_t)l * n + k0 + r]);
+            }
+            group_sum<16>(s);
+            if (sub == 0 && l <= j) pn[(size_t)blockIdx.x * kMaxDots + (j + 2) + l] = s;
+          }
+        }
+        cta_norm_partial(q, dpar ^ 1);
+      }
+      dpar ^= 1;
+      EWB_PROBE(6);
+      grid.sync();  // S2
+      EWB_PROBE(13);
+      const double hn = sqrt(grid_norm(dpar));
+      EWB_PROBE(14);
+      // Givens (linsolve.py:171-194), identical in every CTA
+      if (threadIdx.x == 0) {
+        // apply the previous rotations; only `carry` (the running h_i) is
+        // on the dependency chain
+        cplx carry = s_h[0];
+#pragma unroll 4
+        for (int i = 0; i < j; ++i) {
+          const cplx c = gs.cs[i], sn = gs.sn[i], hn1 = s_h[i + 1];
+          gs.h[i] = c * carry + sn * hn1;
+          carry = (-conj(sn)) * carry + conj(c) * hn1;
+        }
+        gs.h[j] = carry;
+        gs.h[j + 1] = {hn, 0.0};
+        double ahj = hypot(gs.h[j].re, gs.h[j].im), ahn = hypot(gs.h[j + 1].re, gs.h[j + 1].im);
+        double den = sqrt(ahj * ahj + ahn * ahn);
+        if (den == 0.0) {
+          gs.cs[j] = {1.0, 0.0}; gs.sn[j] = {0.0, 0.0};
+        } else if (gs.h[j].re == 0.0 && gs.h[j].im == 0.0) {
+          gs.cs[j] = {0.0, 0.0}; gs.sn[j] = {1.0, 0.0};
+        } else {
+          gs.cs[j] = {ahj / den, 0.0};
+          cplx ph = {gs.h[j].re / ahj, gs.h[j].im / ahj};
+          cplx t = ph * conj(gs.h[j + 1]);
+          gs.sn[j] = {t.re / den, t.im / den};
+        }
+        gs.h[j] = gs.cs[j] * gs.h[j] + gs.sn[j] * gs.h[j + 1];
+        gs.h[j + 1] = {0.0, 0.0};
+        gs.g[j + 1] = (-conj(gs.sn[j])) * gs.g[j];
+        gs.g[j] = gs.cs[j] * gs.g[j];
+        s_est = hypot(gs.g[j + 1].re, gs.g[j + 1].im) / nb;
+        if (blockIdx.x == 0)
+          for (int i = 0; i <= j; ++i) a.H[(size_t)i * kMaxRestart + j] = gs.h[i];
+      }
+      __syncthreads();
+      EWB_PROBE(7);
+      ++its;
+      used = j + 1;
+      const double est = s_est;
+      if (tid == 0 && n_hist < a.hist_cap) a.hist[n_hist] = est;
+      n_hist++;
+      if (est <= a.tol || j + 1 == m) break;
+      // V_{j+1} = u / h_{j+1,j} on own rows (u kept in a.r)
+      if (hn > 0.0) {
+        cplx* vn = a.V + (size_t)(j + 1) * n;
+        for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+          vn[k] = {a.r[k].re / hn, a.r[k].im / hn};
+      }
+      hprev = hn > 0.0 ? hn : 1.0;
+      __syncthreads();
+    }
+    grid.sync();  // H visible to every CTA before the back substitution
+    // back substitution (linsolve.py:196-198): warp 0 of every CTA, with
+    // the upper triangle of H staged (packed) into the idle ring first.
+    {
+      cplx* hsm = ring.buf;
+      for (int i = 0; i < used; ++i)
+        for (int k = i + threadIdx.x; k < used; k += blockDim.x)
+          hsm[i * used - i * (i - 1) / 2 + (k - i)] = a.H[(size_t)i * kMaxRestart + k];
+      __syncthreads();
+      if (wid == 0) {
+        for (int i = used - 1; i >= 0; --i) {
+          const cplx* row = hsm + i * used - i * (i - 1) / 2 - i;
+          cplx s = {0.0, 0.0};
+          for (int k = i + 1 + lane; k < used; k += 32) s = s + row[k] * s_y[k];
+          warp_sum(s);
+          if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, row[i]);
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+    }
+    // x += P^{-1} (V y), per owned element (or own row)
+    {
+      const long long ua = pc ? e0 : k0, ub = pc ? e1 : k1;
+      const int ucnt = pc ? 3 : 1;
+      for (long long u = ua + threadIdx.x; u < ub; u += blockDim.x) {
+        cplx uv[3];
+        for (int c = 0; c < ucnt; ++c) {
+          const long long k = u * ucnt + c;
+          cplx s = {0.0, 0.0};
+#pragma unroll 8
+          for (int i = 0; i < used; ++i) cfma(s, a.V[(size_t)i * n + k], s_y[i]);
+          uv[c] = s;
+        }
+        if (pc) {
+          const cplx* P = a.pinv + 9 * u;
+          for (int r = 0; r < 3; ++r) {
+            cplx s = P[3 * r] * uv[0];
+            s = s + P[3 * r + 1] * uv[1];
+            s = s + P[3 * r + 2] * uv[2];
+            a.x[3 * u + r] = a.x[3 * u + r] + s;
+          }
+        } else {
+          a.x[u] = a.x[u] + uv[0];
+        }
+      }
+    }
+    grid.sync();
+    rnorm = residual(dpar);  // true residual (linsolve.py:200-201)
+    dpar ^= 1;
+    ++n_mv;
     res = rnorm / nb;
   }
   if (tid == 0) {
@@ -998,7 +1608,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gemv_tma(const cplx* A, co
   Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, true);
   const size_t sys = blockIdx.y;
-  matvec_tma<1>(ring, A + sys * n * n, n, x + sys * n, y + sys * n);
+  cplx* ys = y + sys * n;
+  long long r0, r1;
+  cta_rows(n, r0, r1);
+  matvec_rows<1>(ring, A + sys * n * n, n, x + sys * n, r0, r1,
+                 [&](long long row0, int nr, cplx (*sum)[1]) {
+                   if (threadIdx.x < nr) ys[row0 + threadIdx.x] = sum[threadIdx.x][0];
+                 });
 }
 
 // Plain batched GEMV y_b = A_b x_b (one launch, `batch` systems of size n).
@@ -1048,9 +1664,10 @@ static int coop_grid(const void* fn) {
 int solver_grid_blocks() {
   if (g_coop_blocks == 0) {
     int a = coop_grid((const void*)k_gmres), b = coop_grid((const void*)k_sem);
-    int c = coop_grid((const void*)k_gmres_mgs);
+    int c = coop_grid((const void*)k_gmres_mgs), d = coop_grid((const void*)k_gmres_f);
     g_coop_blocks = a < b ? a : b;
     g_coop_blocks = c < g_coop_blocks ? c : g_coop_blocks;
+    g_coop_blocks = d < g_coop_blocks ? d : g_coop_blocks;
   }
   return g_coop_blocks;
 }
@@ -1059,7 +1676,9 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
   note_launch();
-  const void* fn = args.ortho == 1 ? (const void*)k_gmres_mgs : (const void*)k_gmres;
+  const void* fn = args.ortho == 1   ? (const void*)k_gmres_mgs
+                   : args.ortho == 2 ? (const void*)k_gmres
+                                     : (const void*)k_gmres_f;
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kSolveThreads), params, kRingBytes, s);
 }
 
@@ -1072,7 +1691,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_multi_gemv(const cplx* A, 
   __shared__ uint64_t ring_bar[kNS];
   Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, 16.0 * (double)n * (double)n > 96e6);
-  matvec_tma<K>(ring, A, n, X, Y);
+  long long r0, r1;
+  cta_rows(n, r0, r1);
+  matvec_rows<K>(ring, A, n, X, r0, r1, [&](long long row0, int nr, cplx (*sum)[K]) {
+    if (threadIdx.x < nr * K) {
+      const int row = threadIdx.x / K, k = threadIdx.x % K;
+      Y[k * n + row0 + row] = sum[row][k];
+    }
+  });
 }
 
 template <int K>
@@ -1087,8 +1713,7 @@ static cudaError_t launch_multi_gemv(const cplx* A, const cplx* X, cplx* Y, long
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  long long groups = (n + kRR - 1) / kRR;
-  unsigned blocks = (unsigned)(groups < sms ? groups : sms);
+  unsigned blocks = (unsigned)sms;
   EWB_NOTE k_multi_gemv<K><<<blocks, kSolveThreads, kRingBytes, s>>>(A, X, Y, n);
   return cudaGetLastError();
 }
@@ -1122,8 +1747,7 @@ cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long
                          kRingBytes);
     attr = true;
   }
-  long long groups = (n + kRR - 1) / kRR;
-  long long blocks = groups < sms ? groups : sms;
+  long long blocks = sms;
   EWB_NOTE k_gemv_tma<<<dim3((unsigned)blocks, batch), kSolveThreads, kRingBytes, s>>>(A, x, y, n);
   return cudaGetLastError();
 }

@@ -36,7 +36,8 @@ struct GmresArgs {
   GmresOut* out;
   long long n;
   int restart, maxiter, has_x0, hist_cap;
-  int ortho;            // 0: one-reduction MGS (default), 1: sequential MGS
+  int ortho;            // 0: fused one-reduction MGS (default), 1: sequential MGS,
+                        // 2: one-reduction MGS with separate vector phases
   unsigned long long* probe;  // optional phase trace (CTA 0): (phase << 56) | globaltimer
   int probe_cap;
   double tol;

@@ -32,6 +32,11 @@ def timed(fn, reps=3):
 gemv = timed(lambda: _lib.check(lib.ewb_gemv_batched(_lib.ptr(A), _lib.ptr(b), _lib.ptr(y), n, 1,
                                                      _lib.stream_handle())), 10)
 print(f"gemv {gemv:.4f} ms  {16 * n * n / gemv / 1e6:.1f} GB/s")
+import os  # noqa: E402
+pinv = None
+if os.environ.get("PC"):
+    pinv = torch.eye(3, dtype=torch.complex128, device="cuda").repeat(n // 3, 1, 1)
+    pinv += 0.01 * torch.randn(pinv.shape, dtype=torch.complex128, device="cuda", generator=g)
 ws = _Workspace()
 for m in (1, 10, 30, 59):
     x = torch.zeros(n, dtype=torch.complex128, device="cuda")
@@ -39,7 +44,7 @@ for m in (1, 10, 30, 59):
 
     def run():
         x.zero_()
-        stats["st"] = gmres_device(A, b, x, False, 1e-300 if False else 1e-15, 60, m, None, ws=ws,
+        stats["st"] = gmres_device(A, b, x, False, 1e-300 if False else 1e-15, 60, m, pinv, ws=ws,
                                    sync=False)
 
     ms = timed(run)

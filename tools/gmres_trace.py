@@ -32,7 +32,7 @@ probe.zero_()
 x.zero_()
 gmres_device(A, b, x, False, 1e-15, 60, m, None, ws=ws)
 torch.cuda.synchronize()
-p = probe.cpu().numpy().astype(np.uint64)
+p = probe.cpu().numpy()[:32768].astype(np.uint64)
 p = p[p != 0]
 ids = (p >> np.uint64(56)).astype(int)
 ts = (p & np.uint64((1 << 56) - 1)).astype(np.int64)
@@ -43,3 +43,21 @@ print(f"n={n} its={m} traced {(ts[-1] - ts[0]) / 1e3:.1f} us")
 for (a_, b_), v in sorted(acc.items(), key=lambda kv: -sum(kv[1])):
     print(f"{a_:3d} -> {b_:3d}  n={len(v):3d}  mean {np.mean(v) / 1e3:8.2f} us  "
           f"total {sum(v) / 1e3:9.1f} us")
+
+# per-CTA matvec finish times (first cycle), relative to the earliest CTA
+P = probe.cpu().numpy()[32768:].astype(np.int64)
+G = 148
+rows = []
+for j in range(min(m, 100)):
+    t = P[j * G:(j + 1) * G]
+    if (t == 0).any():
+        break
+    rows.append(t - t.min())
+if rows:
+    R = np.array(rows) / 1e3
+    print(f"matvec finish spread per step: mean max-min {R.max(1).mean():.2f} us, "
+          f"median CTA lag {np.median(R, 1).mean():.2f} us")
+    lag = R[1:].mean(0)
+    order = np.argsort(-lag)
+    print("slowest CTAs (mean lag us):", [(int(b), round(float(lag[b]), 2)) for b in order[:12]])
+    print("fastest CTAs:", [(int(b), round(float(lag[b]), 2)) for b in order[-6:]])
