@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EWB_ABI_VERSION 1
+#define EWB_ABI_VERSION 2
 
 enum ewb_status {
   EWB_OK = 0,
@@ -116,6 +116,10 @@ int ewb_assemble_system(ewb_ctx* ctx, double omega_re, double omega_im,
 /* Read and clear the context's fault flags (non-finite entries, singular
  * diagonal blocks) raised by the calls above.  Synchronises. */
 int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite_host, int32_t* singular_host, void* stream);
+/* Stream-ordered variant for pipelined sweeps: moves the four flag words
+ * (non-finite, singular, reserved x2) into flags_dev (device int32[4]) and
+ * clears them, without synchronising. */
+int ewb_ctx_flags_async(ewb_ctx* ctx, int32_t* flags_dev, void* stream);
 
 /* apply_bcs for caller-supplied T, U (assembly.py:263-297). */
 int ewb_apply_bcs(const void* t_dev, const void* u_dev, const uint8_t* kinds_dev,
@@ -131,23 +135,36 @@ int ewb_blockdiag_inverse(const void* a_dev, int64_t n, void* pinv_dev, int32_t*
 int ewb_gemv_batched(const void* a_dev, const void* x_dev, void* y_dev, int64_t n, int32_t batch,
                      void* stream);
 
+/* CTA budget of the solver launches (ewb_gmres, ewb_sem_guess): 0 = one CTA
+ * per SM (default).  A smaller budget leaves SMs to concurrent work on other
+ * streams; the matvec's bandwidth scales with the SMs it streams through
+ * (measured ~46 GB/s per SM), so the default is the fastest solve.
+ * Process-wide; not thread-safe. */
+int ewb_set_solver_ctas(int32_t ctas);
+int32_t ewb_solver_ctas(void);
+
 /* Whole restarted right-preconditioned GMRES solve in one cooperative launch
  * (linsolve.py:107-210).  pinv_dev may be NULL (no preconditioner); x_dev
  * holds x0 when has_x0 != 0 and receives the solution; hist_dev receives the
- * residual history (init, then one estimate per iteration).
+ * residual history (init, then one estimate per iteration).  ax0_dev
+ * (optional, used only with has_x0) holds A x0 when the caller already has
+ * it (ewb_sem_guess returns it): the initial residual b - A x0
+ * (linsolve.py:144) then costs no pass over A.
  * workspace: ewb_gmres_workspace_bytes(n, restart) bytes of device memory. */
 int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart);
 int ewb_gmres(const void* a_dev, const void* b_dev, const void* pinv_dev, void* x_dev,
-              int32_t has_x0, int64_t n, double tol, int32_t restart, int32_t maxiter,
+              int32_t has_x0, const void* ax0_dev, int64_t n, double tol, int32_t restart,
+              int32_t maxiter,
               void* workspace_dev, int64_t workspace_bytes, double* hist_dev, int32_t hist_cap,
               ewb_gmres_result* result_dev, void* stream);
 
 /* Least-squares extrapolated initial guess (sem_initial_guess,
  * linsolve.py:213-242).  x_hist_dev: K history columns, newest first,
- * column c at x_hist_dev + c*n; writes x0_dev (n). */
+ * column c at x_hist_dev + c*n; writes x0_dev (n) and, if ax0_dev is not
+ * NULL, A x0 = (A X) s from the same products (for ewb_gmres). */
 int64_t ewb_sem_workspace_bytes(int64_t n, int32_t K);
 int ewb_sem_guess(const void* a_dev, const void* b_dev, const void* x_hist_dev, int32_t K,
-                  int64_t n, double rank_tol, void* x0_dev, void* workspace_dev,
+                  int64_t n, double rank_tol, void* x0_dev, void* ax0_dev, void* workspace_dev,
                   int64_t workspace_bytes, ewb_sem_result* result_dev, void* stream);
 
 /* conjugate_fill + window_weights + inverse_mft (transform.py:137-203) for D

@@ -21,8 +21,9 @@ EXPORTS = (
     "ewb_abi_version", "ewb_last_error", "ewb_launch_count", "ewb_ctx_create", "ewb_ctx_destroy",
     "ewb_ctx_set_exterior", "ewb_ctx_counts", "ewb_static_rowsums", "ewb_static_tu",
     "ewb_assemble_tu",
-    "ewb_assemble_system", "ewb_ctx_flags", "ewb_apply_bcs", "ewb_blockdiag_inverse",
-    "ewb_gemv_batched", "ewb_gmres_workspace_bytes", "ewb_gmres",
+    "ewb_assemble_system", "ewb_ctx_flags", "ewb_ctx_flags_async", "ewb_apply_bcs", "ewb_blockdiag_inverse",
+    "ewb_gemv_batched", "ewb_set_solver_ctas", "ewb_solver_ctas",
+    "ewb_gmres_workspace_bytes", "ewb_gmres",
     "ewb_sem_workspace_bytes", "ewb_sem_guess", "ewb_window_idft",
     "ewb_matfree_workspace_bytes", "ewb_matfree_apply",
     "ewb_pair_kernels_blocks", "ewb_pair_kernels_workspace_bytes",
@@ -66,13 +67,16 @@ _SIGS = {
     "ewb_assemble_tu": (I32, [P, D, D, P, P, P]),
     "ewb_assemble_system": (I32, [P, D, D, P, P, P, P, P, P]),
     "ewb_ctx_flags": (I32, [P, P, P, P]),
+    "ewb_ctx_flags_async": (I32, [P, P, P]),
     "ewb_apply_bcs": (I32, [P, P, P, P, I64, P, P, P]),
     "ewb_blockdiag_inverse": (I32, [P, I64, P, P, P]),
     "ewb_gemv_batched": (I32, [P, P, P, I64, I32, P]),
+    "ewb_set_solver_ctas": (I32, [I32]),
+    "ewb_solver_ctas": (I32, []),
     "ewb_gmres_workspace_bytes": (I64, [I64, I32]),
-    "ewb_gmres": (I32, [P, P, P, P, I32, I64, D, I32, I32, P, I64, P, I32, P, P]),
+    "ewb_gmres": (I32, [P, P, P, P, I32, P, I64, D, I32, I32, P, I64, P, I32, P, P]),
     "ewb_sem_workspace_bytes": (I64, [I64, I32]),
-    "ewb_sem_guess": (I32, [P, P, P, I32, I64, D, P, P, I64, P, P]),
+    "ewb_sem_guess": (I32, [P, P, P, I32, I64, D, P, P, P, I64, P, P]),
     "ewb_window_idft": (I32, [P, I64, I64, I32, D, D, P, P, P]),
     "ewb_matfree_workspace_bytes": (I64, [P, I32]),
     "ewb_matfree_apply": (I32, [P, D, D, P, P, I32, P, P, P, P, I64, P]),
@@ -98,7 +102,7 @@ def load(path: os.PathLike | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ewb_abi_version() != 1:
+    if lib.ewb_abi_version() != 2:
         raise NativeUnavailable("libewbem_b200.so ABI version mismatch")
     _lib = lib
     return lib

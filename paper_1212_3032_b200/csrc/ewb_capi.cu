@@ -162,6 +162,14 @@ int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite, int32_t* singular, void* str
   return EWB_OK;
 }
 
+int ewb_ctx_flags_async(ewb_ctx* ctx, int32_t* flags_dev, void* stream) {
+  if (!ctx || !flags_dev) return fail(EWB_ERR_INVALID, "ewb_ctx_flags_async: null argument");
+  EWB_CUDA(cudaMemcpyAsync(flags_dev, ctx->c.flags, 16, cudaMemcpyDeviceToDevice, S(stream)),
+           "ewb_ctx_flags_async");
+  EWB_CUDA(cudaMemsetAsync(ctx->c.flags, 0, 16, S(stream)), "ewb_ctx_flags_async");
+  return EWB_OK;
+}
+
 int ewb_apply_bcs(const void* t, const void* u, const uint8_t* kinds, const void* p, int64_t n,
                   void* a, void* b, void* stream) {
   if (!t || !u || !kinds || !p || !a || !b || n < 1)
@@ -192,18 +200,27 @@ int ewb_gemv_batched(const void* a, const void* x, void* y, int64_t n, int32_t b
   return EWB_OK;
 }
 
+int ewb_set_solver_ctas(int32_t ctas) {
+  if (ctas < 0) return fail(EWB_ERR_INVALID, "ewb_set_solver_ctas: ctas must be >= 0");
+  ewb::set_solver_ctas(ctas);
+  return EWB_OK;
+}
+
+int32_t ewb_solver_ctas(void) { return ewb::solver_grid_blocks(); }
+
 // workspace layout: r, w, z (3n), V ((restart+1) n), H, partial
 int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart) {
   int64_t cpl = 16;
-  int64_t G = ewb::solver_grid_blocks();
+  int64_t G = ewb::solver_grid_max();
   return cpl * (3 * n + (int64_t)(restart + 1) * n +
                 2 * (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart +
                 2 * G * (2 * ewb::kMaxRestart + 2)) +
          8 * 2 * G * 16 + 256 * 8;
 }
 
-int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t has_x0, int64_t n,
-              double tol, int32_t restart, int32_t maxiter, void* ws, int64_t ws_bytes,
+int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t has_x0,
+              const void* ax0, int64_t n, double tol, int32_t restart, int32_t maxiter, void* ws,
+              int64_t ws_bytes,
               double* hist, int32_t hist_cap, ewb_gmres_result* result, void* stream) {
   if (!a || !b || !x || !ws || !hist || !result || n < 1)
     return fail(EWB_ERR_INVALID, "ewb_gmres: bad argument");
@@ -220,6 +237,7 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   g.b = (const ewb::cplx*)b;
   g.pinv = (const ewb::cplx*)pinv;
   g.x = (ewb::cplx*)x;
+  g.ax0 = has_x0 ? (const ewb::cplx*)ax0 : nullptr;
   g.r = base;
   g.w = base + n;
   g.z = base + 2 * n;
@@ -227,7 +245,7 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   g.H = g.V + (int64_t)(restart + 1) * n;
   g.Gram = g.H + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
   g.dpart = g.Gram + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
-  g.partial = (double*)(g.dpart + 2 * (int64_t)ewb::solver_grid_blocks() *
+  g.partial = (double*)(g.dpart + 2 * (int64_t)ewb::solver_grid_max() *
                                       (2 * ewb::kMaxRestart + 2));
   {
     const char* env = getenv("EWB_GMRES_ORTHO");
@@ -256,13 +274,13 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
 }
 
 int64_t ewb_sem_workspace_bytes(int64_t n, int32_t K) {
-  int64_t G = ewb::solver_grid_blocks();
+  int64_t G = ewb::solver_grid_max();
   return 16 * (2 * (int64_t)K * n) + 8 * 2 * G * 16 + 256 * 8;
 }
 
 int ewb_sem_guess(const void* a, const void* b, const void* xh, int32_t K, int64_t n,
-                  double rank_tol, void* x0, void* ws, int64_t ws_bytes, ewb_sem_result* result,
-                  void* stream) {
+                  double rank_tol, void* x0, void* ax0, void* ws, int64_t ws_bytes,
+                  ewb_sem_result* result, void* stream) {
   if (!a || !b || !xh || !x0 || !ws || !result || n < 1)
     return fail(EWB_ERR_INVALID, "ewb_sem_guess: bad argument");
   if (K < 1 || K > ewb::kMaxSem) return fail(EWB_ERR_INVALID, "ewb_sem_guess: K must be in [1, 4]");
@@ -277,6 +295,7 @@ int ewb_sem_guess(const void* a, const void* b, const void* xh, int32_t K, int64
   s.Q = base + (int64_t)K * n;
   s.partial = (double*)(base + 2 * (int64_t)K * n);
   s.x0 = (ewb::cplx*)x0;
+  s.ax0 = (ewb::cplx*)ax0;
   s.out = (ewb::SemOut*)result;
   s.n = n;
   s.K = K;

@@ -25,7 +25,13 @@ namespace cg = cooperative_groups;
 
 namespace ewb {
 
-constexpr int kSolveThreads = 512;
+#ifndef EWB_SOLVE_THREADS
+#define EWB_SOLVE_THREADS 512
+#endif
+constexpr int kSolveThreads = EWB_SOLVE_THREADS;
+// register cap 65536 / (kSolveThreads * kSolveMinBlocks) = 128: with 256 threads a
+// solver CTA leaves half of the register file to co-resident assembly CTAs
+constexpr int kSolveMinBlocks = 512 / kSolveThreads;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kMaxRed = 16;  // doubles per grid reduction
 
@@ -362,7 +368,7 @@ struct GivensShared {
 
 // Classic sequential MGS (one grid barrier per projection) — kept as the
 // GmresArgs::ortho == 1 variant for A/B parity checks.
-__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_mgs(GmresArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_mgs(GmresArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
@@ -616,7 +622,7 @@ __device__ __forceinline__ void precond_regs(const cplx* pinv, long long e, cons
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresArgs a) {
   int n_probe = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -884,10 +890,19 @@ __device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& 
   r1 = (long long)(blockIdx.x + 1) * n / gridDim.x;
 }
 
+// kMvSlices row slices of kMvRpt rows; a slice's kMvCols threads each take
+// kCPT columns (col, col + kMvCols, ...) of every tile.  Accumulators per
+// thread: kMvRpt x K (more slices for more right-hand sides keeps that at
+// <= 16 complex values).
 template <int K, typename Epi>
 __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
                             long long r0, long long r1, Epi&& epi) {
-  __shared__ cplx s_red[kSolveWarps][kRpt][K];
+  constexpr int kMvSlices = K <= 2 ? 2 : 4;
+  constexpr int kMvRpt = kRR / kMvSlices;
+  constexpr int kMvCols = kSolveThreads / kMvSlices;
+  constexpr int kCPT = kTC / kMvCols;
+  static_assert(kRR % kMvSlices == 0 && kTC % kMvCols == 0 && kCPT >= 1, "matvec_rows layout");
+  __shared__ cplx s_red[kSolveWarps][kMvRpt][K];
   __shared__ cplx s_sum[kRR][K];
   const long long rows = r1 - r0;
   if (rows <= 0) return;
@@ -916,16 +931,21 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int s = 0; s < S && s < kNS; ++s) issue_next(R.pos + (unsigned)s);
   }
-  const int col = threadIdx.x % kTC, slice = threadIdx.x / kTC;
+  const int col = threadIdx.x % kMvCols, slice = threadIdx.x / kMvCols;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  cplx acc[kRpt][K];
+  cplx acc[kMvRpt][K];
 #pragma unroll
-  for (int r = 0; r < kRpt; ++r)
+  for (int r = 0; r < kMvRpt; ++r)
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
-  cplx xn[K];  // x for the stage being consumed (prefetched one stage ahead)
+  cplx xn[kCPT][K];  // x for the stage being consumed (prefetched one stage ahead)
 #pragma unroll
-  for (int k = 0; k < K; ++k) xn[k] = col < n ? ldg(x + k * n + col) : cplx{0.0, 0.0};
+  for (int m = 0; m < kCPT; ++m)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = col + m * kMvCols;
+      xn[m][k] = c < n ? ldg(x + k * n + c) : cplx{0.0, 0.0};
+    }
   int q = 0, t = 0;
   long long row0;
   int nrows;
@@ -933,29 +953,50 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
   for (int s = 0; s < S; ++s) {
     const long long c0 = (long long)t * kTC;
     const int tc = t == ntile - 1 ? last_tc : kTC;
-    cplx xv[K];
+    // next stage's x: loaded before this stage's wait (K <= 2: double
+    // buffer) or right after its FMAs (K > 2: single buffer, fewer registers)
+    auto prefetch = [&](cplx (&dst)[kCPT][K]) {
+      const long long cb = (t == ntile - 1 ? 0 : c0 + kTC) + col;
 #pragma unroll
-    for (int k = 0; k < K; ++k) xv[k] = xn[k];
-    {  // prefetch the next stage's x
-      const long long cn = (t == ntile - 1 ? 0 : c0 + kTC) + col;
+      for (int m = 0; m < kCPT; ++m)
 #pragma unroll
-      for (int k = 0; k < K; ++k) xn[k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
+        for (int k = 0; k < K; ++k) {
+          const long long cn = cb + m * kMvCols;
+          dst[m][k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
+        }
+    };
+    constexpr bool kDouble = K <= 2;
+    cplx xb[kDouble ? kCPT : 1][kDouble ? K : 1];
+    if constexpr (kDouble) {
+#pragma unroll
+      for (int m = 0; m < kCPT; ++m)
+#pragma unroll
+        for (int k = 0; k < K; ++k) xb[m][k] = xn[m][k];
+      prefetch(xn);
     }
+    auto& xv = *reinterpret_cast<cplx(*)[kCPT][K]>(kDouble ? &xb[0][0] : &xn[0][0]);
     const unsigned pos = R.pos + (unsigned)s;
     ring_wait(R, pos);
-    if (col < tc) {
+    {
       const cplx* tile = R.buf + (size_t)(pos % kNS) * kStageElems;
 #pragma unroll
-      for (int r = 0; r < kRpt; ++r) {
-        const int row = slice * kRpt + r;
-        if (row < nrows) {
-          double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + col);
-          cplx av = {a2.x, a2.y};
+      for (int m = 0; m < kCPT; ++m) {
+        const int c = col + m * kMvCols;
+        if (c < tc) {
 #pragma unroll
-          for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[k]);
+          for (int r = 0; r < kMvRpt; ++r) {
+            const int row = slice * kMvRpt + r;
+            if (row < nrows) {
+              double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + c);
+              cplx av = {a2.x, a2.y};
+#pragma unroll
+              for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[m][k]);
+            }
+          }
         }
       }
     }
+    if constexpr (!kDouble) prefetch(xn);
     __syncthreads();  // every consumer is done with this stage's buffer
     if (threadIdx.x == 0 && s + kNS < S) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -963,7 +1004,7 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
     }
     if (t == ntile - 1) {  // last tile of the block: reduce, then the epilogue
 #pragma unroll
-      for (int r = 0; r < kRpt; ++r)
+      for (int r = 0; r < kMvRpt; ++r)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           warp_sum(acc[r][k]);
@@ -973,8 +1014,8 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
       __syncthreads();
       if (threadIdx.x < kRR * K) {
         const int row = threadIdx.x / K, k = threadIdx.x % K;
-        const int h = row / kRpt, r = row % kRpt;
-        constexpr int wps = kSolveWarps / kSlices;  // warps per row slice
+        const int h = row / kMvRpt, r = row % kMvRpt;
+        constexpr int wps = kSolveWarps / kMvSlices;  // warps per row slice
         cplx sum = {0.0, 0.0};
         for (int w = 0; w < wps; ++w) sum = sum + s_red[h * wps + w][r][k];
         s_sum[row][k] = sum;
@@ -989,6 +1030,16 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
     }
   }
   R.pos += (unsigned)S;
+}
+
+// sum over aligned groups of G lanes (result in every lane of the group)
+template <int G>
+__device__ __forceinline__ void group_sum(cplx& v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
+    v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
+  }
 }
 
 // Fixed-order reduction of `cnt` CTA partials (layout part[b * stride + t]):
@@ -1053,17 +1104,8 @@ __device__ void reduce_parts(const cplx* part, int stride, int cnt, cplx* out) {
 constexpr int kNormSlot = kMaxDots - 1;
 constexpr int kGrp = kRR <= 16 ? 16 : 32;  // lanes per epilogue dot
 
-// sum over aligned groups of G lanes (result in every lane of the group)
-template <int G>
-__device__ __forceinline__ void group_sum(cplx& v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) {
-    v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
-    v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
-  }
-}
 
-__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_f(GmresArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(GmresArgs a) {
   int n_probe = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -1158,7 +1200,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_f(GmresArgs a) {
   }
   int n_mv = 0;
   double rnorm;
-  if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
+  if (v2[1] > 0.0 && a.ax0) {  // r = b - A x0 with A x0 supplied (SEM's Y s)
+    double q = 0.0;
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      const cplx r = a.b[k] - a.ax0[k];
+      a.r[k] = r;
+      q += abs2(r);
+    }
+    cta_norm_partial(q, dpar);
+    grid.sync();
+    rnorm = sqrt(grid_norm(dpar));
+    dpar ^= 1;
+  } else if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
     rnorm = residual(dpar);
     dpar ^= 1;
     ++n_mv;
@@ -1567,9 +1620,13 @@ __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
         s[i] = cdiv(t, Rm[i][i]);
       }
       for (long long k = tid; k < n; k += nth) {
-        cplx x = {0.0, 0.0};
-        for (int i = 0; i < kk; ++i) cfma(x, a.X[(size_t)keep[i] * n + k], s[i]);
+        cplx x = {0.0, 0.0}, y = {0.0, 0.0};
+        for (int i = 0; i < kk; ++i) {
+          cfma(x, a.X[(size_t)keep[i] * n + k], s[i]);
+          if (a.ax0) cfma(y, a.Y[(size_t)keep[i] * n + k], s[i]);
+        }
         a.x0[k] = x;
+        if (a.ax0) a.ax0[k] = y;
       }
       if (tid == 0) { a.out->kept = kk; a.out->fallback = 0; }
       return;
@@ -1584,11 +1641,14 @@ __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
     __syncthreads();
     if (ng == 0) break;
   }
-  for (long long k = tid; k < n; k += nth) a.x0[k] = a.X[k];
+  for (long long k = tid; k < n; k += nth) {
+    a.x0[k] = a.X[k];
+    if (a.ax0) a.ax0[k] = a.Y[k];
+  }
   if (tid == 0) { a.out->kept = 0; a.out->fallback = 1; }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, 1) k_sem(SemArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_sem(SemArgs a) {
   cg::grid_group grid = cg::this_grid();
   GridRed R{a.partial, 0};
   switch (a.K) {
@@ -1601,7 +1661,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) k_sem(SemArgs a) {
 
 // Batched GEMV y_b = A_b x_b through the TMA ring (regular launch; system
 // blockIdx.y, row groups dealt over blockIdx.x).
-__global__ void __launch_bounds__(kSolveThreads, 1) k_gemv_tma(const cplx* A, const cplx* x,
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gemv_tma(const cplx* A, const cplx* x,
                                                                cplx* y, long long n) {
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
@@ -1661,7 +1721,16 @@ static int coop_grid(const void* fn) {
   return sms * per;
 }
 
+static int g_solver_limit = 0;  // 0: every co-resident CTA
+
+void set_solver_ctas(int ctas) { g_solver_limit = ctas > 0 ? ctas : 0; }
+
 int solver_grid_blocks() {
+  const int m = solver_grid_max();
+  return g_solver_limit > 0 && g_solver_limit < m ? g_solver_limit : m;
+}
+
+int solver_grid_max() {
   if (g_coop_blocks == 0) {
     int a = coop_grid((const void*)k_gmres), b = coop_grid((const void*)k_sem);
     int c = coop_grid((const void*)k_gmres_mgs), d = coop_grid((const void*)k_gmres_f);
@@ -1685,7 +1754,7 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
 // Y = A X for K <= 4 columns in one TMA-streamed pass (SEM's products,
 // linsolve.py:228).  Regular launch, 1 CTA/SM, full register budget.
 template <int K>
-__global__ void __launch_bounds__(kSolveThreads, 1) k_multi_gemv(const cplx* A, const cplx* X,
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_multi_gemv(const cplx* A, const cplx* X,
                                                                  cplx* Y, long long n) {
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
@@ -1710,23 +1779,25 @@ static cudaError_t launch_multi_gemv(const cplx* A, const cplx* X, cplx* Y, long
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBytes);
     attr = true;
   }
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  unsigned blocks = (unsigned)sms;
+  // the solver's CTA budget (the rest of the GPU may be assembling)
+  unsigned blocks = (unsigned)solver_grid_blocks();
   EWB_NOTE k_multi_gemv<K><<<blocks, kSolveThreads, kRingBytes, s>>>(A, X, Y, n);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
-  // Measured: the K-vector matvec spills beyond K = 2 under the 128-register
-  // cap of a 512-thread CTA (K=4 in one pass: 2.04 ms at n=15360), so the
-  // columns go two at a time.
-  cudaError_t e = cudaSuccess;
-  for (int c = 0; c < args.K && e == cudaSuccess; c += 2) {
-    const long long off = (long long)c * args.n;
-    if (args.K - c >= 2) e = launch_multi_gemv<2>(args.A, args.X + off, args.Y + off, args.n, s);
-    else e = launch_multi_gemv<1>(args.A, args.X + off, args.Y + off, args.n, s);
+  // Y = A X.  Measured at n = 15360 (one pass + QR): K=1 0.59 ms, K=2 0.67,
+  // K=3 0.77, K=4 in one pass 1.51 (register spills) -> K=4 runs as 2 + 2.
+  cudaError_t e;
+  switch (args.K) {
+    case 1: e = launch_multi_gemv<1>(args.A, args.X, args.Y, args.n, s); break;
+    case 2: e = launch_multi_gemv<2>(args.A, args.X, args.Y, args.n, s); break;
+    case 3: e = launch_multi_gemv<3>(args.A, args.X, args.Y, args.n, s); break;
+    default:
+      e = launch_multi_gemv<2>(args.A, args.X, args.Y, args.n, s);
+      if (e == cudaSuccess)
+        e = launch_multi_gemv<2>(args.A, args.X + 2 * args.n, args.Y + 2 * args.n, args.n, s);
+      break;
   }
   if (e != cudaSuccess) return e;
   int G = solver_grid_blocks();

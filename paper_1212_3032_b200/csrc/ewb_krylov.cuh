@@ -24,6 +24,7 @@ struct GmresArgs {
   const cplx* b;        // (n,)
   const cplx* pinv;     // (n/3, 3, 3) or nullptr (no preconditioner)
   cplx* x;              // in: x0 if has_x0; out: solution
+  const cplx* ax0;      // optional A x0 (initial residual without a pass over A)
   cplx* r;              // scratch (n)
   cplx* w;              // scratch (n)
   cplx* z;              // scratch (n)
@@ -55,6 +56,7 @@ struct SemArgs {
   cplx* Y;              // scratch K n
   cplx* Q;              // scratch K n
   cplx* x0;             // out (n)
+  cplx* ax0;            // optional out (n): A x0 = Y s
   double* partial;
   SemOut* out;
   long long n;
@@ -62,7 +64,9 @@ struct SemArgs {
   double rank_tol;
 };
 
-int solver_grid_blocks();
+int solver_grid_max();      // co-resident CTAs of the solver kernels (workspace sizing)
+int solver_grid_blocks();   // CTAs the solver launches use (<= max, see set_solver_ctas)
+void set_solver_ctas(int ctas);
 cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s);
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s);
 cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long n, int batch,

@@ -162,24 +162,37 @@ _WS = _Workspace()
 
 def gmres_device(a, b, x, has_x0: bool, tol: float, restart: int, maxiter: int, pinv=None,
                  ws: _Workspace | None = None, stats: SolveStats | None = None,
-                 sync: bool = True):
-    """Dense GMRES on device tensors; x (n,) is in/out.  Returns SolveStats."""
+                 sync: bool = True, ax0=None, res=None, hist=None):
+    """Dense GMRES on device tensors; x (n,) is in/out.  Returns SolveStats.
+
+    ax0: optional device A x0 (e.g. from :func:`sem_device`), saving the
+    initial residual's pass over A.  res / hist: optional caller-owned result
+    (64 B) and history buffers, so several solves can be queued without a
+    host read-back in between (``sync=False``)."""
     lib = _lib.load()
     ws = ws or _WS
     n = int(b.shape[0])
     nbytes = int(lib.ewb_gmres_workspace_bytes(n, restart))
     buf = ws.get(nbytes)
-    cap = maxiter + 2 + maxiter // max(restart, 1) + 2
-    hist = ws.hist_buf(cap)
-    res = ws.result()
+    cap = gmres_hist_cap(maxiter, restart)
+    hist = ws.hist_buf(cap) if hist is None else hist
+    cap = min(cap, hist.numel())
+    res = ws.result() if res is None else res
     _lib.check(lib.ewb_gmres(_lib.ptr(a), _lib.ptr(b), _lib.ptr(pinv) if pinv is not None else None,
-                             _lib.ptr(x), int(bool(has_x0)), n, float(tol), int(restart),
+                             _lib.ptr(x), int(bool(has_x0)),
+                             _lib.ptr(ax0) if (ax0 is not None and has_x0) else None,
+                             n, float(tol), int(restart),
                              int(maxiter), _lib.ptr(buf), buf.numel(), _lib.ptr(hist), cap,
                              _lib.ptr(res), _lib.stream_handle()), "ewb_gmres")
     st = stats or SolveStats()
     if sync:
         _fill_stats(st, res, hist)
     return st
+
+
+def gmres_hist_cap(maxiter: int, restart: int) -> int:
+    """Residual-history slots one solve can write (init + per iteration + per cycle)."""
+    return maxiter + 2 + maxiter // max(restart, 1) + 2
 
 
 def _fill_stats(st: SolveStats, res, hist):
@@ -254,15 +267,19 @@ class SemWorkspace:
 _SEM_WS = SemWorkspace()
 
 
-def sem_device(a, b, xcols, rank_tol: float, x0_out, ws: SemWorkspace | None = None):
-    """x0_out <- SEM guess for dense a (device); xcols (K, n) newest first."""
+def sem_device(a, b, xcols, rank_tol: float, x0_out, ws: SemWorkspace | None = None,
+               ax0_out=None):
+    """x0_out <- SEM guess for dense a (device); xcols (K, n) newest first.
+    ax0_out (optional): receives A x0 from the same products."""
     lib = _lib.load()
     ws = ws or _SEM_WS
     K, n = int(xcols.shape[0]), int(xcols.shape[1])
     nbytes = int(lib.ewb_sem_workspace_bytes(n, K))
     buf, res = ws.get(nbytes)
     _lib.check(lib.ewb_sem_guess(_lib.ptr(a), _lib.ptr(b), _lib.ptr(xcols), K, n,
-                                 float(rank_tol), _lib.ptr(x0_out), _lib.ptr(buf), buf.numel(),
+                                 float(rank_tol), _lib.ptr(x0_out),
+                                 _lib.ptr(ax0_out) if ax0_out is not None else None,
+                                 _lib.ptr(buf), buf.numel(),
                                  _lib.ptr(res), _lib.stream_handle()), "ewb_sem_guess")
     return res
 

@@ -125,7 +125,7 @@ def test_parse_config_matches_live_reference(tmp_path, reference):
 # ----------------------------------------------------------------------
 def _declared_symbols():
     text = (ROOT / "include" / "ewbem_b200.h").read_text()
-    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(ewb_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|int32_t|int64_t|const char\*)\s+(ewb_\w+)\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -139,7 +139,7 @@ def test_library_exports_every_declared_symbol():
     assert sorted(_lib.EXPORTS) == declared
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.ewb_abi_version() == 1
+    assert lib.ewb_abi_version() == 2
     out = subprocess.run(["nm", "-D", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     for name in declared:
         assert re.search(rf" T {name}$", out, re.M), name
@@ -172,7 +172,7 @@ def test_argument_validation_without_gpu():
     from paper_1212_3032_b200 import _lib
 
     lib = _lib.load()
-    assert lib.ewb_gmres(None, None, None, None, 0, 0, 1e-5, 60, 1000, None, 0, None, 0,
+    assert lib.ewb_gmres(None, None, None, None, 0, None, 0, 1e-5, 60, 1000, None, 0, None, 0,
                          None, None) == _lib.EWB_ERR_INVALID
     assert b"bad argument" in lib.ewb_last_error()
     assert lib.ewb_blockdiag_inverse(ctypes.c_void_p(16), 4, ctypes.c_void_p(16),

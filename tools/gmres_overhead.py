@@ -1,4 +1,5 @@
 """Per-iteration GMRES cost vs the pure TMA GEMV (N = 15360, fixed iteration counts)."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -8,6 +9,8 @@ from paper_1212_3032_b200 import _lib  # noqa: E402
 from paper_1212_3032_b200.linsolve import _Workspace, gmres_device  # noqa: E402
 
 lib = _lib.load()
+if os.environ.get("CTAS"):
+    _lib.check(lib.ewb_set_solver_ctas(int(os.environ["CTAS"])))
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 15360
 g = torch.Generator(device="cuda")
 g.manual_seed(0)
