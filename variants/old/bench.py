@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 per-frequency BEM solve (BASELINE.json metric/config).
+
+Default workload = BASELINE configs[1] (cfg2): flipped icosphere L4, 5120
+triangles / 15360 complex DOF, unit-step cavity pressure, N_omega = 256 ->
+129 sequential solves (SEM K = 4, GMRES tol 1e-8, restart 60).  One step =
+one full sweep through the device path (assembly + BCs + preconditioner +
+SEM + GMRES for all 129 frequencies + windowed IDFT of the probes) with the
+mesh context and the per-run inputs already resident in HBM.  Metric: s per
+sweep (lower is better).  `e2e` is the same sweep through the public API
+`run_sweep(cfg)` from host arrays (context creation, host->device uploads
+and the device->host read-back of histories/stats included).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg3|cfg4]
+
+`--impl reference` times the reference algorithm on the host CPU (the numpy
+oracle port under oracle/, since the Python reference cannot travel to the
+GPU box): a seeded column sample of the assembly plus scaled dense-matrix
+timings, extrapolated to one full sweep (see `cpu_sweep_estimate`).
+Multi-GPU (torchrun): SEM makes the sweep sequential, so N ranks run N
+replica sweeps (scaling "weak"); time = max over ranks of CUDA-event time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "s per sweep"
+BASELINE_METRIC = ("element-pair kernel evals/s (FP64 % peak); complex matvec HBM GB/s; "
+                   "s per sweep")
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg1", "cfg3", "cfg4", "cfg5"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args(argv)
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ----------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text())
+    return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+# ----------------------------------------------------------------------
+# CPU side: the reference algorithm (numpy oracle port), bounded sample
+# ----------------------------------------------------------------------
+def _time_dense_parts(n_full: int, n_sample: int, passes_per_freq: float, seed: int):
+    """Scaled timings of apply_bcs, block_diag_precond and the zgemv passes."""
+    from oracle import ewbem_oracle as O
+
+    rng = np.random.default_rng(seed)
+    ns = n_sample - n_sample % 3
+    t = rng.normal(size=(ns, ns)) + 1j * rng.normal(size=(ns, ns))
+    u = rng.normal(size=(ns, ns)) + 1j * rng.normal(size=(ns, ns))
+    kinds = np.zeros(ns, np.uint8)
+    p = rng.normal(size=ns) + 1j * rng.normal(size=ns)
+    t0 = time.perf_counter()
+    a, b = O.apply_bcs(t, u, kinds, p)
+    t1 = time.perf_counter()
+    nb = min(ns // 3, 512)
+    O.block_precond(a[: 3 * nb, : 3 * nb])
+    t2 = time.perf_counter()
+    # zgemv at a bandwidth-representative size (matrix >> LLC), scaled by N^2
+    ng = min(6144, n_full)
+    big = np.ones((ng, ng), dtype=complex)
+    vg = np.ones(ng, dtype=complex)
+    reps = 3
+    big @ vg   # BLAS thread start-up outside the timing
+    t2b = time.perf_counter()
+    for _ in range(reps):
+        big @ vg
+    t3 = time.perf_counter()
+    gemv_s = (t3 - t2b) / reps * (n_full / ng) ** 2
+    del big
+    # assemble_tu's dense bookkeeping: two zeroed (n_e,3,n_e,3) arrays, the
+    # per-column block scatter u_mat[rows,:,j,:] = ... and the finite check
+    # (assembly.py:229-253)
+    ne = ns // 3
+    blk = rng.normal(size=(ne, 3, 3)) + 0j
+    t4 = time.perf_counter()
+    tm = np.zeros((ne, 3, ne, 3), dtype=complex)
+    um = np.zeros((ne, 3, ne, 3), dtype=complex)
+    rows = np.arange(ne)
+    for j in range(ne):
+        tm[rows, :, j, :] = blk
+        um[rows, :, j, :] = blk
+    ok = np.isfinite(tm).all() and np.isfinite(um).all()
+    t5 = time.perf_counter()
+    assert ok
+    scale = (n_full / ns) ** 2
+    return dict(apply_bcs=(t1 - t0) * scale, precond=(t2 - t1) * (n_full / 3) / nb,
+                gemv=gemv_s * passes_per_freq, scatter=(t5 - t4) * scale)
+
+
+def cpu_sweep_estimate(cfg, n_cols: int, freq_ids, seed: int, passes_per_freq: float):
+    """Extrapolated CPU seconds for one full sweep of ``cfg`` (reference algorithm).
+
+    Sample: ``n_cols`` seeded columns of the assembly (prep + static pass +
+    dynamic assembly at the frequencies ``freq_ids``), scaled by n_e / n_cols;
+    apply_bcs / block preconditioner / zgemv timed on a smaller dense matrix
+    and scaled by (N / n_sample)^2; GMRES = passes_per_freq zgemv passes per
+    frequency (the reference's SEM does K separate matvecs).
+    """
+    from oracle import ewbem_oracle as O
+
+    m = cfg.mesh
+    med = O.Medium(cfg.material.lam, cfg.material.mu, cfg.material.rho)
+    eta = O.eta_from_kappa(cfg.kappa, cfg.period)
+    om = O.frequency_grid(cfg.period, cfg.n_omega, eta)
+    rng = np.random.default_rng(seed)
+    cols = np.sort(rng.choice(m.n_elements, size=min(n_cols, m.n_elements), replace=False))
+    t0 = time.perf_counter()
+    dyn = []
+    prep = static = 0.0
+    for i, k in enumerate(freq_ids):
+        s = O.column_sample_seconds(m.vertices, m.triangles, med, cols, om[k])
+        dyn.append(s["dynamic"])
+        if i == 0:
+            prep, static = s["prep"], s["static"]
+    scale = m.n_elements / len(cols)
+    dense = _time_dense_parts(m.n_dofs, 3072, passes_per_freq, seed)
+    nf = len(om)
+    per_freq = statistics.mean(dyn) * scale + dense["scatter"] + dense["apply_bcs"] + \
+        dense["precond"] + dense["gemv"]
+    total = (prep + static) * scale + nf * per_freq
+    wall = time.perf_counter() - t0
+    return dict(value=total, sample=(
+        f"{len(cols)} of {m.n_elements} assembly columns (seed {seed}) at k={list(freq_ids)}, "
+        f"scaled x{scale:.1f}; apply_bcs/precond/zgemv timed at N=3072 and scaled by N^2; "
+        f"{passes_per_freq:g} zgemv passes per frequency; {nf} frequencies; "
+        f"{wall:.1f} s of CPU work"), wall=wall,
+        parts=dict(prep_static_s=(prep + static) * scale,
+                   assembly_per_freq_s=statistics.mean(dyn) * scale,
+                   scatter_per_freq_s=dense["scatter"],
+                   apply_bcs_per_freq_s=dense["apply_bcs"], gemv_per_freq_s=dense["gemv"]))
+
+
+# ----------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------
+def fp64_peak():
+    import ctypes
+
+    from paper_1212_3032_b200 import _lib
+
+    lib = _lib.load()
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    best = 0.0
+    for _ in range(3):
+        _lib.check(lib.ewb_fp64_peak_probe(20000, 4, ctypes.byref(tf), ctypes.byref(ms),
+                                           _lib.stream_handle()))
+        best = max(best, tf.value)
+    return best
+
+
+def build_cfg(workload: str):
+    from paper_1212_3032_b200 import workloads
+
+    if workload == "cfg1":
+        return workloads.cfg1(), ("cfg1: unit cube 768 el / 2304 DOF, z- clamped, z+ unit step "
+                                  "traction, N_omega=128 -> 65 solves, SEM K=2, tol 1e-8")
+    return workloads.cfg2(), ("cfg2: flipped icosphere L4 5120 el / 15360 DOF, unit step "
+                              "cavity pressure, N_omega=256 -> 129 solves, SEM K=4, tol 1e-8, "
+                              "restart 60")
+
+
+def run_ours_sweep(args, rank, world, local_rank):
+    import torch
+
+    from paper_1212_3032_b200 import _lib, run_sweep
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.transform import windowed_inverse_device
+
+    lib = _lib.require_cuda()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg, desc = build_cfg(args.workload)
+    peak64 = fp64_peak()
+
+    t0 = time.perf_counter()
+    ds = DeviceSweep(cfg)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    counts = ds.asm.pair_counts()
+    pe = ds.asm.point_evals()
+    n_pairs = counts["far"] + counts["mid"] + counts["near"] + counts["n_elements"]
+    flops_per_asm = 397.0 * pe + 120.0 * n_pairs        # SURVEY §8(d) algorithmic count
+
+    def one_step():
+        ds.run(timing=True)
+        half = ds.probe_half(cfg.probes)
+        windowed_inverse_device(half, cfg.window, ds.eta, cfg.period)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    launches0 = lib.ewb_launch_count()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    asm_ms = solve_ms = 0.0
+    matvecs = 0
+    its = 0
+    nfreq = 0
+    for _ in range(args.steps):
+        one_step()
+        asm_ms += ds.phase["assembly_ms"]
+        solve_ms += ds.phase["solve_ms"]
+        matvecs += ds.phase["matvecs"]
+        nfreq += ds.phase["solves"]
+    stop.record()
+    torch.cuda.synchronize()
+    launches = lib.ewb_launch_count() - launches0
+    clocks = sampler.stop()
+    elapsed_ms = start.elapsed_time(stop)
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = elapsed_ms / args.steps
+    value = (elapsed_ms / 1e3) / (args.steps * world)   # s per sweep, whole job
+    its = sum(s for s in [0])
+    # per-frequency assembly: FP64 roofline;  solve phase: HBM roofline
+    n = ds.n
+    asm_per_freq_ms = asm_ms / max(nfreq, 1)
+    asm_tflops = flops_per_asm / (asm_per_freq_ms * 1e-3) / 1e12
+    bytes_per_pass = 16.0 * n * n + 32.0 * n
+    solve_gbs = matvecs * bytes_per_pass / (solve_ms * 1e-3) / 1e9
+    peaks = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    pair_evals_per_s = (counts["far"] + counts["mid"] + counts["near"] + counts["n_elements"]) / \
+        (asm_per_freq_ms * 1e-3)
+    rl_asm = {"bound": "fp64", "kernel": "assembly (k_farmid+k_near+k_self_dyn, fused BCs)",
+              "achieved": round(asm_tflops, 3), "peak": round(peak64, 3), "unit": "TFLOP/s",
+              "frac": round(asm_tflops / peak64, 4),
+              "peak_source": "measured DFMA probe in this run (MEASURED_PEAKS.json has no FP64)",
+              "traffic": None, "algorithmic_flops_per_launch": flops_per_asm,
+              "ms_per_launch": round(asm_per_freq_ms, 4)}
+    rl_solve = {"bound": "hbm", "kernel": "k_gmres + k_sem (persistent, dense matvec)",
+                "achieved": round(solve_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(solve_gbs / hbm_peak, 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)", "traffic": None,
+                "algorithmic_bytes_per_pass": bytes_per_pass,
+                "passes_per_sweep": matvecs / max(args.steps, 1)}
+    asm_share = asm_ms / max(asm_ms + solve_ms, 1e-9)
+    roof, roof2 = (rl_asm, rl_solve) if asm_share >= 0.5 else (rl_solve, rl_asm)
+
+    # e2e through the public API from host arrays
+    e2e_times, h2d, d2h = [], 0, 0
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        keep = []
+        t1 = time.perf_counter()
+        res = run_sweep(cfg, _sweep_out=keep, distributed=False)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t1)
+        h2d, d2h = keep[0].h2d_bytes, keep[0].d2h_bytes
+    e2e_s = statistics.median(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    total_its = res.total_iterations
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        passes = (matvecs / max(nfreq, 1)) + cfg.sem_depth - 1   # reference: K separate matvecs
+        est = cpu_sweep_estimate(cfg, 48, [1, ds.n_freq // 2, ds.n_freq - 1], 7, passes)
+        cpu = {"value": round(est["value"], 1), "unit": "s/sweep", "cores": os.cpu_count(),
+               "kind": "port", "sample": est["sample"], "parts": est["parts"]}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "s/sweep", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seedless deterministic mesh + step load, BASELINE cfg2)",
+            "config": {"workload": desc, "baseline_metric": BASELINE_METRIC,
+                       "l2": "inputs larger than L2 (A = 16 N^2 = %.2f GB)" % (16 * n * n / 1e9),
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "roofline": roof, "roofline_secondary": roof2,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_s / world, "unit": "s/sweep", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "metrics": {"element_pair_evals_per_s": pair_evals_per_s,
+                        "point_evals_per_assembly": pe, "assembly_ms_per_freq": asm_per_freq_ms,
+                        "assembly_share": round(asm_share, 4),
+                        "solve_ms_per_sweep": solve_ms / args.steps,
+                        "matvec_hbm_gbs_solve_phase": solve_gbs,
+                        "total_gmres_iterations": total_its, "setup_ms": setup_s * 1e3,
+                        "fp64_peak_tflops_measured": peak64},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank, world):
+    """The reference algorithm on the host CPU (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    cfg, desc = build_cfg(args.workload)
+    nf = cfg.n_omega // 2 + 1
+    passes = 8.0 if args.workload == "cfg2" else 40.0
+    times = []
+    for step in range(args.warmup + args.steps):
+        k = [1 + (step * 37) % (nf - 1)]
+        est = cpu_sweep_estimate(cfg, 24, k, 100 + step, passes)
+        if step >= args.warmup:
+            times.append(est["value"])
+            sample = est["sample"]
+    value = statistics.mean(times)
+    line = {"metric": METRIC, "value": value, "unit": "s/sweep", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": desc, "baseline_metric": BASELINE_METRIC},
+            "cpu_baseline": {"value": value, "unit": "s/sweep", "cores": os.cpu_count(),
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "s/sweep", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    rank, world, local_rank = env_rank()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if args.workload in ("cfg1", "cfg2"):
+        run_ours_sweep(args, rank, world, local_rank)
+    else:
+        from benchmarks import micro
+
+        micro.main(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,867 @@
+// sm_100a FP64 collocation assembly: per-mesh setup, static pass, and the
+// per-frequency dense assembly fused with the boundary-condition column
+// swap, the right-hand side and the 3x3 block-diagonal preconditioner.
+//
+// Reference map (ewbem 0.1.0):
+//   tier classification ........ assembly.py:132-136, quadrature.py:223-228
+//   near grading ............... assembly.py:152-161, quadrature.py:230-235,
+//                                mesh.py:165-204 (point_triangle_distance)
+//   field points ............... quadrature.py:58-60 (points @ verts)
+//   self rule .................. quadrature.py:135-185 (Duffy / asinh)
+//   static pass / row sums ..... assembly.py:193-216
+//   dynamic assembly ........... assembly.py:219-254
+//   boundary conditions ........ assembly.py:263-297
+//   block preconditioner ....... linsolve.py:80-104
+//
+// Work decomposition: one warp = one collocation row element i x 32
+// consecutive column elements j (lane = j), so the 3x3 blocks a warp
+// produces form three contiguous 1.5 KB row segments of the row-major
+// N x N matrix.  Far (gauss3) and mid (gauss7) pairs are evaluated there;
+// near pairs (subdivided gauss7, Q = 28..1792) come from a per-mesh CSR
+// list and take one warp per pair (lanes split the quadrature points);
+// diagonal blocks take one warp per element (384-point self rule).  No
+// atomics: every output element has exactly one writer and every sum has
+// a fixed order, so assembly is bit-reproducible (test_assembly.py:74-81).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "ewb_ctx.cuh"
+
+namespace ewb {
+
+// point_triangle_distance (mesh.py:165-204) for one point.
+__device__ double point_tri_distance(double px, double py, double pz, const double v[9]) {
+  double e0x = v[3] - v[0], e0y = v[4] - v[1], e0z = v[5] - v[2];
+  double e1x = v[6] - v[0], e1y = v[7] - v[1], e1z = v[8] - v[2];
+  double wx = px - v[0], wy = py - v[1], wz = pz - v[2];
+  double a = e0x * e0x + e0y * e0y + e0z * e0z;
+  double b = e0x * e1x + e0y * e1y + e0z * e1z;
+  double c = e1x * e1x + e1y * e1y + e1z * e1z;
+  double d = wx * e0x + wy * e0y + wz * e0z;
+  double e = wx * e1x + wy * e1y + wz * e1z;
+  double det = a * c - b * b;
+  double s = (c * d - b * e) / det, t = (a * e - b * d) / det;
+  s = fmin(fmax(s, 0.0), 1.0);
+  t = fmin(fmax(t, 0.0), 1.0);
+  if (s + t > 1.0) {
+    double sh = (s + t - 1.0) / 2.0;
+    s = fmin(fmax(s - sh, 0.0), 1.0);
+    t = fmin(fmax(t - sh, 0.0), 1.0);
+  }
+  double qx = v[0] + s * e0x + t * e1x, qy = v[1] + s * e0y + t * e1y, qz = v[2] + s * e0z + t * e1z;
+  double best = sqrt((px - qx) * (px - qx) + (py - qy) * (py - qy) + (pz - qz) * (pz - qz));
+  for (int k = 0; k < 3; ++k) {
+    int k1 = (k + 1) % 3;
+    double ax = v[3 * k], ay = v[3 * k + 1], az = v[3 * k + 2];
+    double sx = v[3 * k1] - ax, sy = v[3 * k1 + 1] - ay, sz = v[3 * k1 + 2] - az;
+    double tt = ((px - ax) * sx + (py - ay) * sy + (pz - az) * sz) / (sx * sx + sy * sy + sz * sz);
+    tt = fmin(fmax(tt, 0.0), 1.0);
+    double rx = px - (ax + tt * sx), ry = py - (ay + tt * sy), rz = pz - (az + tt * sz);
+    best = fmin(best, sqrt(rx * rx + ry * ry + rz * rz));
+  }
+  return best;
+}
+
+// ---------------------------------------------------------------------
+// setup kernels
+// ---------------------------------------------------------------------
+// Field points of the far/mid rules: y = bary @ verts (quadrature.py:58-60).
+__global__ void k_field_points(Geo g, const double* bary3, const double* bary7, double* yfar,
+                               double* ymid) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= g.n_e) return;
+  double v[9];
+  load_corners(g, j, v);
+  for (int q = 0; q < 10; ++q) {
+    const double* b = q < 3 ? bary3 + 3 * q : bary7 + 3 * (q - 3);
+    double* out = q < 3 ? yfar + (size_t)(3 * q) * g.n_e : ymid + (size_t)(3 * (q - 3)) * g.n_e;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      out[(size_t)c * g.n_e + j] = fma(b[2], v[6 + c], fma(b[1], v[3 + c], b[0] * v[c]));
+  }
+}
+
+// Duffy / asinh self rule (quadrature.py:135-185): thread per (element,
+// sub-triangle, angular node); loops the 8 radial nodes.
+__global__ void k_self_rule(Geo g, const double* gl8, const double* gl16, double4* out) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= g.n_e * 48) return;
+  int j = tid / 48, rem = tid % 48, sub = rem / 16, an = rem % 16;
+  double v[9];
+  load_corners(g, j, v);
+  double c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = ((v[k] + v[3 + k]) + v[6 + k]) / 3.0;
+  int k0 = sub, k1 = (sub + 1) % 3;
+  double a[3], b[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { a[k] = v[3 * k0 + k] - c[k]; b[k] = v[3 * k1 + k] - c[k]; }
+  double na = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+  double e1[3] = {a[0] / na, a[1] / na, a[2] / na};
+  double nr[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+  double nn = sqrt(nr[0] * nr[0] + nr[1] * nr[1] + nr[2] * nr[2]);
+  nr[0] /= nn; nr[1] /= nn; nr[2] /= nn;
+  double e2[3] = {nr[1] * e1[2] - nr[2] * e1[1], nr[2] * e1[0] - nr[0] * e1[2],
+                  nr[0] * e1[1] - nr[1] * e1[0]};
+  double a2x = a[0] * e1[0] + a[1] * e1[1] + a[2] * e1[2];
+  double a2y = a[0] * e2[0] + a[1] * e2[1] + a[2] * e2[2];
+  double b2x = b[0] * e1[0] + b[1] * e1[1] + b[2] * e1[2];
+  double b2y = b[0] * e2[0] + b[1] * e2[1] + b[2] * e2[2];
+  double th1 = atan2(a2y, a2x), th2 = atan2(b2y, b2x);
+  if (th2 <= th1) th2 += 2.0 * M_PI;
+  double dx = b2x - a2x, dy = b2y - a2y;
+  double tp = -(a2x * dx + a2y * dy) / (dx * dx + dy * dy);
+  double px = a2x + tp * dx, py = a2y + tp * dy;
+  double h = sqrt(px * px + py * py);
+  double thp = atan2(py, px);
+  double u1 = asinh(tan(th1 - thp)), u2 = asinh(tan(th2 - thp));
+  double u = 0.5 * (u2 - u1) * gl16[an] + 0.5 * (u2 + u1);
+  double wu = 0.5 * (u2 - u1) * gl16[16 + an];
+  double th = thp + atan(sinh(u));
+  double ch = cosh(u);
+  double rho = h * ch;
+  double st, ct;
+  sincos(th, &st, &ct);
+  for (int rr = 0; rr < 8; ++rr) {
+    double s = 0.5 * (gl8[rr] + 1.0), ws = 0.5 * gl8[8 + rr];
+    double w = ws * (wu / ch) * s * (rho * rho);
+    double p2x = s * rho * ct, p2y = s * rho * st;
+    double4 o;
+    o.x = c[0] + p2x * e1[0] + p2y * e2[0];
+    o.y = c[1] + p2x * e1[1] + p2y * e2[1];
+    o.z = c[2] + p2x * e1[2] + p2y * e2[2];
+    o.w = w;
+    out[(size_t)j * kSelfQ + sub * 128 + rr * 16 + an] = o;
+  }
+}
+
+// Near-pair census: warp per row; counts far / mid / near (off-diagonal).
+__global__ void k_near_count(Geo g, int* near_cnt, long long* far_cnt, long long* mid_cnt) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= g.n_e) return;
+  int i = warp;
+  double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+  int nn = 0, nf = 0, nm = 0;
+  for (int j0 = 0; j0 < g.n_e; j0 += 32) {
+    int j = j0 + lane;
+    int tier = 3;
+    if (j < g.n_e && j != i) tier = exact_tier(xi, yi, zi, g.cx[j], g.cy[j], g.cz[j], g.diam[j]);
+    nn += __popc(__ballot_sync(0xffffffffu, tier == 2));
+    nf += __popc(__ballot_sync(0xffffffffu, tier == 0));
+    nm += __popc(__ballot_sync(0xffffffffu, tier == 1));
+  }
+  if (lane == 0) { near_cnt[i] = nn; far_cnt[i] = nf; mid_cnt[i] = nm; }
+}
+
+__global__ void k_near_fill(Geo g, const int* near_ptr, int* near_j, int* near_row, int* near_lvl) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= g.n_e) return;
+  int i = warp;
+  double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+  int pos = near_ptr[i];
+  for (int j0 = 0; j0 < g.n_e; j0 += 32) {
+    int j = j0 + lane;
+    bool nr = false;
+    if (j < g.n_e && j != i) nr = exact_tier(xi, yi, zi, g.cx[j], g.cy[j], g.cz[j], g.diam[j]) == 2;
+    unsigned m = __ballot_sync(0xffffffffu, nr);
+    if (nr) {
+      int p = pos + __popc(m & ((1u << lane) - 1u));
+      double v[9];
+      load_corners(g, j, v);
+      double sep = point_tri_distance(xi, yi, zi, v) / g.diam[j];
+      int lvl = 1 + (sep < 0.60) + (sep < 0.30) + (sep < 0.15);   // quadrature.py:209,230-235
+      near_j[p] = j;
+      near_row[p] = i;
+      near_lvl[p] = lvl;
+    }
+    pos += __popc(m);
+  }
+}
+
+// ---------------------------------------------------------------------
+// pair kernels
+// ---------------------------------------------------------------------
+enum : int { OUT_TU = 1, OUT_SYS = 2, OUT_ROWSUM = 4 };
+
+struct SysArgs {
+  const uint8_t* kinds;      // (N,) NEUMANN / DIRICHLET per DOF
+  const cplx* p;             // (N,) prescribed values
+  cplx* A;                   // (N,N)
+  cplx* pinv;                // (n_e, 3, 3) inverse diagonal blocks
+  cplx* b;                   // (N,)
+};
+
+struct PairOut {
+  void* T;                   // (N,N) complex (dynamic) or real (static)
+  void* U;
+  SysArgs sys;
+  cplx* bpart;               // [n_tiles][N]
+  cplx* bnear;               // [n_near][3]
+  double* spart;             // [n_tiles][n_e][9]
+  double* snear;             // [n_near][9]
+  int* flags;
+};
+
+// Store a 3x3 block (row element i, column element j) into row-major N x N.
+template <typename S>
+__device__ __forceinline__ void store_block(S* M, long long N, int i, int j, const S B[3][3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    S* row = M + (size_t)(3 * i + a) * N + 3 * j;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) row[b] = B[a][b];
+  }
+}
+
+// BC mix of one block into A, and its right-hand-side contribution
+// (assembly.py:290-296):  Neumann column: A = T, b += U p;  Dirichlet: A = -U, b -= T p.
+__device__ __forceinline__ void sys_block(const SysArgs& s, long long N, int i, int j,
+                                          const cplx U[3][3], const cplx T[3][3], cplx bc[3]) {
+  uint8_t kd[3];
+  cplx pv[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { kd[c] = s.kinds[3 * j + c]; pv[c] = s.p[3 * j + c]; }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cplx* row = s.A + (size_t)(3 * i + a) * N + 3 * j;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (kd[c] == kDirichlet) {
+        row[c] = -U[a][c];
+        bc[a] = bc[a] - T[a][c] * pv[c];
+      } else {
+        row[c] = T[a][c];
+        bc[a] = bc[a] + U[a][c] * pv[c];
+      }
+    }
+  }
+}
+
+// Far/mid pairs: warp = (row element i, column tile t), lane = column j.
+#ifndef EWB_FARMID_MINB
+#define EWB_FARMID_MINB 3
+#endif
+#ifndef EWB_FARMID_ROWS
+#define EWB_FARMID_ROWS 4
+#endif
+constexpr int kFarRows = EWB_FARMID_ROWS;
+
+// Far/mid pairs: warp = (kFarRows consecutive row elements, column tile t),
+// lane = column j.  The column element's data (centroid, diameter, normal,
+// area, the 3 far field points) is loaded once per warp and reused for the
+// kFarRows rows, so its load latency is paid once per kFarRows pairs.
+template <bool DYN, int OUT>
+__global__ void __launch_bounds__(128, EWB_FARMID_MINB) k_farmid(Geo g, Phys<DYN> ph, PairOut o) {
+  using S = typename Phys<DYN>::S;
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int ntile = (g.n_e + 31) >> 5;
+  const int ngroups = (g.n_e + kFarRows - 1) / kFarRows;
+  if (warp >= (long long)ngroups * ntile) return;
+  const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
+  const int j = t * 32 + lane;
+  const bool jv = j < g.n_e;
+  const long long N = 3LL * g.n_e;
+  const int jj = jv ? j : 0;
+  const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
+  const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
+  double yf[9];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) yf[c] = g.yfar[(size_t)c * g.n_e + jj];
+  for (int r = 0; r < kFarRows; ++r) {
+    const int i = rg * kFarRows + r;
+    if (i >= g.n_e) break;
+    const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+    int tier = 3;
+    if (jv && j != i) tier = exact_tier(xi, yi, zi, cxj, cyj, czj, dj);
+    const bool active = tier < 2;
+    S U[3][3], T[3][3];
+    if (active) {
+      Acc<S> acc;
+      acc_zero(acc);
+      auto point = [&](double px, double py, double pz, double wq) {
+        double dx = px - xi, dy = py - yi, dz = pz - zi;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double ir = rsqrt(r2);
+        double rr = r2 * ir;
+        dx *= ir; dy *= ir; dz *= ir;
+        double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+        ph.point(acc, rr, ir, dx, dy, dz, dn, wq * ar);
+      };
+      if (tier == 0) {
+#pragma unroll 1
+        for (int q = 0; q < 3; ++q) point(yf[3 * q], yf[3 * q + 1], yf[3 * q + 2], g.wfar[q]);
+      } else {
+        for (int q = 0; q < 7; ++q)
+          point(g.ymid[(size_t)(3 * q) * g.n_e + j], g.ymid[(size_t)(3 * q + 1) * g.n_e + j],
+                g.ymid[(size_t)(3 * q + 2) * g.n_e + j], g.wmid[q]);
+      }
+      acc_finalize(acc, nx, ny, nz, ph.i4pm(), ph.i4p(), U, T);
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
+      if (!ok) o.flags[0] = 1;
+      if (OUT & OUT_TU) {
+        store_block((S*)o.T, N, i, j, T);
+        store_block((S*)o.U, N, i, j, U);
+      }
+    }
+    if constexpr (DYN && (OUT & OUT_SYS)) {
+      cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+      if (active) sys_block(o.sys, N, i, j, U, T, bc);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        warp_sum(bc[a]);
+        if (lane == 0) o.bpart[(size_t)t * N + 3 * i + a] = bc[a];
+      }
+    }
+    if constexpr (!DYN && (OUT & OUT_ROWSUM)) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          double v = active ? to_c(T[a][b]).re : 0.0;
+          warp_sum(v);
+          if (lane == 0) o.spart[((size_t)t * g.n_e + i) * 9 + 3 * a + b] = v;
+        }
+    }
+  }
+}
+template <bool DYN, int OUT>
+__global__ void __launch_bounds__(128, 3) k_near(Geo g, Phys<DYN> ph, PairOut o, int n_near) {
+  using S = typename Phys<DYN>::S;
+  const int lane = threadIdx.x & 31;
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_near) return;
+  const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
+  const long long N = 3LL * g.n_e;
+  const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+  const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
+  double v[9];
+  load_corners(g, j, v);
+  const RuleRef rr = g.sub[L];
+  const double* bary = g.rules + rr.off;
+  const double* wq = bary + 3 * rr.q;
+  Acc<S> acc;
+  acc_zero(acc);
+  for (int q = lane; q < rr.q; q += 32) {
+    double b0 = bary[3 * q], b1 = bary[3 * q + 1], b2 = bary[3 * q + 2];
+    double dx = fma(b2, v[6], fma(b1, v[3], b0 * v[0])) - xi;
+    double dy = fma(b2, v[7], fma(b1, v[4], b0 * v[1])) - yi;
+    double dz = fma(b2, v[8], fma(b1, v[5], b0 * v[2])) - zi;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
+    dx *= ir; dy *= ir; dz *= ir;
+    double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+    ph.point(acc, r, ir, dx, dy, dz, dn, wq[q] * ar);
+  }
+  // butterfly reduction: every lane holds the totals, then lanes 0..8 each
+  // finalise one block entry (a, c) in parallel (kernels.py:336-356)
+  acc_warp_allsum(acc);
+  const int a = lane / 3, c = lane % 3;
+  S u_ac, t_ac;
+  {
+    const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+    const double n[3] = {nx, ny, nz};
+    const int ac = lane < 9 ? sym[a][c] : 0;
+    const int aa = lane < 9 ? a : 0, cc = lane < 9 ? c : 0;
+    S pu = acc.P[ac];
+    u_ac = aa == cc ? acc.su - pu : -pu;
+    u_ac = ph.i4pm() * u_ac;
+    S t = acc.B[ac];
+    madd(t, n[aa], acc.va[cc]);
+    madd(t, n[cc], acc.vc[aa]);
+    if (aa == cc) t = t + acc.sa;
+    t_ac = ph.i4p() * t;
+  }
+  const bool ok = lane >= 9 || (finite(u_ac) && finite(t_ac));
+  if (!__all_sync(0xffffffffu, ok) && lane == 0) o.flags[0] = 1;
+  if (OUT & OUT_TU) {
+    if (lane < 9) {
+      ((S*)o.T)[(size_t)(3 * i + a) * N + 3 * j + c] = t_ac;
+      ((S*)o.U)[(size_t)(3 * i + a) * N + 3 * j + c] = u_ac;
+    }
+  }
+  if constexpr (DYN && (OUT & OUT_SYS)) {
+    // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
+    // Dirichlet column A = -U, b -= T p;  b summed over c = 0, 1, 2 in order
+    cplx bt = {0.0, 0.0};
+    if (lane < 9) {
+      const size_t col = 3 * (size_t)j + c;
+      const bool dir = o.sys.kinds[col] == kDirichlet;
+      const cplx pv = o.sys.p[col];
+      o.sys.A[(size_t)(3 * i + a) * N + col] = dir ? -u_ac : t_ac;
+      bt = dir ? -(t_ac * pv) : u_ac * pv;
+    }
+    const cplx b1 = {__shfl_down_sync(0xffffffffu, bt.re, 1), __shfl_down_sync(0xffffffffu, bt.im, 1)};
+    const cplx b2 = {__shfl_down_sync(0xffffffffu, bt.re, 2), __shfl_down_sync(0xffffffffu, bt.im, 2)};
+    if (lane < 9 && c == 0) o.bnear[(size_t)3 * p + a] = (cplx{0.0, 0.0} + bt + b1) + b2;
+  }
+  if constexpr (!DYN && (OUT & OUT_ROWSUM)) {
+    if (lane < 9) o.snear[(size_t)9 * p + 3 * a + c] = to_c(t_ac).re;
+  }
+}
+
+// Self rule accumulation shared by the static and dynamic self kernels.
+template <bool DYN>
+__device__ __forceinline__ void self_accumulate(const Geo& g, const Phys<DYN>& ph, int j,
+                                                Acc<typename Phys<DYN>::S>& acc) {
+  const int lane = threadIdx.x & 31;
+  const double xi = g.cx[j], yi = g.cy[j], zi = g.cz[j];
+  const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j];
+  acc_zero(acc);
+  const double4* sp = g.self_pts + (size_t)j * kSelfQ;
+  for (int q = lane; q < kSelfQ; q += 32) {
+    double4 y = sp[q];
+    double dx = y.x - xi, dy = y.y - yi, dz = y.z - zi;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    double ir = rsqrt(r2);  // one MUFU + Newton: replaces sqrt + divide (~1 ulp)
+    double r = r2 * ir;
+    dx *= ir; dy *= ir; dz *= ir;
+    double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+    ph.point(acc, r, ir, dx, dy, dz, dn, y.w);
+  }
+  acc_warp_sum(acc);
+}
+
+// Static self integrals (U_sta, T_sta of the self rule), once per mesh.
+__global__ void k_self_static(Geo g, Phys<false> ph, double* u_self, double* t_self) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= g.n_e) return;
+  Acc<double> acc;
+  self_accumulate(g, ph, j, acc);
+  if ((threadIdx.x & 31) != 0) return;
+  double U[3][3], T[3][3];
+  acc_finalize(acc, g.nx[j], g.ny[j], g.nz[j], ph.i4pm(), ph.i4p(), U, T);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      u_self[9 * j + 3 * a + b] = U[a][b];
+      t_self[9 * j + 3 * a + b] = T[a][b];
+    }
+}
+
+// Row sums of the static off-diagonal T (assembly.py:204-205), fixed order:
+// far/mid tiles ascending, then the row's near pairs ascending in j.
+__global__ void k_rowsum_finalize(Geo g, const double* spart, const double* snear,
+                                  const double* t_self, double* rowsums, double* diag_base,
+                                  int ntile) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= g.n_e * 9) return;
+  int i = tid / 9, ab = tid % 9;
+  double s = 0.0;
+  for (int t = 0; t < ntile; ++t) s += spart[((size_t)t * g.n_e + i) * 9 + ab];
+  for (int p = g.near_ptr[i]; p < g.near_ptr[i + 1]; ++p) s += snear[(size_t)9 * p + ab];
+  rowsums[tid] = s;
+  diag_base[tid] = -s - t_self[tid];
+}
+
+// Exterior-problem diagonal: the reference enforces the
+// interior identity c + PV int T = 0 (assembly.py:243-246); an unbounded
+// medium needs c + PV int T = I, i.e. +I on every T diagonal block.  No
+// reference mode exists, so this option's parity is unpinned.
+__global__ void k_diag_shift(int n_e, double* diag_base, double shift) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_e) return;
+  for (int a = 0; a < 3; ++a) diag_base[9 * e + 4 * a] += shift;
+}
+
+// Static diagonal for omega = 0 (assembly.py:207-216): T_ee = -rowsum, U_ee = U_sta_self.
+__global__ void k_static_diag(int n_e, const double* rowsums, const double* u_self, double* T,
+                              double* U) {
+  int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n_e * 9) return;
+  int e = tid / 9, a = (tid % 9) / 3, b = tid % 3;
+  long long N = 3LL * n_e;
+  T[(size_t)(3 * e + a) * N + 3 * e + b] = -rowsums[tid];
+  U[(size_t)(3 * e + a) * N + 3 * e + b] = u_self[tid];
+}
+
+// 3x3 complex inverse by Gauss-Jordan with partial pivoting on |re|+|im|
+// (LAPACK izamax / dcabs1, as np.linalg.inv uses); exact-zero pivot ->
+// singular (linsolve.py:95-99 falls back to the identity).
+__device__ bool inv3(const cplx Ain[3][3], cplx Inv[3][3]) {
+  cplx M[3][6];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      M[r][c] = Ain[r][c];
+      M[r][3 + c] = {r == c ? 1.0 : 0.0, 0.0};
+    }
+  for (int col = 0; col < 3; ++col) {
+    int piv = col;
+    double best = fabs(M[col][col].re) + fabs(M[col][col].im);
+    for (int r = col + 1; r < 3; ++r) {
+      double v = fabs(M[r][col].re) + fabs(M[r][col].im);
+      if (v > best) { best = v; piv = r; }
+    }
+    if (best == 0.0) return false;
+    if (piv != col)
+      for (int c = 0; c < 6; ++c) { cplx tmp = M[col][c]; M[col][c] = M[piv][c]; M[piv][c] = tmp; }
+    cplx inv_p = cdiv(cplx{1.0, 0.0}, M[col][col]);
+    for (int c = 0; c < 6; ++c) M[col][c] = M[col][c] * inv_p;
+    for (int r = 0; r < 3; ++r) {
+      if (r == col) continue;
+      cplx f = M[r][col];
+      for (int c = 0; c < 6; ++c) M[r][c] = M[r][c] - f * M[col][c];
+    }
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) Inv[r][c] = M[r][3 + c];
+  return true;
+}
+
+__device__ __forceinline__ void write_pinv(cplx* pinv, int e, const cplx D[3][3], int* singular) {
+  cplx Inv[3][3];
+  if (!inv3(D, Inv)) {
+    atomicAdd(singular, 1);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) Inv[a][b] = {a == b ? 1.0 : 0.0, 0.0};
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) pinv[9 * e + 3 * a + b] = Inv[a][b];
+}
+
+// Dynamic diagonal blocks (assembly.py:239-246):
+//   U_jj = U_dyn_self,  T_jj = -rowsum_j + (T_dyn_self - T_sta_self).
+// In system mode also: BC mix, b finalisation for row j, P^{-1} block.
+template <int OUT>
+__global__ void __launch_bounds__(128) k_self_dyn(Geo g, Phys<true> ph, PairOut o,
+                                                  const double* diag_base, int ntile) {
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= g.n_e) return;
+  const long long N = 3LL * g.n_e;
+  Acc<cplx> acc;
+  self_accumulate(g, ph, j, acc);
+  cplx U[3][3], T[3][3];
+  acc_finalize(acc, g.nx[j], g.ny[j], g.nz[j], ph.i4pm(), ph.i4p(), U, T);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) T[a][b] = T[a][b] + cplx{diag_base[9 * j + 3 * a + b], 0.0};
+  if (lane == 0) {
+    bool ok = true;
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
+    if (!ok) o.flags[0] = 1;
+  }
+  if constexpr (OUT & OUT_TU) {
+    if (lane == 0) {
+      store_block((cplx*)o.T, N, j, j, T);
+      store_block((cplx*)o.U, N, j, j, U);
+    }
+  }
+  if constexpr (OUT & OUT_SYS) {
+    // b_j: lanes split the far/mid tile partials (fixed stride order), then
+    // the near partials of row j, then the self contribution.
+    cplx bs[3];
+    for (int a = 0; a < 3; ++a) {
+      cplx s = {0.0, 0.0};
+      for (int t = lane; t < ntile; t += 32) s = s + o.bpart[(size_t)t * N + 3 * j + a];
+      warp_sum(s);
+      bs[a] = s;
+    }
+    if (lane != 0) return;
+    for (int p = g.near_ptr[j]; p < g.near_ptr[j + 1]; ++p)
+      for (int a = 0; a < 3; ++a) bs[a] = bs[a] + o.bnear[(size_t)3 * p + a];
+    cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+    sys_block(o.sys, N, j, j, U, T, bc);
+    for (int a = 0; a < 3; ++a) o.sys.b[3 * j + a] = bs[a] + bc[a];
+    cplx D[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int c = 0; c < 3; ++c) D[a][c] = o.sys.A[(size_t)(3 * j + a) * N + 3 * j + c];
+    write_pinv(o.sys.pinv, j, D, o.flags + 1);
+  }
+}
+
+// Standalone apply_bcs (assembly.py:263-297) for user-supplied T, U.
+__global__ void k_apply_bcs_cols(const cplx* T, const cplx* U, const uint8_t* kinds, long long n,
+                                 cplx* A) {
+  size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n * n) return;
+  size_t c = idx % n;
+  A[idx] = kinds[c] == kDirichlet ? -U[idx] : T[idx];
+}
+
+// b = U[:,N] p_N - T[:,D] p_D : warp per row, fixed lane-strided order.
+__global__ void k_apply_bcs_rhs(const cplx* T, const cplx* U, const uint8_t* kinds, const cplx* p,
+                                long long n, cplx* b) {
+  long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  cplx sn = {0, 0}, sd = {0, 0};
+  for (long long c = lane; c < n; c += 32) {
+    if (kinds[c] == kDirichlet) cfma(sd, T[row * n + c], p[c]);
+    else cfma(sn, U[row * n + c], p[c]);
+  }
+  warp_sum(sn);
+  warp_sum(sd);
+  if (lane == 0) b[row] = sn - sd;
+}
+
+__global__ void k_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int* singular) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n / 3) return;
+  cplx D[3][3];
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < 3; ++c) D[a][c] = A[(size_t)(3 * e + a) * n + 3 * e + c];
+  write_pinv(pinv, e, D, singular);
+}
+
+// ---------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------
+static inline unsigned blocks_for(long long threads, int bs) {
+  return (unsigned)((threads + bs - 1) / bs);
+}
+
+StaticConst static_const(const Context& c) {
+  StaticConst s;
+  s.g2 = c.mu / (c.lam + 2.0 * c.mu);
+  s.ratio = (c.lam + 2.0 * c.mu) / c.mu;
+  s.inv4pimu = 1.0 / (4.0 * M_PI * c.mu);
+  s.inv4pi = 1.0 / (4.0 * M_PI);
+  return s;
+}
+
+FreqConst freq_const(const Context& c, double ore, double oim) {
+  // material.py:68-75, 94 and kernels.py:73-75, with Python complex
+  // arithmetic semantics (complex / real divides both parts).
+  double cs = sqrt(c.mu / c.rho), cp = sqrt((c.lam + 2.0 * c.mu) / c.rho);
+  FreqConst f;
+  f.ks = {ore / cs, oim / cs};
+  f.kp = {ore / cp, oim / cp};
+  auto cdiv_h = [](cplx a, cplx b) {
+    // CPython complex division (Smith-like, Objects/complexobject.c _Py_c_quot)
+    double abs_breal = fabs(b.re), abs_bimag = fabs(b.im);
+    cplx r;
+    if (abs_breal >= abs_bimag) {
+      double ratio = b.im / b.re, denom = b.re + b.im * ratio;
+      r = {(a.re + a.im * ratio) / denom, (a.im - a.re * ratio) / denom};
+    } else {
+      double ratio = b.re / b.im, denom = b.re * ratio + b.im;
+      r = {(a.re * ratio + a.im) / denom, (a.im * ratio - a.re) / denom};
+    }
+    return r;
+  };
+  f.iks = cdiv_h({1.0, 0.0}, f.ks);
+  f.ikp = cdiv_h({1.0, 0.0}, f.kp);
+  cplx q = cdiv_h(f.kp, f.ks);
+  f.g2 = {q.re * q.re - q.im * q.im, q.re * q.im + q.im * q.re};
+  f.ks_abs = hypot(f.ks.re, f.ks.im);
+  f.sw = kSeriesSwitch;
+  f.ratio = (c.lam + 2.0 * c.mu) / c.mu;
+  f.inv4pimu = 1.0 / (4.0 * M_PI * c.mu);
+  f.inv4pi = 1.0 / (4.0 * M_PI);
+  return f;
+}
+
+template <typename T>
+static T* dalloc(Context& c, size_t count, cudaError_t& err) {
+  void* p = nullptr;
+  if (err != cudaSuccess) return nullptr;
+  err = cudaMalloc(&p, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+  if (err == cudaSuccess) c.owned.push_back(p);
+  return (T*)p;
+}
+
+cudaError_t setup_context(Context& c, const double* centroids, const double* normals,
+                          const double* areas, const double* diameters, const double* corners,
+                          const double* gl8, const double* gl16, const double* rules_host,
+                          const int* rule_off, const int* rule_q, cudaStream_t s) {
+  cudaError_t err = cudaSuccess;
+  const int n = c.n_e;
+  c.stream = s;
+  err = upload_series(s);
+  if (err) return err;
+  // SoA geometry: 8 arrays + 9 corner arrays
+  std::vector<double> soa((size_t)17 * n);
+  for (int e = 0; e < n; ++e) {
+    for (int k = 0; k < 3; ++k) {
+      soa[(size_t)k * n + e] = centroids[3 * e + k];
+      soa[(size_t)(3 + k) * n + e] = normals[3 * e + k];
+    }
+    soa[(size_t)6 * n + e] = areas[e];
+    soa[(size_t)7 * n + e] = diameters[e];
+    for (int v = 0; v < 3; ++v)
+      for (int k = 0; k < 3; ++k)  // vx block: [v][e]; vy, vz likewise
+        soa[(size_t)(8 + 3 * k + v) * n + e] = corners[9 * e + 3 * v + k];
+  }
+  double* geo = dalloc<double>(c, soa.size(), err);
+  int n_rules_d = rule_off[6] + 4 * rule_q[6];
+  double* rules = dalloc<double>(c, n_rules_d, err);
+  double* gl = dalloc<double>(c, 48, err);
+  double* yfar = dalloc<double>(c, (size_t)9 * n, err);
+  double* ymid = dalloc<double>(c, (size_t)21 * n, err);
+  double4* selfp = dalloc<double4>(c, (size_t)kSelfQ * n, err);
+  int* near_cnt = dalloc<int>(c, n + 1, err);
+  long long* far_cnt = dalloc<long long>(c, n, err);
+  long long* mid_cnt = dalloc<long long>(c, n, err);
+  c.flags = dalloc<int>(c, 4, err);
+  if (err) return err;
+  err = cudaMemcpyAsync(geo, soa.data(), soa.size() * 8, cudaMemcpyHostToDevice, s);
+  if (err) return err;
+  err = cudaMemcpyAsync(rules, rules_host, (size_t)n_rules_d * 8, cudaMemcpyHostToDevice, s);
+  if (err) return err;
+  double glh[48];
+  for (int k = 0; k < 16; ++k) glh[k] = gl8[k];          // 8 nodes, 8 weights
+  for (int k = 0; k < 32; ++k) glh[16 + k] = gl16[k];    // 16 nodes, 16 weights
+  err = cudaMemcpyAsync(gl, glh, sizeof(glh), cudaMemcpyHostToDevice, s);
+  if (err) return err;
+  cudaMemsetAsync(c.flags, 0, 16, s);
+  Geo& g = c.g;
+  g.n_e = n;
+  g.cx = geo; g.cy = geo + n; g.cz = geo + 2 * (size_t)n;
+  g.nx = geo + 3 * (size_t)n; g.ny = geo + 4 * (size_t)n; g.nz = geo + 5 * (size_t)n;
+  g.area = geo + 6 * (size_t)n; g.diam = geo + 7 * (size_t)n;
+  g.vx = geo + 8 * (size_t)n; g.vy = geo + 11 * (size_t)n; g.vz = geo + 14 * (size_t)n;
+  g.rules = rules;
+  // rule slots: 0 gauss3, 1 gauss7, 2..5 sub1..sub4
+  g.wfar = rules + rule_off[0] + 3 * rule_q[0];
+  g.wmid = rules + rule_off[1] + 3 * rule_q[1];
+  for (int L = 1; L <= kMaxNearLevel; ++L) g.sub[L] = RuleRef{rule_off[1 + L], rule_q[1 + L]};
+  g.sub[0] = RuleRef{rule_off[1], rule_q[1]};
+  g.yfar = yfar;
+  g.ymid = ymid;
+  g.self_pts = selfp;
+  EWB_NOTE k_field_points<<<blocks_for(n, 128), 128, 0, s>>>(g, rules + rule_off[0], rules + rule_off[1],
+                                                    yfar, ymid);
+  EWB_NOTE k_self_rule<<<blocks_for((long long)n * 48, 128), 128, 0, s>>>(g, gl, gl + 16, selfp);
+  EWB_NOTE k_near_count<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_cnt, far_cnt, mid_cnt);
+  err = cudaGetLastError();
+  if (err) return err;
+  std::vector<int> cnt(n);
+  std::vector<long long> fc(n), mc(n);
+  cudaMemcpyAsync(cnt.data(), near_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(fc.data(), far_cnt, (size_t)n * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(mc.data(), mid_cnt, (size_t)n * 8, cudaMemcpyDeviceToHost, s);
+  err = cudaStreamSynchronize(s);
+  if (err) return err;
+  std::vector<int> ptr(n + 1, 0);
+  c.n_far = c.n_mid = 0;
+  for (int e = 0; e < n; ++e) {
+    ptr[e + 1] = ptr[e] + cnt[e];
+    c.n_far += fc[e];
+    c.n_mid += mc[e];
+  }
+  c.n_near = ptr[n];
+  int* near_ptr = dalloc<int>(c, n + 1, err);
+  int* near_j = dalloc<int>(c, c.n_near, err);
+  int* near_row = dalloc<int>(c, c.n_near, err);
+  int* near_lvl = dalloc<int>(c, c.n_near, err);
+  if (err) return err;
+  cudaMemcpyAsync(near_ptr, ptr.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, s);
+  g.near_ptr = near_ptr; g.near_j = near_j; g.near_row = near_row; g.near_lvl = near_lvl;
+  EWB_NOTE k_near_fill<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_ptr, near_j, near_row,
+                                                                 near_lvl);
+  // near level census
+  std::vector<int> lv(c.n_near);
+  if (c.n_near) cudaMemcpyAsync(lv.data(), near_lvl, (size_t)c.n_near * 4, cudaMemcpyDeviceToHost, s);
+  err = cudaStreamSynchronize(s);
+  if (err) return err;
+  for (int L = 0; L <= kMaxNearLevel; ++L) c.n_near_lvl[L] = 0;
+  for (int v : lv) c.n_near_lvl[v]++;
+  c.n_tiles = (n + 31) / 32;
+  c.rowsums = dalloc<double>(c, (size_t)9 * n, err);
+  c.u_sta_self = dalloc<double>(c, (size_t)9 * n, err);
+  c.t_sta_self = dalloc<double>(c, (size_t)9 * n, err);
+  c.diag_base = dalloc<double>(c, (size_t)9 * n, err);
+  c.bpart = dalloc<cplx>(c, (size_t)c.n_tiles * 3 * n, err);
+  c.bnear = dalloc<cplx>(c, (size_t)3 * c.n_near + 1, err);
+  c.spart = dalloc<double>(c, (size_t)c.n_tiles * 9 * n, err);
+  c.snear = dalloc<double>(c, (size_t)9 * c.n_near + 1, err);
+  if (err) return err;
+  // the static pass is part of setup: row sums feed every frequency
+  return launch_static_pass(c, nullptr, nullptr, s);
+}
+
+cudaError_t launch_static_pass(Context& c, double* t_out, double* u_out, cudaStream_t s) {
+  Phys<false> ph{static_const(c)};
+  PairOut o{};
+  o.T = t_out; o.U = u_out; o.spart = c.spart; o.snear = c.snear; o.flags = c.flags;
+  const int n = c.n_e;
+  long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  if (t_out) {
+    EWB_NOTE k_farmid<false, OUT_TU | OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+    if (c.n_near)
+      EWB_NOTE k_near<false, OUT_TU | OUT_ROWSUM><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(
+          c.g, ph, o, c.n_near);
+  } else {
+    EWB_NOTE k_farmid<false, OUT_ROWSUM><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, ph, o);
+    if (c.n_near)
+      EWB_NOTE k_near<false, OUT_ROWSUM><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(
+          c.g, ph, o, c.n_near);
+  }
+  EWB_NOTE k_self_static<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, c.u_sta_self,
+                                                                   c.t_sta_self);
+  EWB_NOTE k_rowsum_finalize<<<blocks_for((long long)n * 9, 128), 128, 0, s>>>(
+      c.g, c.spart, c.snear, c.t_sta_self, c.rowsums, c.diag_base, c.n_tiles);
+  if (t_out)
+    EWB_NOTE k_static_diag<<<blocks_for((long long)n * 9, 128), 128, 0, s>>>(n, c.rowsums, c.u_sta_self,
+                                                                    t_out, u_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_tu(Context& c, double ore, double oim, cplx* T, cplx* U,
+                               cudaStream_t s) {
+  Phys<true> ph{freq_const(c, ore, oim)};
+  PairOut o{};
+  o.T = T; o.U = U; o.flags = c.flags;
+  const int n = c.n_e;
+  long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  Phys<true> phf = ph;
+  phf.fc.sw = kFarSwitch;
+  EWB_NOTE k_farmid<true, OUT_TU><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, phf, o);
+  if (c.n_near)
+    EWB_NOTE k_near<true, OUT_TU><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
+                                                                                 c.n_near);
+  EWB_NOTE k_self_dyn<OUT_TU><<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, o, c.diag_base,
+                                                                       c.n_tiles);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_system(Context& c, double ore, double oim, const uint8_t* kinds,
+                                   const cplx* prescribed, cplx* A, cplx* b, cplx* pinv,
+                                   cudaStream_t s) {
+  Phys<true> ph{freq_const(c, ore, oim)};
+  PairOut o{};
+  o.sys = SysArgs{kinds, prescribed, A, pinv, b};
+  o.bpart = c.bpart; o.bnear = c.bnear; o.flags = c.flags;
+  const int n = c.n_e;
+  long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  Phys<true> phf = ph;
+  phf.fc.sw = kFarSwitch;
+  EWB_NOTE k_farmid<true, OUT_SYS><<<blocks_for(warps * 32, 128), 128, 0, s>>>(c.g, phf, o);
+  if (c.n_near)
+    EWB_NOTE k_near<true, OUT_SYS><<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, ph, o,
+                                                                                   c.n_near);
+  EWB_NOTE k_self_dyn<OUT_SYS><<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(c.g, ph, o, c.diag_base,
+                                                                        c.n_tiles);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_bcs(const cplx* T, const cplx* U, const uint8_t* kinds, const cplx* p,
+                             long long n, cplx* A, cplx* b, cudaStream_t s) {
+  EWB_NOTE k_apply_bcs_cols<<<blocks_for(n * n, 256), 256, 0, s>>>(T, U, kinds, n, A);
+  EWB_NOTE k_apply_bcs_rhs<<<blocks_for(n * 32, 128), 128, 0, s>>>(T, U, kinds, p, n, b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int* singular,
+                                     cudaStream_t s) {
+  EWB_NOTE k_blockdiag_inverse<<<blocks_for(n / 3, 128), 128, 0, s>>>(A, n, pinv, singular);
+  return cudaGetLastError();
+}
+
+cudaError_t set_exterior(Context& c, int on, cudaStream_t s) {
+  on = on ? 1 : 0;
+  if (on == c.exterior) return cudaSuccess;
+  EWB_NOTE k_diag_shift<<<blocks_for(c.n_e, 128), 128, 0, s>>>(c.n_e, c.diag_base,
+                                                                on ? 1.0 : -1.0);
+  c.exterior = on;
+  return cudaGetLastError();
+}
+
+}  // namespace ewb

@@ -1,0 +1,465 @@
+// extern "C" boundary (include/ewbem_b200.h).  Validation, error codes and
+// the thread-local error string live here; kernels live in the other files.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ewbem_b200.h"
+#include "ewb_ctx.cuh"
+#include "ewb_krylov.cuh"
+
+namespace ewb {
+cudaError_t launch_window_idft(const cplx* half, long long n_half, long long D, const double* win,
+                               const cplx* tw, double eta_dt, double* out, double* residue,
+                               cudaStream_t s);
+}
+
+struct ewb_ctx {
+  ewb::Context c;
+};
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void ewb::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(EWB_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define EWB_CUDA(call, where)                 \
+  do {                                        \
+    cudaError_t e_ = (call);                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int ewb_abi_version(void) { return EWB_ABI_VERSION; }
+
+const char* ewb_last_error(void) { return g_err.c_str(); }
+
+int64_t ewb_launch_count(void) { return g_launches.load(); }
+
+int ewb_ctx_create(const double* centroids, const double* normals, const double* areas,
+                   const double* diameters, const double* corners, int64_t n_elements,
+                   double lam, double mu, double rho, const double* gl8, const double* gl16,
+                   const double* rules, const int32_t* rule_off, const int32_t* rule_q,
+                   void* stream, ewb_ctx** out) {
+  if (!out || !centroids || !normals || !areas || !diameters || !corners || !gl8 || !gl16 ||
+      !rules || !rule_off || !rule_q)
+    return fail(EWB_ERR_INVALID, "ewb_ctx_create: null argument");
+  if (n_elements < 1 || n_elements > (1LL << 22))
+    return fail(EWB_ERR_INVALID, "ewb_ctx_create: n_elements out of range");
+  if (!(mu > 0) || !(rho > 0) || !(lam + 2 * mu > 0))
+    return fail(EWB_ERR_INVALID, "ewb_ctx_create: invalid material");
+  for (int k = 0; k < 6; ++k)
+    if (rule_q[k] < 1) return fail(EWB_ERR_INVALID, "ewb_ctx_create: empty rule table");
+  auto* h = new ewb_ctx();
+  h->c.n_e = (int)n_elements;
+  h->c.lam = lam;
+  h->c.mu = mu;
+  h->c.rho = rho;
+  cudaError_t e = ewb::setup_context(h->c, centroids, normals, areas, diameters, corners, gl8,
+                                     gl16, rules, rule_off, rule_q, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e != cudaSuccess) {
+    for (void* p : h->c.owned) cudaFree(p);
+    delete h;
+    return cuda_fail(e, "ewb_ctx_create");
+  }
+  *out = h;
+  return EWB_OK;
+}
+
+int ewb_ctx_destroy(ewb_ctx* ctx) {
+  if (!ctx) return EWB_OK;
+  cudaDeviceSynchronize();
+  for (void* p : ctx->c.owned) cudaFree(p);
+  delete ctx;
+  return EWB_OK;
+}
+
+int ewb_ctx_set_exterior(ewb_ctx* ctx, int32_t on, void* stream) {
+  if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_set_exterior: null argument");
+  EWB_CUDA(ewb::set_exterior(ctx->c, on, S(stream)), "ewb_ctx_set_exterior");
+  return EWB_OK;
+}
+
+int ewb_ctx_counts(const ewb_ctx* ctx, int64_t* counts) {
+  if (!ctx || !counts) return fail(EWB_ERR_INVALID, "ewb_ctx_counts: null argument");
+  counts[0] = ctx->c.n_e;
+  counts[1] = ctx->c.n_far;
+  counts[2] = ctx->c.n_mid;
+  counts[3] = ctx->c.n_near;
+  for (int L = 1; L <= 4; ++L) counts[3 + L] = ctx->c.n_near_lvl[L];
+  return EWB_OK;
+}
+
+int ewb_static_rowsums(ewb_ctx* ctx, double* out, void* stream) {
+  if (!ctx || !out) return fail(EWB_ERR_INVALID, "ewb_static_rowsums: null argument");
+  EWB_CUDA(cudaMemcpyAsync(out, ctx->c.rowsums, sizeof(double) * 9 * ctx->c.n_e,
+                           cudaMemcpyDeviceToDevice, S(stream)),
+           "ewb_static_rowsums");
+  return EWB_OK;
+}
+
+int ewb_static_tu(ewb_ctx* ctx, double* t, double* u, void* stream) {
+  if (!ctx || !t || !u) return fail(EWB_ERR_INVALID, "ewb_static_tu: null argument");
+  EWB_CUDA(ewb::launch_static_pass(ctx->c, t, u, S(stream)), "ewb_static_tu");
+  return EWB_OK;
+}
+
+static int check_omega(double ore, double oim, const char* who) {
+  // material.py:92-93
+  double mag = std::hypot(ore, oim);
+  if (!std::isfinite(ore) || !std::isfinite(oim))
+    return fail(EWB_ERR_INVALID, std::string(who) + ": non-finite frequency");
+  if (oim > 1e-12 * (mag > 1.0 ? mag : 1.0))
+    return fail(EWB_ERR_INVALID, std::string(who) + ": frequency has positive imaginary part");
+  if (ore == 0.0 && oim == 0.0)
+    return fail(EWB_ERR_INVALID, std::string(who) + ": omega == 0 takes the static path");
+  return EWB_OK;
+}
+
+int ewb_assemble_tu(ewb_ctx* ctx, double ore, double oim, void* t, void* u, void* stream) {
+  if (!ctx || !t || !u) return fail(EWB_ERR_INVALID, "ewb_assemble_tu: null argument");
+  if (int rc = check_omega(ore, oim, "ewb_assemble_tu")) return rc;
+  EWB_CUDA(ewb::launch_assemble_tu(ctx->c, ore, oim, (ewb::cplx*)t, (ewb::cplx*)u, S(stream)),
+           "ewb_assemble_tu");
+  return EWB_OK;
+}
+
+int ewb_assemble_system(ewb_ctx* ctx, double ore, double oim, const uint8_t* kinds,
+                        const void* p, void* a, void* b, void* pinv, void* stream) {
+  if (!ctx || !kinds || !p || !a || !b || !pinv)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system: null argument");
+  if (int rc = check_omega(ore, oim, "ewb_assemble_system")) return rc;
+  EWB_CUDA(ewb::launch_assemble_system(ctx->c, ore, oim, kinds, (const ewb::cplx*)p,
+                                       (ewb::cplx*)a, (ewb::cplx*)b, (ewb::cplx*)pinv, S(stream)),
+           "ewb_assemble_system");
+  return EWB_OK;
+}
+
+int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite, int32_t* singular, void* stream) {
+  if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_flags: null argument");
+  int h[4] = {0, 0, 0, 0};
+  EWB_CUDA(cudaMemcpyAsync(h, ctx->c.flags, 16, cudaMemcpyDeviceToHost, S(stream)), "ewb_ctx_flags");
+  EWB_CUDA(cudaMemsetAsync(ctx->c.flags, 0, 16, S(stream)), "ewb_ctx_flags");
+  EWB_CUDA(cudaStreamSynchronize(S(stream)), "ewb_ctx_flags");
+  if (nonfinite) *nonfinite = h[0];
+  if (singular) *singular = h[1];
+  return EWB_OK;
+}
+
+int ewb_apply_bcs(const void* t, const void* u, const uint8_t* kinds, const void* p, int64_t n,
+                  void* a, void* b, void* stream) {
+  if (!t || !u || !kinds || !p || !a || !b || n < 1)
+    return fail(EWB_ERR_INVALID, "ewb_apply_bcs: bad argument");
+  EWB_CUDA(ewb::launch_apply_bcs((const ewb::cplx*)t, (const ewb::cplx*)u, kinds,
+                                 (const ewb::cplx*)p, n, (ewb::cplx*)a, (ewb::cplx*)b, S(stream)),
+           "ewb_apply_bcs");
+  return EWB_OK;
+}
+
+int ewb_blockdiag_inverse(const void* a, int64_t n, void* pinv, int32_t* singular, void* stream) {
+  if (!a || !pinv || !singular) return fail(EWB_ERR_INVALID, "ewb_blockdiag_inverse: null argument");
+  if (n < 3 || n % 3)
+    return fail(EWB_ERR_INVALID, "matrix must be square with size divisible by 3");
+  EWB_CUDA(ewb::launch_blockdiag_inverse((const ewb::cplx*)a, n, (ewb::cplx*)pinv, singular,
+                                         S(stream)),
+           "ewb_blockdiag_inverse");
+  return EWB_OK;
+}
+
+int ewb_gemv_batched(const void* a, const void* x, void* y, int64_t n, int32_t batch,
+                     void* stream) {
+  if (!a || !x || !y || n < 1 || batch < 1)
+    return fail(EWB_ERR_INVALID, "ewb_gemv_batched: bad argument");
+  EWB_CUDA(ewb::launch_gemv_batched((const ewb::cplx*)a, (const ewb::cplx*)x, (ewb::cplx*)y, n,
+                                    batch, S(stream)),
+           "ewb_gemv_batched");
+  return EWB_OK;
+}
+
+// workspace layout: r, w, z (3n), V ((restart+1) n), H, partial
+int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart) {
+  int64_t cpl = 16;
+  int64_t G = ewb::solver_grid_blocks();
+  return cpl * (3 * n + (int64_t)(restart + 1) * n +
+                2 * (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart +
+                2 * G * (2 * ewb::kMaxRestart + 2)) +
+         8 * 2 * G * 16 + 256 * 8;
+}
+
+int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t has_x0, int64_t n,
+              double tol, int32_t restart, int32_t maxiter, void* ws, int64_t ws_bytes,
+              double* hist, int32_t hist_cap, ewb_gmres_result* result, void* stream) {
+  if (!a || !b || !x || !ws || !hist || !result || n < 1)
+    return fail(EWB_ERR_INVALID, "ewb_gmres: bad argument");
+  if (!(tol > 0.0 && tol < 1.0)) return fail(EWB_ERR_INVALID, "tol must be in (0, 1)");
+  if (restart < 1 || restart > ewb::kMaxRestart)
+    return fail(EWB_ERR_INVALID, "ewb_gmres: restart must be in [1, 128]");
+  if (maxiter < 0) return fail(EWB_ERR_INVALID, "ewb_gmres: maxiter must be >= 0");
+  if (pinv && n % 3) return fail(EWB_ERR_INVALID, "ewb_gmres: preconditioner needs n % 3 == 0");
+  if (ws_bytes < ewb_gmres_workspace_bytes(n, restart))
+    return fail(EWB_ERR_INVALID, "ewb_gmres: workspace too small");
+  ewb::GmresArgs g{};
+  auto* base = (ewb::cplx*)ws;
+  g.A = (const ewb::cplx*)a;
+  g.b = (const ewb::cplx*)b;
+  g.pinv = (const ewb::cplx*)pinv;
+  g.x = (ewb::cplx*)x;
+  g.r = base;
+  g.w = base + n;
+  g.z = base + 2 * n;
+  g.V = base + 3 * n;
+  g.H = g.V + (int64_t)(restart + 1) * n;
+  g.Gram = g.H + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
+  g.dpart = g.Gram + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
+  g.partial = (double*)(g.dpart + 2 * (int64_t)ewb::solver_grid_blocks() *
+                                      (2 * ewb::kMaxRestart + 2));
+  {
+    const char* env = getenv("EWB_GMRES_ORTHO");
+    g.ortho = env ? atoi(env) : 0;
+  }
+  g.probe = nullptr;
+  g.probe_cap = 0;
+  {
+    // diagnostics: EWB_GMRES_PROBE=<device address> enables the phase trace
+    const char* env = getenv("EWB_GMRES_PROBE");
+    if (env) {
+      g.probe = (unsigned long long*)strtoull(env, nullptr, 0);
+      g.probe_cap = 1 << 16;
+    }
+  }
+  g.hist = hist;
+  g.out = (ewb::GmresOut*)result;
+  g.n = n;
+  g.restart = restart;
+  g.maxiter = maxiter;
+  g.has_x0 = has_x0;
+  g.hist_cap = hist_cap;
+  g.tol = tol;
+  EWB_CUDA(ewb::launch_gmres(g, S(stream)), "ewb_gmres");
+  return EWB_OK;
+}
+
+int64_t ewb_sem_workspace_bytes(int64_t n, int32_t K) {
+  int64_t G = ewb::solver_grid_blocks();
+  return 16 * (2 * (int64_t)K * n) + 8 * 2 * G * 16 + 256 * 8;
+}
+
+int ewb_sem_guess(const void* a, const void* b, const void* xh, int32_t K, int64_t n,
+                  double rank_tol, void* x0, void* ws, int64_t ws_bytes, ewb_sem_result* result,
+                  void* stream) {
+  if (!a || !b || !xh || !x0 || !ws || !result || n < 1)
+    return fail(EWB_ERR_INVALID, "ewb_sem_guess: bad argument");
+  if (K < 1 || K > ewb::kMaxSem) return fail(EWB_ERR_INVALID, "ewb_sem_guess: K must be in [1, 4]");
+  if (ws_bytes < ewb_sem_workspace_bytes(n, K))
+    return fail(EWB_ERR_INVALID, "ewb_sem_guess: workspace too small");
+  ewb::SemArgs s{};
+  auto* base = (ewb::cplx*)ws;
+  s.A = (const ewb::cplx*)a;
+  s.b = (const ewb::cplx*)b;
+  s.X = (const ewb::cplx*)xh;
+  s.Y = base;
+  s.Q = base + (int64_t)K * n;
+  s.partial = (double*)(base + 2 * (int64_t)K * n);
+  s.x0 = (ewb::cplx*)x0;
+  s.out = (ewb::SemOut*)result;
+  s.n = n;
+  s.K = K;
+  s.rank_tol = rank_tol;
+  EWB_CUDA(ewb::launch_sem(s, S(stream)), "ewb_sem_guess");
+  return EWB_OK;
+}
+
+int ewb_window_idft(const void* half, int64_t n_half, int64_t D, int32_t window, double eta,
+                    double period, double* out, double* residue, void* stream) {
+  if (!half || !out || !residue || n_half < 2 || D < 1)
+    return fail(EWB_ERR_INVALID, "ewb_window_idft: bad argument");
+  if (window < 0 || window > 2) return fail(EWB_ERR_INVALID, "ewb_window_idft: unknown window");
+  const int64_t N = 2 * (n_half - 1);
+  if (N > 4096) return fail(EWB_ERR_INVALID, "ewb_window_idft: N > 4096 unsupported");
+  // host-exact tables: window_weights (transform.py:157-176) and e^{2 pi i m / N}
+  std::vector<double> tab(3 * N);
+  for (int64_t k = 0; k < N; ++k) {
+    double ph = 2.0 * M_PI * (double)k / (double)N;
+    double w = 1.0;
+    if (window == EWB_WIN_HANNING) w = 0.5 * (1.0 + std::cos(ph));
+    else if (window == EWB_WIN_BLACKMAN) w = 0.42 + 0.5 * std::cos(ph) + 0.08 * std::cos(2.0 * ph);
+    tab[k] = w;
+    tab[N + 2 * k] = std::cos(ph);
+    tab[N + 2 * k + 1] = std::sin(ph);
+  }
+  void* dtab = nullptr;
+  EWB_CUDA(cudaMallocAsync(&dtab, sizeof(double) * 3 * N, S(stream)), "ewb_window_idft");
+  EWB_CUDA(cudaMemcpyAsync(dtab, tab.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice,
+                           S(stream)),
+           "ewb_window_idft");
+  double dt = period / (double)N;
+  EWB_CUDA(ewb::launch_window_idft((const ewb::cplx*)half, n_half, D, (const double*)dtab,
+                                   (const ewb::cplx*)((double*)dtab + N), eta * dt, out, residue,
+                                   S(stream)),
+           "ewb_window_idft");
+  EWB_CUDA(cudaFreeAsync(dtab, S(stream)), "ewb_window_idft");
+  // the host table must outlive the async copy
+  EWB_CUDA(cudaStreamSynchronize(S(stream)), "ewb_window_idft");
+  return EWB_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------
+// matrix-free, pair-kernel microbenchmark, FP64 probe
+// ---------------------------------------------------------------------
+namespace ewb {
+size_t mf_workspace_bytes(const Context& c, int K);
+cudaError_t launch_matfree(Context& c, double ore, double oim, const cplx* vt, const cplx* vu,
+                           int K, cplx* y, const uint8_t* kinds, cplx* pinv, void* ws,
+                           cudaStream_t s);
+cudaError_t launch_pair_blocks(const double* x, long long P, const double* tri, long long M,
+                               const FreqConst* fcs_dev, int F, const double* b7, const double* w7,
+                               cplx* u, cplx* t, cudaStream_t s);
+cudaError_t launch_pair_reduce(const double* x, long long P, const double* tri, long long M,
+                               const cplx* xv, const FreqConst* fcs_dev, int F, const double* b7,
+                               const double* w7, cplx* yu, cplx* yt, cplx* part, int nchunk,
+                               cudaStream_t s);
+cudaError_t fp64_peak_probe(long long iters, int blocks_per_sm, double* tflops, double* ms,
+                            cudaStream_t s);
+}  // namespace ewb
+
+static int pair_chunks(int64_t P, int64_t M) {
+  (void)M;
+  int64_t pblocks = (P + 127) / 128;
+  int64_t want = (148 * 4 + pblocks - 1) / pblocks;
+  if (want < 1) want = 1;
+  if (want > 16) want = 16;
+  return (int)want;
+}
+
+// gauss7 tables exactly as quadrature.py:75-88 builds them.
+static void gauss7_tables(double b7[21], double w7[7]) {
+  double s15 = std::sqrt(15.0);
+  double a = (6.0 + s15) / 21.0, b = (6.0 - s15) / 21.0;
+  double wa = (155.0 + s15) / 1200.0, wb = (155.0 - s15) / 1200.0;
+  b7[0] = b7[1] = b7[2] = 1.0 / 3;
+  w7[0] = 9.0 / 40.0;
+  int q = 1;
+  for (int g = 0; g < 2; ++g) {
+    double v = g == 0 ? a : b, w = g == 0 ? wa : wb, o = 1 - 2 * v;
+    double pts[3][3] = {{v, v, o}, {v, o, v}, {o, v, v}};
+    for (int k = 0; k < 3; ++k, ++q) {
+      for (int c = 0; c < 3; ++c) b7[3 * q + c] = pts[k][c];
+      w7[q] = w;
+    }
+  }
+}
+
+extern "C" {
+
+int64_t ewb_matfree_workspace_bytes(const ewb_ctx* ctx, int32_t K) {
+  if (!ctx || K < 1 || K > 5) return -1;
+  return (int64_t)ewb::mf_workspace_bytes(ctx->c, K);
+}
+
+int ewb_matfree_apply(ewb_ctx* ctx, double ore, double oim, const void* vt, const void* vu,
+                      int32_t K, void* y, const uint8_t* kinds, void* pinv, void* ws,
+                      int64_t ws_bytes, void* stream) {
+  if (!ctx || !vt || !y || !ws) return fail(EWB_ERR_INVALID, "ewb_matfree_apply: null argument");
+  if (K < 1 || K > 5) return fail(EWB_ERR_INVALID, "ewb_matfree_apply: K must be in [1, 5]");
+  if (int rc = check_omega(ore, oim, "ewb_matfree_apply")) return rc;
+  if (ws_bytes < (int64_t)ewb::mf_workspace_bytes(ctx->c, K))
+    return fail(EWB_ERR_INVALID, "ewb_matfree_apply: workspace too small");
+  EWB_CUDA(ewb::launch_matfree(ctx->c, ore, oim, (const ewb::cplx*)vt, (const ewb::cplx*)vu, K,
+                               (ewb::cplx*)y, kinds, (ewb::cplx*)pinv, ws, S(stream)),
+           "ewb_matfree_apply");
+  return EWB_OK;
+}
+
+static int pair_prep(const double* omega_host, int32_t F, double lam, double mu, double rho,
+                     cudaStream_t s, void** dev_tables) {
+  // tables: FreqConst[F] | b7[21] | w7[7]
+  ewb::Context tmp;
+  tmp.lam = lam; tmp.mu = mu; tmp.rho = rho;
+  std::vector<ewb::FreqConst> fcs(F);
+  for (int f = 0; f < F; ++f) fcs[f] = ewb::freq_const(tmp, omega_host[2 * f], omega_host[2 * f + 1]);
+  double b7[21], w7[7];
+  gauss7_tables(b7, w7);
+  size_t bytes = sizeof(ewb::FreqConst) * F + 28 * 8;
+  std::vector<unsigned char> h(bytes);
+  memcpy(h.data(), fcs.data(), sizeof(ewb::FreqConst) * F);
+  memcpy(h.data() + sizeof(ewb::FreqConst) * F, b7, 21 * 8);
+  memcpy(h.data() + sizeof(ewb::FreqConst) * F + 21 * 8, w7, 7 * 8);
+  EWB_CUDA(cudaMallocAsync(dev_tables, bytes, s), "pair kernels");
+  EWB_CUDA(cudaMemcpyAsync(*dev_tables, h.data(), bytes, cudaMemcpyHostToDevice, s), "pair kernels");
+  EWB_CUDA(cudaStreamSynchronize(s), "pair kernels");
+  return EWB_OK;
+}
+
+int ewb_pair_kernels_blocks(const double* x, int64_t P, const double* tri, int64_t M,
+                            const double* omega_host, int32_t F, double lam, double mu, double rho,
+                            void* u, void* t, void* stream) {
+  if (!x || !tri || !omega_host || !u || !t || P < 1 || M < 1 || F < 1)
+    return fail(EWB_ERR_INVALID, "ewb_pair_kernels_blocks: bad argument");
+  for (int f = 0; f < F; ++f)
+    if (int rc = check_omega(omega_host[2 * f], omega_host[2 * f + 1], "ewb_pair_kernels_blocks"))
+      return rc;
+  void* tab = nullptr;
+  if (int rc = pair_prep(omega_host, F, lam, mu, rho, S(stream), &tab)) return rc;
+  auto* fcs = (const ewb::FreqConst*)tab;
+  const double* b7 = (const double*)((unsigned char*)tab + sizeof(ewb::FreqConst) * F);
+  EWB_CUDA(ewb::launch_pair_blocks(x, P, tri, M, fcs, F, b7, b7 + 21, (ewb::cplx*)u,
+                                   (ewb::cplx*)t, S(stream)),
+           "ewb_pair_kernels_blocks");
+  EWB_CUDA(cudaFreeAsync(tab, S(stream)), "ewb_pair_kernels_blocks");
+  return EWB_OK;
+}
+
+int64_t ewb_pair_kernels_workspace_bytes(int64_t P, int64_t M, int32_t F) {
+  return (int64_t)pair_chunks(P, M) * F * P * 6 * 16;
+}
+
+int ewb_pair_kernels_reduce(const double* x, int64_t P, const double* tri, int64_t M,
+                            const void* xv, const double* omega_host, int32_t F, double lam,
+                            double mu, double rho, void* yu, void* yt, void* ws, int64_t ws_bytes,
+                            void* stream) {
+  if (!x || !tri || !xv || !omega_host || !yu || !yt || !ws || P < 1 || M < 1 || F < 1)
+    return fail(EWB_ERR_INVALID, "ewb_pair_kernels_reduce: bad argument");
+  if (ws_bytes < ewb_pair_kernels_workspace_bytes(P, M, F))
+    return fail(EWB_ERR_INVALID, "ewb_pair_kernels_reduce: workspace too small");
+  for (int f = 0; f < F; ++f)
+    if (int rc = check_omega(omega_host[2 * f], omega_host[2 * f + 1], "ewb_pair_kernels_reduce"))
+      return rc;
+  void* tab = nullptr;
+  if (int rc = pair_prep(omega_host, F, lam, mu, rho, S(stream), &tab)) return rc;
+  auto* fcs = (const ewb::FreqConst*)tab;
+  const double* b7 = (const double*)((unsigned char*)tab + sizeof(ewb::FreqConst) * F);
+  EWB_CUDA(ewb::launch_pair_reduce(x, P, tri, M, (const ewb::cplx*)xv, fcs, F, b7, b7 + 21,
+                                   (ewb::cplx*)yu, (ewb::cplx*)yt, (ewb::cplx*)ws,
+                                   pair_chunks(P, M), S(stream)),
+           "ewb_pair_kernels_reduce");
+  EWB_CUDA(cudaFreeAsync(tab, S(stream)), "ewb_pair_kernels_reduce");
+  return EWB_OK;
+}
+
+int ewb_fp64_peak_probe(int64_t iters, int32_t blocks_per_sm, double* tflops, double* ms,
+                        void* stream) {
+  if (!tflops || !ms || iters < 1 || blocks_per_sm < 1)
+    return fail(EWB_ERR_INVALID, "ewb_fp64_peak_probe: bad argument");
+  EWB_CUDA(ewb::fp64_peak_probe(iters, blocks_per_sm, tflops, ms, S(stream)), "ewb_fp64_peak_probe");
+  return EWB_OK;
+}
+
+}  // extern "C"

@@ -25,13 +25,7 @@ namespace cg = cooperative_groups;
 
 namespace ewb {
 
-#ifndef EWB_SOLVE_THREADS
-#define EWB_SOLVE_THREADS 512
-#endif
-constexpr int kSolveThreads = EWB_SOLVE_THREADS;
-// register cap 65536 / (kSolveThreads * kSolveMinBlocks) = 128: with 256 threads a
-// solver CTA leaves half of the register file to co-resident assembly CTAs
-constexpr int kSolveMinBlocks = 512 / kSolveThreads;
+constexpr int kSolveThreads = 512;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kMaxRed = 16;  // doubles per grid reduction
 
@@ -167,18 +161,8 @@ struct Ring {
   cplx* buf;            // dynamic shared memory, kNS stages
   uint64_t* bar;        // kNS mbarriers (static shared)
   unsigned pos;         // stages consumed so far by this CTA (uniform)
-  unsigned evict_first; // L2 policy for A: evict_first (A larger than L2) or evict_last
+  uint64_t policy;      // L2 cache policy for A
 };
-
-// Optional L2 residency of part of A: the first kPinRows rows of every CTA's
-// slice are loaded evict_last, the rest evict_first, so ~kPinRows x 148 rows
-// stay in L2 across passes.  Measured (n = 15360): 2 rows lift a standalone
-// GEMV from 6.76 to 6.88 TB/s but slow the cfg2 sweep from 4.02 to 4.09 s
-// (the pinned rows crowd the Krylov basis out of L2), so it is off.
-#ifndef EWB_PIN_ROWS
-#define EWB_PIN_ROWS 0
-#endif
-constexpr int kPinRows = EWB_PIN_ROWS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -190,35 +174,28 @@ __device__ __forceinline__ void ring_init(Ring& R, bool evict_first) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&R.bar[s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  R.evict_first = evict_first ? 1u : 0u;
+  if (evict_first)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(R.policy));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(R.policy));
   R.pos = 0;
   __syncthreads();
 }
 
 __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cplx* A, long long n,
-                                           long long row0, int nrows, long long c0, int tc,
-                                           int npin = 0) {
+                                           long long row0, int nrows, long long c0, int tc) {
   const int b = pos % kNS;
   const uint32_t bar = smem_u32(&R.bar[b]);
   const uint32_t bytes = (uint32_t)(nrows * tc * 16);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
-  // policies are made here (issuing thread only) instead of living in
-  // registers of every thread across the whole solve
-  uint64_t stream_pol, pin_pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pin_pol));
-  if (R.evict_first)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream_pol));
-  else
-    stream_pol = pin_pol;
-  if (kPinRows == 0) npin = 0;
   for (int r = 0; r < nrows; ++r) {
     const uint32_t dst = smem_u32(R.buf + (size_t)b * kStageElems + r * kTC);
     const cplx* src = A + (row0 + r) * n + c0;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-        "l"(src), "r"(tc * 16), "r"(bar), "l"(r < npin ? pin_pol : stream_pol)
+        "l"(src), "r"(tc * 16), "r"(bar), "l"(R.policy)
         : "memory");
   }
 }
@@ -385,11 +362,11 @@ struct GivensShared {
 
 // Classic sequential MGS (one grid barrier per projection) — kept as the
 // GmresArgs::ortho == 1 variant for A/B parity checks.
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_mgs(GmresArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_mgs(GmresArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
   __shared__ GivensShared gs;
   __shared__ cplx s_y[kMaxRestart];
@@ -639,7 +616,7 @@ __device__ __forceinline__ void precond_regs(const cplx* pinv, long long e, cons
   }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres(GmresArgs a) {
   int n_probe = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -649,7 +626,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresA
   __shared__ cplx s_dots[kMaxDots];
   __shared__ cplx s_h[kMaxRestart + 1];
   __shared__ double s_est;
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
   const long long n = a.n;
   const long long tid = gtid(), nth = gthreads();
@@ -912,30 +889,32 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
                             long long r0, long long r1, Epi&& epi) {
   __shared__ cplx s_red[kSolveWarps][kRpt][K];
   __shared__ cplx s_sum[kRR][K];
-  __shared__ int s_rel[kNS];  // warps done with each ring slot
-  const int rows = (int)(r1 - r0);
+  const long long rows = r1 - r0;
   if (rows <= 0) return;
-  const int nblk = (rows + kRR - 1) / kRR;
+  const int nblk = (int)((rows + kRR - 1) / kRR);
   const int ntile = (int)((n + kTC - 1) / kTC);
   const int S = nblk * ntile;
   const int last_tc = (int)(n - (long long)(ntile - 1) * kTC);
-  // block q covers rows r0 + [q rows / nblk, (q+1) rows / nblk); stage
-  // u = q ntile + t.  (32-bit arithmetic: rows per CTA << 2^31 / nblk.)
-  // Stage u goes to ring slot (R.pos + u) % kNS; the LAST warp to finish
-  // reading a slot refills it with stage u + kNS, so no warp ever waits for
-  // another except on data arrival (no CTA barrier per stage).
-  auto issue = [&](int u) {
-    const int q = u / ntile, t = u - q * ntile;
-    const int rel0 = q * rows / nblk, nr = (q + 1) * rows / nblk - rel0;
-    const int tc = t == ntile - 1 ? last_tc : kTC;
-    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc,
-               max(0, min(nr, kPinRows - rel0)));
+  // block q covers rows [r0 + q rows / nblk, r0 + (q+1) rows / nblk); stage
+  // s = q ntile + t.  Coordinates advance incrementally (no 64-bit division
+  // per stage).
+  auto block_rows = [&](int q, long long& row0, int& nrows) {
+    row0 = r0 + (long long)q * rows / nblk;
+    nrows = (int)(r0 + (long long)(q + 1) * rows / nblk - row0);
   };
-  if (threadIdx.x < kNS) s_rel[threadIdx.x] = 0;
-  __syncthreads();
+  // producer state (thread 0): next stage to issue
+  int pq = 0, pt = 0;
+  long long prow0 = 0;
+  int pnrows = 0;
+  auto issue_next = [&](unsigned pos) {
+    if (pt == 0) block_rows(pq, prow0, pnrows);
+    const int tc = pt == ntile - 1 ? last_tc : kTC;
+    ring_issue(R, pos, A, n, prow0, pnrows, (long long)pt * kTC, tc);
+    if (++pt == ntile) { pt = 0; ++pq; }
+  };
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (int u = 0; u < S && u < kNS; ++u) issue(u);
+    for (int s = 0; s < S && s < kNS; ++s) issue_next(R.pos + (unsigned)s);
   }
   const int col = threadIdx.x % kTC, slice = threadIdx.x / kTC;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -948,8 +927,9 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
 #pragma unroll
   for (int k = 0; k < K; ++k) xn[k] = col < n ? ldg(x + k * n + col) : cplx{0.0, 0.0};
   int q = 0, t = 0;
-  long long row0 = r0;
-  int nrows = rows / nblk;
+  long long row0;
+  int nrows;
+  block_rows(0, row0, nrows);
   for (int s = 0; s < S; ++s) {
     const long long c0 = (long long)t * kTC;
     const int tc = t == ntile - 1 ? last_tc : kTC;
@@ -976,14 +956,10 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
         }
       }
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0 &&
-        atomicAdd(&s_rel[pos % kNS], 1) == kSolveWarps - 1) {  // last reader of the slot
-      s_rel[pos % kNS] = 0;
-      if (s + kNS < S) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(s + kNS);
-      }
+    __syncthreads();  // every consumer is done with this stage's buffer
+    if (threadIdx.x == 0 && s + kNS < S) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_next(pos + kNS);
     }
     if (t == ntile - 1) {  // last tile of the block: reduce, then the epilogue
 #pragma unroll
@@ -1007,26 +983,12 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
       epi(row0, nrows, s_sum);
       __syncthreads();
       t = 0;
-      if (++q < nblk) {
-        const int rel0 = q * rows / nblk;
-        row0 = r0 + rel0;
-        nrows = (q + 1) * rows / nblk - rel0;
-      }
+      if (++q < nblk) block_rows(q, row0, nrows);
     } else {
       ++t;
     }
   }
   R.pos += (unsigned)S;
-}
-
-// sum over aligned groups of G lanes (result in every lane of the group)
-template <int G>
-__device__ __forceinline__ void group_sum(cplx& v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) {
-    v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
-    v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
-  }
 }
 
 // Fixed-order reduction of `cnt` CTA partials (layout part[b * stride + t]):
@@ -1091,8 +1053,17 @@ __device__ void reduce_parts(const cplx* part, int stride, int cnt, cplx* out) {
 constexpr int kNormSlot = kMaxDots - 1;
 constexpr int kGrp = kRR <= 16 ? 16 : 32;  // lanes per epilogue dot
 
+// sum over aligned groups of G lanes (result in every lane of the group)
+template <int G>
+__device__ __forceinline__ void group_sum(cplx& v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    v.re += __shfl_xor_sync(0xffffffffu, v.re, o);
+    v.im += __shfl_xor_sync(0xffffffffu, v.im, o);
+  }
+}
 
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(GmresArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gmres_f(GmresArgs a) {
   int n_probe = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -1106,7 +1077,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(Gmre
   __shared__ cplx s_wblk[kRR];
   __shared__ double s_nrm[kSolveWarps];
   __shared__ double s_est;
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
   const long long n = a.n;
   const long long tid = gtid(), nth = gthreads();
@@ -1187,20 +1158,6 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(Gmre
   }
   int n_mv = 0;
   double rnorm;
-#ifndef EWB_NO_AX0
-  if (v2[1] > 0.0 && a.ax0) {  // r = b - A x0 with A x0 supplied (SEM's Y s)
-    double q = 0.0;
-    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-      const cplx r = a.b[k] - a.ax0[k];
-      a.r[k] = r;
-      q += abs2(r);
-    }
-    cta_norm_partial(q, dpar);
-    grid.sync();
-    rnorm = sqrt(grid_norm(dpar));
-    dpar ^= 1;
-  } else
-#endif
   if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
     rnorm = residual(dpar);
     dpar ^= 1;
@@ -1610,13 +1567,9 @@ __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
         s[i] = cdiv(t, Rm[i][i]);
       }
       for (long long k = tid; k < n; k += nth) {
-        cplx x = {0.0, 0.0}, y = {0.0, 0.0};
-        for (int i = 0; i < kk; ++i) {
-          cfma(x, a.X[(size_t)keep[i] * n + k], s[i]);
-          if (a.ax0) cfma(y, a.Y[(size_t)keep[i] * n + k], s[i]);
-        }
+        cplx x = {0.0, 0.0};
+        for (int i = 0; i < kk; ++i) cfma(x, a.X[(size_t)keep[i] * n + k], s[i]);
         a.x0[k] = x;
-        if (a.ax0) a.ax0[k] = y;
       }
       if (tid == 0) { a.out->kept = kk; a.out->fallback = 0; }
       return;
@@ -1631,14 +1584,11 @@ __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
     __syncthreads();
     if (ng == 0) break;
   }
-  for (long long k = tid; k < n; k += nth) {
-    a.x0[k] = a.X[k];
-    if (a.ax0) a.ax0[k] = a.Y[k];
-  }
+  for (long long k = tid; k < n; k += nth) a.x0[k] = a.X[k];
   if (tid == 0) { a.out->kept = 0; a.out->fallback = 1; }
 }
 
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_sem(SemArgs a) {
+__global__ void __launch_bounds__(kSolveThreads, 1) k_sem(SemArgs a) {
   cg::grid_group grid = cg::this_grid();
   GridRed R{a.partial, 0};
   switch (a.K) {
@@ -1651,11 +1601,11 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_sem(SemArgs 
 
 // Batched GEMV y_b = A_b x_b through the TMA ring (regular launch; system
 // blockIdx.y, row groups dealt over blockIdx.x).
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gemv_tma(const cplx* A, const cplx* x,
+__global__ void __launch_bounds__(kSolveThreads, 1) k_gemv_tma(const cplx* A, const cplx* x,
                                                                cplx* y, long long n) {
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, true);
   const size_t sys = blockIdx.y;
   cplx* ys = y + sys * n;
@@ -1711,16 +1661,7 @@ static int coop_grid(const void* fn) {
   return sms * per;
 }
 
-static int g_solver_limit = 0;  // 0: every co-resident CTA
-
-void set_solver_ctas(int ctas) { g_solver_limit = ctas > 0 ? ctas : 0; }
-
 int solver_grid_blocks() {
-  const int m = solver_grid_max();
-  return g_solver_limit > 0 && g_solver_limit < m ? g_solver_limit : m;
-}
-
-int solver_grid_max() {
   if (g_coop_blocks == 0) {
     int a = coop_grid((const void*)k_gmres), b = coop_grid((const void*)k_sem);
     int c = coop_grid((const void*)k_gmres_mgs), d = coop_grid((const void*)k_gmres_f);
@@ -1744,11 +1685,11 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
 // Y = A X for K <= 4 columns in one TMA-streamed pass (SEM's products,
 // linsolve.py:228).  Regular launch, 1 CTA/SM, full register budget.
 template <int K>
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_multi_gemv(const cplx* A, const cplx* X,
+__global__ void __launch_bounds__(kSolveThreads, 1) k_multi_gemv(const cplx* A, const cplx* X,
                                                                  cplx* Y, long long n) {
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0ull};
   ring_init(ring, 16.0 * (double)n * (double)n > 96e6);
   long long r0, r1;
   cta_rows(n, r0, r1);
@@ -1769,15 +1710,18 @@ static cudaError_t launch_multi_gemv(const cplx* A, const cplx* X, cplx* Y, long
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBytes);
     attr = true;
   }
-  // the solver's CTA budget (the rest of the GPU may be assembling)
-  unsigned blocks = (unsigned)solver_grid_blocks();
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned blocks = (unsigned)sms;
   EWB_NOTE k_multi_gemv<K><<<blocks, kSolveThreads, kRingBytes, s>>>(A, X, Y, n);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
-  // Y = A X, at most two columns per pass (more accumulators than that spill
-  // under the 128-register cap of a 512-thread CTA): K = 3 as 2 + 1, 4 as 2 + 2.
+  // Measured: the K-vector matvec spills beyond K = 2 under the 128-register
+  // cap of a 512-thread CTA (K=4 in one pass: 2.04 ms at n=15360), so the
+  // columns go two at a time.
   cudaError_t e = cudaSuccess;
   for (int c = 0; c < args.K && e == cudaSuccess; c += 2) {
     const long long off = (long long)c * args.n;

@@ -32,7 +32,7 @@ import numpy as np
 from . import _lib
 from .assembly import DIRICHLET, NEUMANN, Assembler
 from .config import SweepConfig
-from .linsolve import SolveStats, block_diag_precond, gmres_device, sem_device
+from .linsolve import SolveStats, _WS, _fill_stats, block_diag_precond, gmres_device, sem_device
 from .transform import (check_residue, eta_from_kappa, forward_mft, frequency_grid,
                         windowed_inverse_device)
 
@@ -105,11 +105,6 @@ def gather_frequency_results(local: dict, n_freq: int, width: int, dist=None):
     if not np.all(owned == 1):
         raise SweepError("frequency ownership is not a partition of the sweep")
     return vals, meta
-
-
-def n_hist_passes(K: int) -> int:
-    """Passes over A of one SEM product Y = A X (two columns per pass)."""
-    return (K + 1) // 2
 
 
 class DeviceSweep:
@@ -213,35 +208,20 @@ class DeviceSweep:
         return stats
 
     def run(self, timing: bool = False):
-        """Sweep the owned frequencies; returns {k: SolveStats}.
-
-        Every launch of the sweep is queued without a host read-back: the
-        fault flags, GMRES results and residual histories of each frequency
-        land in per-frequency device slots that are read once at the end
-        (the first non-finite frequency then raises, as in driver.py:141-145).
-        SEM also returns A x0, so GMRES starts without a pass over A."""
+        """Sweep the owned frequencies; returns {k: SolveStats}."""
         import torch
-
-        from .linsolve import gmres_hist_cap
 
         if getattr(self, "matrix_free", False):
             return self.run_matrix_free()
         cfg = self.cfg
         asm = self.asm
-        lib = asm._lib
         stats = {}
         ev = []
         n_hist = 0
         K = cfg.sem_depth
         self.hist.zero_()
         self.phase = {"assembly_ms": 0.0, "solve_ms": 0.0, "matvecs": 0, "solves": 0}
-        nf = len(self.frequencies)
-        cap = gmres_hist_cap(cfg.maxiter, cfg.restart)
-        res_all = torch.zeros((nf, 64), dtype=torch.uint8, device="cuda")
-        hist_all = torch.zeros((nf, cap), dtype=torch.float64, device="cuda")
-        flags_all = torch.zeros((nf, 4), dtype=torch.int32, device="cuda")
-        ax0 = torch.empty(self.n, dtype=torch.complex128, device="cuda")
-        for idx, k in enumerate(self.frequencies):
+        for k in self.frequencies:
             omega = complex(self.omegas[k])
             try:
                 if timing:
@@ -253,57 +233,49 @@ class DeviceSweep:
                     sysm.pinv = block_diag_precond(sysm.A).pinv
                 else:
                     self.system = sysm
-                _lib.check(lib.ewb_ctx_flags_async(asm.ctx, _lib.ptr(flags_all[idx]),
-                                                   _lib.stream_handle()), "ewb_ctx_flags_async")
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
                 use_sem = cfg.sem_enabled and n_hist > 0
                 if use_sem:
-                    sem_device(sysm.A, sysm.b, self.hist[:n_hist], 1e-10, self.x, ax0_out=ax0)
+                    sem_device(sysm.A, sysm.b, self.hist[:n_hist], 1e-10, self.x)
+                st = SolveStats()
                 gmres_device(sysm.A, sysm.b, self.x, use_sem, cfg.tol, cfg.restart, cfg.maxiter,
-                             sysm.pinv, sync=False, ax0=ax0 if use_sem else None,
-                             res=res_all[idx], hist=hist_all[idx])
+                             sysm.pinv, stats=st, sync=False)
                 e1.record()
+                nf, sg = ctypes.c_int32(), ctypes.c_int32()
+                _lib.check(asm._lib.ewb_ctx_flags(asm.ctx, ctypes.byref(nf), ctypes.byref(sg),
+                                                  _lib.stream_handle()))
+                if nf.value:
+                    raise FloatingPointError(f"non-finite entries assembled at omega = {omega}")
+                if sg.value:
+                    log.warning("%d singular 3x3 diagonal blocks; identity fallback", sg.value)
+                _fill_stats(st, _WS.result(), _WS.hist_buf(1))
+                self.d2h_bytes += 8 + 32 + 8 * len(st.residual_history)
             except SweepError:
                 raise
             except Exception as exc:
                 raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
-            ev.append((idx, k, omega, e_a if timing else None, e0, e1, n_hist if use_sem else 0))
+            st.k = k
+            st.omega = omega
+            stats[k] = st
+            ev.append((k, e_a if timing else None, e0, e1, use_sem))
             self.sol[k] = self.x
             if cfg.sem_enabled:
                 self.hist[1:] = self.hist[:-1].clone()
                 self.hist[0] = self.x
                 n_hist = min(n_hist + 1, K)
-        torch.cuda.synchronize()
-        flags = flags_all.cpu().numpy()
-        res_host = res_all.cpu().numpy()
-        for idx, k, omega, ea, e0, e1, sem_cols in ev:
-            if flags[idx, 0]:
-                raise SweepError(f"frequency index {k} (omega={omega:.6g}): non-finite entries "
-                                 f"assembled at omega = {omega}")
-            if flags[idx, 1]:
-                log.warning("%d singular 3x3 diagonal blocks; identity fallback", flags[idx, 1])
-            out = _lib.GmresResult.from_buffer_copy(res_host[idx, :32].tobytes())
-            st = SolveStats(k=k, omega=omega, iterations=out.iterations,
-                            init_residual=out.init_residual, final_residual=out.final_residual,
-                            converged=bool(out.converged), matvecs=out.matvecs)
-            nh = min(out.n_hist, cap)
-            st.residual_history = hist_all[idx, :nh].cpu().tolist() if nh else []
-            self.d2h_bytes += 16 + 32 + 8 * nh
             if not st.converged:
-                log.warning("GMRES stalled at residual %.3e after %d iterations (k=%d)",
-                            st.final_residual, st.iterations, k)
-            st.seconds = e0.elapsed_time(e1) * 1e-3
-            stats[k] = st
+                log.warning("GMRES stalled at residual %.3e after %d iterations",
+                            st.final_residual, st.iterations)
+        torch.cuda.synchronize()
+        for k, ea, e0, e1, use_sem in ev:
+            stats[k].seconds = e0.elapsed_time(e1) * 1e-3
             if timing:
                 self.phase["assembly_ms"] += ea.elapsed_time(e0)
                 self.phase["solve_ms"] += e0.elapsed_time(e1)
-                if idx + 1 < len(ev):
-                    self.phase["gap_ms"] = self.phase.get("gap_ms", 0.0) + \
-                        e1.elapsed_time(ev[idx + 1][3])
-            # passes over A: the solver's own count + SEM's Y = A X pass(es)
-            self.phase["matvecs"] += st.matvecs + (n_hist_passes(sem_cols) if sem_cols else 0)
+            # passes over A: the solver's own count + SEM's single Y = A X pass
+            self.phase["matvecs"] += stats[k].matvecs + (1 if use_sem else 0)
             self.phase["solves"] += 1
         return stats
 

@@ -1,0 +1,190 @@
+"""GPU parity: dense assembly, static pass, fused system vs golden + oracle.
+
+Tolerance (north star): matrix entries within 1e-10 of max|entry|
+(max-abs normalisation as test_assembly.py:70 uses).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_max
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _unit():
+    from paper_1212_3032_b200 import Material
+
+    return Material.from_young_poisson(1.0, 0.25, 1.0)
+
+
+def _steel():
+    from paper_1212_3032_b200 import Material
+
+    return Material.from_young_poisson(2.11e11, 0.0, 7850.0)
+
+
+@pytest.fixture(scope="module")
+def cube(cuda):
+    from paper_1212_3032_b200 import Assembler, generate_box_mesh
+
+    return Assembler(generate_box_mesh((1, 1, 1), (2, 2, 2)), _unit())
+
+
+def test_cube_tu_all_frequencies_match_golden(cube):
+    g = golden("small")
+    assert np.array_equal(cube.mesh.vertices, g["cube_vertices"])
+    for i, om in enumerate(g["cube_omegas"]):
+        t, u = cube.assemble_tu(complex(om), host=True)
+        assert rel_max(t, g[f"cube_T{i}"]) <= TOL, (om, rel_max(t, g[f"cube_T{i}"]))
+        assert rel_max(u, g[f"cube_U{i}"]) <= TOL, (om, rel_max(u, g[f"cube_U{i}"]))
+
+
+def test_cube_rowsums_match_golden(cube):
+    g = golden("small")
+    assert rel_max(cube.static_offdiag_rowsums(), g["cube_rowsums"]) <= 1e-12
+
+
+def test_rod32_steel_matches_golden(cuda):
+    from paper_1212_3032_b200 import Assembler, generate_box_mesh
+
+    g = golden("small")
+    t, u = Assembler(generate_box_mesh((1, 1, 2), (2, 2, 1)), _steel()).assemble_tu(
+        2000.0 - 300.0j, host=True)
+    assert rel_max(t, g["rod32_T"]) <= TOL
+    assert rel_max(u, g["rod32_U"]) <= TOL
+
+
+def test_flipped_icosphere_matches_golden(cuda):
+    from paper_1212_3032_b200 import Assembler, generate_icosphere
+
+    g = golden("small")
+    t, u = Assembler(generate_icosphere((0, 0, 0), 1.0, 1, flip=True), _unit()).assemble_tu(
+        1.5 - 0.3j, host=True)
+    assert rel_max(t, g["ico1_T"]) <= TOL
+    assert rel_max(u, g["ico1_U"]) <= TOL
+
+
+@pytest.fixture(scope="module")
+def cfg1_asm(cuda):
+    from paper_1212_3032_b200 import Assembler, generate_box_mesh
+
+    return Assembler(generate_box_mesh((1, 1, 1), (8, 8, 8)), _unit())
+
+
+def test_cfg1_pair_census_matches_reference_tiers(cfg1_asm):
+    """GPU exact-rounding tiers == numpy tiers on the box mesh with 388 ties."""
+    g = golden("tiers")
+    n = int(g["cfg1_n"])
+    bits = np.unpackbits(g["cfg1_tier"])[: 2 * n * n].reshape(2, n, n)
+    tier = bits[0] + 2 * bits[1]
+    off = ~np.eye(n, dtype=bool)
+    pc = cfg1_asm.pair_counts()
+    assert pc["far"] == int(((tier == 0) & off).sum())
+    assert pc["mid"] == int(((tier == 1) & off).sum())
+    assert pc["near"] == int(((tier == 2) & off).sum())
+    near = g["cfg1_near"]
+    for lvl in (1, 2, 3, 4):
+        assert pc["near_levels"][lvl] == int((near[2] == lvl).sum())
+    assert cfg1_asm.point_evals() == 4825892
+
+
+def test_cfg1_rows_diagonals_and_matvecs_match_golden(cfg1_asm):
+    from paper_1212_3032_b200.transform import eta_from_kappa, frequency_grid
+
+    g = golden("cfg1_rows")
+    c_s = _unit().c_s
+    period = 8.0 / c_s
+    om = frequency_grid(period, 128, eta_from_kappa(6.0 / np.log(10.0), period))
+    elems = g["elements"]
+    rows = (3 * elems[:, None] + np.arange(3)).ravel()
+    assert rel_max(cfg1_asm.static_offdiag_rowsums(), g["rowsums"]) <= 1e-12
+    v = g["v"]
+    for k in (1, 64):
+        t, u = cfg1_asm.assemble_tu(om[k], host=True)
+        tmax, umax = float(g[f"Tmax_k{k}"]), float(g[f"Umax_k{k}"])
+        assert np.abs(t[rows] - g[f"T_rows_k{k}"]).max() <= TOL * tmax
+        assert np.abs(u[rows] - g[f"U_rows_k{k}"]).max() <= TOL * umax
+        tb, ub = t.reshape(768, 3, 768, 3), u.reshape(768, 3, 768, 3)
+        ids = np.arange(768)
+        assert np.abs(tb[ids, :, ids, :] - g[f"T_diag_k{k}"]).max() <= TOL * tmax
+        assert np.abs(ub[ids, :, ids, :] - g[f"U_diag_k{k}"]).max() <= TOL * umax
+        assert rel_max(t @ v, g[f"Tv_k{k}"]) <= TOL
+        assert rel_max(u @ v, g[f"Uv_k{k}"]) <= TOL
+
+
+def test_assembly_is_bit_deterministic(cube):
+    t1, u1 = cube.assemble_tu(0.7 - 0.2j, host=True)
+    t2, u2 = cube.assemble_tu(0.7 - 0.2j, host=True)
+    assert np.array_equal(t1, t2) and np.array_equal(u1, u2)
+
+
+def test_conjugate_reflection(cube):
+    om = 4.05 - 0.594j
+    t, u = cube.assemble_tu(om, host=True)
+    tr, ur = cube.assemble_tu(-np.conj(om), host=True)
+    assert np.abs(tr - np.conj(t)).max() <= 1e-12 * np.abs(t).max()
+    assert np.abs(ur - np.conj(u)).max() <= 1e-12 * np.abs(u).max()
+
+
+def test_rigid_body_rowsum_near_static(cube):
+    t, _ = cube.assemble_tu(-1e-6j, host=True)
+    ones = np.tile(np.eye(3), (cube.mesh.n_elements, 1))
+    assert np.abs(t @ ones).max() <= 1e-7 * np.abs(t).max()
+    ts, _ = cube.assemble_static_tu(host=True)
+    assert np.abs(ts @ ones).max() <= 1e-12 * np.abs(ts).max()
+
+
+def test_positive_imaginary_frequency_rejected(cube):
+    with pytest.raises(ValueError, match="positive imaginary"):
+        cube.assemble_tu(1.0 + 0.5j)
+
+
+def _rod_bcs(mesh):
+    from paper_1212_3032_b200 import DIRICHLET, NEUMANN, BoundaryConditionSet
+
+    bcs = BoundaryConditionSet.traction_free(mesh.n_elements)
+    bcs.set_region(mesh, 0, (0, 1, 2), DIRICHLET, 0)
+    bcs.set_region(mesh, 1, (0,), NEUMANN, 1)
+    return bcs
+
+
+def test_fused_system_equals_oracle_apply_bcs(cube):
+    from oracle import ewbem_oracle as O
+
+    g = golden("small")
+    rng = np.random.default_rng(3)
+    bcs = _rod_bcs(cube.mesh)
+    p = rng.normal(size=cube.n) + 1j * rng.normal(size=cube.n)
+    om = complex(g["cube_omegas"][3])
+    a_ref, b_ref = O.apply_bcs(g["cube_T3"], g["cube_U3"], bcs.flat_kind(), p)
+    sysm = cube.assemble_system(om, bcs, p)
+    a = sysm.A.cpu().numpy()
+    assert rel_max(a, a_ref) <= TOL
+    assert rel_max(sysm.b.cpu().numpy(), b_ref) <= TOL
+    _, inv = O.block_precond(a_ref)
+    assert rel_max(sysm.pinv.cpu().numpy(), inv) <= 1e-9
+
+
+def test_apply_bcs_device_matches_oracle(cube):
+    from oracle import ewbem_oracle as O
+    from paper_1212_3032_b200 import apply_bcs, scatter_solution
+
+    g = golden("small")
+    rng = np.random.default_rng(8)
+    bcs = _rod_bcs(cube.mesh)
+    p = rng.normal(size=cube.n) + 1j * rng.normal(size=cube.n)
+    a_ref, b_ref = O.apply_bcs(g["cube_T2"], g["cube_U2"], bcs.flat_kind(), p)
+    sysm = apply_bcs(g["cube_T2"], g["cube_U2"], bcs, p)
+    assert np.array_equal(sysm.A.cpu().numpy(), a_ref)
+    assert rel_max(sysm.b.cpu().numpy(), b_ref) <= 1e-13
+    with pytest.raises(ValueError, match="unresolved"):
+        apply_bcs(g["cube_T2"], g["cube_U2"], bcs, np.full(cube.n, np.nan, complex))
+    with pytest.raises(ValueError, match="length"):
+        apply_bcs(g["cube_T2"], g["cube_U2"], bcs, np.zeros(3, complex))
+    a = np.linalg.solve(a_ref, b_ref)
+    u, t = scatter_solution(sysm, a, p)
+    kinds = bcs.flat_kind()
+    assert np.array_equal(u.cpu().numpy()[kinds == 1], p[kinds == 1])
+    assert np.array_equal(t.cpu().numpy()[kinds == 0], p[kinds == 0])

@@ -1,0 +1,263 @@
+"""GPU parity: GMRES, block preconditioner, SEM, time reconstruction, sweeps."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_max
+
+pytestmark = pytest.mark.gpu
+
+
+def test_gmres_random_system_matches_golden(cuda):
+    from paper_1212_3032_b200 import gmres
+
+    g = golden("linsolve")
+    x, st = gmres(g["rand_A"], g["rand_b"], tol=1e-12, restart=20)
+    # the golden run stalls at maxiter=1000 (restart 20 on a hard system);
+    # our run must walk the same path: same count, same monotone cycles
+    assert st.iterations == int(g["rand_its"])
+    h = np.array(st.residual_history)
+    ref = g["rand_hist"]
+    assert len(h) == len(ref)
+    assert np.abs(np.log10(h[:200]) - np.log10(ref[:200])).max() < 1e-3
+
+
+def test_gmres_rod_bem_system_with_block_precond(cuda):
+    from paper_1212_3032_b200 import block_diag_precond, gmres
+
+    g = golden("linsolve")
+    a, b = g["rod_A"], g["rod_b"]
+    x, st = gmres(a, b, tol=1e-6, precond=block_diag_precond(a))
+    assert st.converged
+    assert abs(st.iterations - int(g["rod_its"])) <= 1
+    x_direct = np.linalg.solve(a, b)
+    assert np.abs(x.cpu().numpy() - x_direct).max() <= 1e-4 * np.abs(x_direct).max()
+
+
+def test_gmres_nonconvergence_flagged(cuda):
+    from paper_1212_3032_b200 import gmres
+
+    g = golden("linsolve")
+    x, st = gmres(g["nc_A"], g["nc_b"], tol=1e-14, restart=5, maxiter=10)
+    assert not st.converged
+    assert st.iterations == 10
+    assert st.final_residual > 1e-14
+    assert np.isfinite(x.cpu().numpy()).all()
+    assert abs(st.final_residual - float(g["nc_final"])) <= 1e-10
+
+
+def test_gmres_edge_cases(cuda):
+    from paper_1212_3032_b200 import gmres
+
+    rng = np.random.default_rng(0)
+    b = rng.normal(size=30) + 1j * rng.normal(size=30)
+    x, st = gmres(np.eye(30, dtype=complex), b, tol=1e-10)
+    assert st.iterations == 1 and st.converged
+    np.testing.assert_allclose(x.cpu().numpy(), b, rtol=1e-12)
+    x, st = gmres(np.eye(5, dtype=complex), np.zeros(5, complex))
+    assert st.iterations == 0 and not x.cpu().numpy().any()
+    with pytest.raises(ValueError):
+        gmres(np.eye(3, dtype=complex), np.ones(3, complex), tol=0.0)
+    a = rng.normal(size=(64, 64)) + 1j * rng.normal(size=(64, 64)) + 10 * np.eye(64)
+    bb = rng.normal(size=64) + 1j * rng.normal(size=64)
+    xe = np.linalg.solve(a, bb)
+    x, st = gmres(a, bb, x0=xe, tol=1e-6)
+    assert st.iterations == 0 and st.init_residual <= 1e-12
+
+
+def test_block_diag_precond_identity_and_singular(cuda):
+    from paper_1212_3032_b200 import block_diag_precond
+
+    rng = np.random.default_rng(5)
+    n = 60
+    a = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n)) + 4 * np.eye(n)
+    pc = block_diag_precond(a)
+    import torch
+
+    pa = torch.stack([pc(torch.from_numpy(a[:, i]).cuda()) for i in range(n)], dim=1).cpu().numpy()
+    for i in range(n // 3):
+        assert np.abs(pa[3 * i:3 * i + 3, 3 * i:3 * i + 3] - np.eye(3)).max() <= 1e-13
+    s = np.eye(6, dtype=complex)
+    s[3:6, 3:6] = 0.0
+    pc = block_diag_precond(s)
+    v = np.arange(6.0).astype(complex)
+    np.testing.assert_allclose(pc(torch.from_numpy(v).cuda()).cpu().numpy(), v)
+    with pytest.raises(ValueError):
+        block_diag_precond(np.eye(4, dtype=complex))
+
+
+def test_sem_matches_golden(cuda):
+    from paper_1212_3032_b200 import SolutionHistory, sem_initial_guess
+
+    g = golden("linsolve")
+    hist = SolutionHistory(4)
+    X = g["sem_X"]
+    for c in X.T[::-1]:
+        hist.push(c)
+    x0 = sem_initial_guess(hist, g["sem_A"], g["sem_b"]).cpu().numpy()
+    assert rel_max(x0, g["sem_x0"]) <= 1e-10
+    hist2 = SolutionHistory(3)
+    for c in g["sem2_X"].T[::-1]:
+        hist2.push(c)
+    x0 = sem_initial_guess(hist2, g["sem_A"], g["sem2_b"]).cpu().numpy()
+    a = g["sem_A"]
+    assert np.linalg.norm(a @ x0 - g["sem2_b"]) <= 1e-9 * np.linalg.norm(g["sem2_b"])
+
+
+def test_window_idft_matches_golden(cuda):
+    import torch
+
+    from paper_1212_3032_b200.transform import Spectrum, inverse_mft, windowed_inverse_device
+
+    g = golden("transform")
+    period, eta = float(g["period"]), float(g["eta"])
+    half = g["half"]
+    for w in ("rectangular", "hanning", "blackman"):
+        out = inverse_mft(Spectrum(g["full"], period, eta), w, eta)
+        assert rel_max(out, g[f"inv_{w}"]) <= 1e-12
+    # many columns at once
+    cols = np.stack([half, 2 * half, half * (1 - 1j)], axis=1)
+    out, res = windowed_inverse_device(torch.from_numpy(cols).cuda(), "hanning", eta, period)
+    out = out.cpu().numpy()
+    assert rel_max(out[:, 0], g["inv_hanning"]) <= 1e-12
+    assert rel_max(out[:, 1], 2 * g["inv_hanning"]) <= 1e-12
+    assert float(res.max()) < 1e-12
+
+
+def _tiny_cfg(**kw):
+    from paper_1212_3032_b200 import (DIRICHLET, NEUMANN, BoundaryConditionSet, Material, Probe,
+                                      SweepConfig, TimeSignal, generate_box_mesh)
+    from paper_1212_3032_b200.workloads import face_center_element
+
+    divisions = kw.pop("divisions", (1, 1, 1))
+    mesh = generate_box_mesh((3.0, 1.0, 1.0), divisions)
+    zm = np.flatnonzero(mesh.region_tag == 4)
+    mid = int(zm[np.argmin(np.linalg.norm(mesh.centroids[zm] - np.array([1.5, 0.5, 0.0]),
+                                          axis=1))])
+    bcs = BoundaryConditionSet.traction_free(mesh.n_elements)
+    bcs.set_region(mesh, 0, (0, 1, 2), DIRICHLET, 0)
+    bcs.set_region(mesh, 1, (0,), NEUMANN, 1)
+    args = dict(n_omega=8, kappa=4.0, window="hanning", sem_enabled=True, sem_depth=4, tol=1e-5)
+    args.update(kw)
+    return SweepConfig(
+        mesh=mesh, material=Material.from_young_poisson(2.11e11, 0.0, 7850.0), bcs=bcs,
+        signals=[TimeSignal.zero(), TimeSignal.heaviside(-1e6)], signal_names=["zero", "load"],
+        probes=[Probe("tip_ux", face_center_element(mesh, 1), 0, "displacement"),
+                Probe("mid_ux", mid, 0, "displacement"),
+                Probe("root_tx", face_center_element(mesh, 0), 0, "traction")],
+        period=0.0155, figures=False, **args)
+
+
+def _check_sweep(res, g, prefix, its_tol=1, hist_tol=1e-6):
+    its = np.array([s.iterations for s in res.stats])
+    ref = g[f"{prefix}_its"]
+    assert np.abs(its - ref).max() <= its_tol, (its, ref)
+    for name in g[f"{prefix}_probes"]:
+        h = res.histories[str(name)]
+        href = g[f"{prefix}_h_{name}"]
+        err = np.linalg.norm(h - href) / np.linalg.norm(href)
+        assert err <= hist_tol, (name, err)
+
+
+@pytest.mark.parametrize("prefix,kw", [("tiny", {}), ("tiny_nosem", {"sem_enabled": False}),
+                                       ("rod622", {"divisions": (6, 2, 2), "n_omega": 32})])
+def test_small_sweeps_match_golden(cuda, prefix, kw):
+    from paper_1212_3032_b200 import run_sweep
+
+    g = golden("sweeps")
+    res = run_sweep(_tiny_cfg(**kw))
+    _check_sweep(res, g, prefix)
+
+
+def test_cfg1_stepwise_iterations_equal_reference(cuda):
+    """BASELINE cfg1, every frequency: our SEM + GMRES fed the reference's own
+    solution history reproduce the reference's iteration count (+-1) and its
+    solution (1e-6).  This isolates per-solve parity from history drift."""
+    import torch
+
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.linsolve import gmres_device, sem_device
+    from paper_1212_3032_b200.transform import eta_from_kappa, forward_mft, frequency_grid
+    from paper_1212_3032_b200.workloads import cfg1
+
+    g = golden("cfg1_solutions")
+    cfg = cfg1()
+    asm = Assembler(cfg.mesh, cfg.material)
+    eta = eta_from_kappa(cfg.kappa, cfg.period)
+    om = frequency_grid(cfg.period, cfg.n_omega, eta)
+    spectra = np.stack([forward_mft(s, cfg.period, cfg.n_omega, eta).values for s in cfg.signals])
+    sig = cfg.bcs.flat_signal()
+    xref = g["x"]
+    x = torch.zeros(cfg.mesh.n_dofs, dtype=torch.complex128, device="cuda")
+    sysm = None
+    diffs = []
+    for k in range(len(om)):
+        sysm = asm.assemble_system(om[k], cfg.bcs, spectra[sig, k], out=sysm)
+        if k:
+            hist = torch.from_numpy(xref[max(0, k - 2):k][::-1].copy()).cuda()
+            sem_device(sysm.A, sysm.b, hist, 1e-10, x)
+        st = gmres_device(sysm.A, sysm.b, x, k > 0, cfg.tol, cfg.restart, cfg.maxiter, sysm.pinv)
+        diffs.append(st.iterations - int(g["its"][k]))
+        assert abs(st.init_residual - g["init"][k]) <= 1e-6 * g["init"][k] + 1e-14
+        assert rel_max(x.cpu().numpy(), xref[k]) <= 1e-6
+    assert max(abs(d) for d in diffs) <= 1, diffs
+
+
+def test_cfg1_sweep_matches_reference_run(cuda):
+    """BASELINE cfg1 end to end (65 SEM-chained solves, tol 1e-8, K=2).
+
+    Histories within 1e-6.  Iteration counts: each solve stops within tol
+    with a rounding-different iterate, and SEM feeds it forward, so the
+    chained counts drift like the reference's own rerun on another CPU
+    (9/65 frequencies off, max 2).  Bar: |d| <= 1 on >= 95 %
+    of frequencies, <= 2 everywhere, total within 1 %."""
+    from paper_1212_3032_b200 import run_sweep
+    from paper_1212_3032_b200.workloads import cfg1
+
+    g = golden("cfg1_sweep")
+    res = run_sweep(cfg1())
+    its = np.array([s.iterations for s in res.stats])
+    d = np.abs(its - g["cfg1_its"])
+    assert d.max() <= 2 and (d <= 1).mean() >= 0.95, d
+    assert abs(its.sum() - g["cfg1_its"].sum()) <= 0.01 * g["cfg1_its"].sum()
+    for name in g["cfg1_probes"]:
+        h, href = res.histories[str(name)], g[f"cfg1_h_{name}"]
+        assert np.linalg.norm(h - href) / np.linalg.norm(href) <= 1e-6
+    assert not res.failed_frequencies
+
+
+def test_cfg2_head_matches_reference(cuda):
+    """BASELINE cfg2 (ico4, 15360 DOF): full-size T v / U v at k=1 and the first
+    three SEM solves (iterations +-1, solutions 1e-6)."""
+    import torch
+
+    from paper_1212_3032_b200 import Assembler, BoundaryConditionSet, SolutionHistory
+    from paper_1212_3032_b200.linsolve import gmres_device, sem_device
+    from paper_1212_3032_b200.workloads import cfg2
+
+    g = golden("cfg2_head")
+    cfg = cfg2()
+    asm = Assembler(cfg.mesh, cfg.material)
+    t, u = asm.assemble_tu(complex(g["omegas"][1]))
+    v = torch.from_numpy(g["v"]).cuda()
+    assert rel_max((t @ v).cpu().numpy(), g["Tv_k1"]) <= 1e-10
+    assert rel_max((u @ v).cpu().numpy(), g["Uv_k1"]) <= 1e-10
+    assert np.abs(t[:3].cpu().numpy() - g["T_row0_k1"]).max() <= 1e-10 * float(g["Tmax_k1"])
+    assert np.abs(u[:3].cpu().numpy() - g["U_row0_k1"]).max() <= 1e-10 * float(g["Umax_k1"])
+    del t, u
+    torch.cuda.empty_cache()
+    bcs = BoundaryConditionSet.traction_free(cfg.mesh.n_elements)
+    load = (-1.0 * cfg.mesh.normals).ravel()
+    hist = torch.zeros((4, cfg.mesh.n_dofs), dtype=torch.complex128, device="cuda")
+    x = torch.zeros(cfg.mesh.n_dofs, dtype=torch.complex128, device="cuda")
+    sysm = None
+    for k in range(3):
+        p = load * g["unit_spec"][k]
+        sysm = asm.assemble_system(complex(g["omegas"][k]), bcs, p, out=sysm)
+        if k:
+            sem_device(sysm.A, sysm.b, hist[:k], 1e-10, x)
+        st = gmres_device(sysm.A, sysm.b, x, k > 0, 1e-8, 60, 1000, sysm.pinv)
+        assert abs(st.iterations - int(g["its"][k])) <= 1, (k, st.iterations, g["its"][k])
+        assert rel_max(x.cpu().numpy(), g["x"][k]) <= 1e-6
+        hist[1:] = hist[:-1].clone()
+        hist[0] = x
