@@ -1092,7 +1092,12 @@ constexpr int kNormSlot = kMaxDots - 1;
 constexpr int kGrp = kRR <= 16 ? 16 : 32;  // lanes per epilogue dot
 
 
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(GmresArgs a) {
+#ifdef EWB_GMRES_MAXNREG
+__global__ void __maxnreg__(EWB_GMRES_MAXNREG)
+#else
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks)
+#endif
+k_gmres_f(GmresArgs a) {
   int n_probe = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];

@@ -33,7 +33,7 @@ from . import _lib
 from .assembly import DIRICHLET, NEUMANN, Assembler
 from .config import SweepConfig
 from .linsolve import SolveStats, block_diag_precond, gmres_device, sem_device
-from .transform import (check_residue, eta_from_kappa, forward_mft, frequency_grid,
+from .transform import (check_residue, eta_from_kappa, forward_mft_batch, frequency_grid,
                         windowed_inverse_device)
 
 log = logging.getLogger(__name__)
@@ -132,8 +132,7 @@ class DeviceSweep:
         self.omegas = frequency_grid(cfg.period, cfg.n_omega, self.eta)
         self.n_freq = len(self.omegas)
         self.h2d_bytes = 0
-        spectra = np.stack([forward_mft(s, cfg.period, cfg.n_omega, self.eta).values[:self.n_freq]
-                            for s in cfg.signals])
+        spectra = forward_mft_batch(cfg.signals, cfg.period, cfg.n_omega, self.eta, self.n_freq)
         self.asm = assembler or Assembler(cfg.mesh, cfg.material)
         if assembler is None:
             m = cfg.mesh
