@@ -261,3 +261,66 @@ def test_cfg2_head_matches_reference(cuda):
         assert rel_max(x.cpu().numpy(), g["x"][k]) <= 1e-6
         hist[1:] = hist[:-1].clone()
         hist[0] = x
+
+
+def test_sem_ax0_and_gmres_start_from_it(cuda):
+    """SEM's A x0 (= Y s, ABI v2) equals A @ x0, and GMRES started from it
+    takes the same iterations to the same solution as with b - A x0."""
+    import torch
+
+    from paper_1212_3032_b200 import block_diag_precond
+    from paper_1212_3032_b200.linsolve import gmres_device, sem_device
+
+    g = golden("linsolve")
+    a = torch.from_numpy(g["rod_A"]).cuda()
+    b = torch.from_numpy(g["rod_b"]).cuda()
+    n = b.shape[0]
+    rng = np.random.default_rng(5)
+    xs = np.linalg.solve(g["rod_A"], g["rod_b"])
+    cols = np.stack([xs + 1e-3 * (rng.normal(size=n) + 1j * rng.normal(size=n))
+                     for _ in range(3)])
+    X = torch.from_numpy(cols).cuda()
+    x0 = torch.empty_like(b)
+    ax0 = torch.empty_like(b)
+    sem_device(a, b, X, 1e-10, x0, ax0_out=ax0)
+    assert rel_max(ax0.cpu().numpy(), (a @ x0).cpu().numpy()) <= 1e-12
+    pinv = block_diag_precond(a).pinv
+    xa, xb = x0.clone(), x0.clone()
+    sa = gmres_device(a, b, xa, True, 1e-9, 60, 1000, pinv, ax0=ax0)
+    sb = gmres_device(a, b, xb, True, 1e-9, 60, 1000, pinv)
+    assert sa.converged and sb.converged
+    assert abs(sa.iterations - sb.iterations) <= 1
+    if sa.iterations == sb.iterations:
+        assert sb.matvecs - sa.matvecs == 1      # the skipped b - A x0 pass
+    assert rel_max(xa.cpu().numpy(), xb.cpu().numpy()) <= 1e-7
+    assert abs(sa.init_residual - sb.init_residual) <= 1e-12 * sb.init_residual
+
+
+def test_solver_cta_budget_same_result(cuda):
+    """ewb_set_solver_ctas: fewer CTAs, same algorithm (fixed-order sums over a
+    different partition: results agree to rounding)."""
+    import torch
+
+    from paper_1212_3032_b200 import _lib, block_diag_precond
+    from paper_1212_3032_b200.linsolve import gmres_device
+
+    lib = _lib.load()
+    g = golden("linsolve")
+    a = torch.from_numpy(g["rod_A"]).cuda()
+    b = torch.from_numpy(g["rod_b"]).cuda()
+    pinv = block_diag_precond(a).pinv
+    full = int(lib.ewb_solver_ctas())
+    x1 = torch.zeros_like(b)
+    s1 = gmres_device(a, b, x1, False, 1e-8, 30, 1000, pinv)
+    try:
+        _lib.check(lib.ewb_set_solver_ctas(37))
+        assert lib.ewb_solver_ctas() == min(37, full)
+        x2 = torch.zeros_like(b)
+        s2 = gmres_device(a, b, x2, False, 1e-8, 30, 1000, pinv)
+    finally:
+        _lib.check(lib.ewb_set_solver_ctas(0))
+    assert lib.ewb_solver_ctas() == full
+    assert abs(s1.iterations - s2.iterations) <= 1
+    assert rel_max(x1.cpu().numpy(), x2.cpu().numpy()) <= 1e-6
+    with pytest.raises(ValueError):
+        _lib.check(lib.ewb_set_solver_ctas(-1))

@@ -232,3 +232,21 @@ def test_gloo_two_rank_gather(tmp_path):
     outs = [p.communicate(timeout=120)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
     assert all("ok" in o for o in outs)
+
+
+def test_forward_transform_batch_equals_per_signal():
+    """forward_mft_batch (linearity for steps, one FFT for tabulated signals)
+    equals the per-signal transform (transform.py:206-211) to 1 ulp."""
+    from paper_1212_3032_b200.transform import TimeSignal, forward_mft, forward_mft_batch
+
+    period, n, eta = 12.5, 128, 0.37
+    sigs = [TimeSignal.zero(), TimeSignal.heaviside(-1.0), TimeSignal.heaviside(0.3137),
+            TimeSignal.tabulated([0.0, 2.0, 5.0, 12.0], [0.0, 1.0, -0.5, 0.25]),
+            TimeSignal.heaviside(1e-7)]
+    ref = np.stack([forward_mft(s, period, n, eta).values for s in sigs])
+    got = forward_mft_batch(sigs, period, n, eta)
+    assert np.abs(got - ref).max() <= 4e-16 * np.abs(ref).max()
+    np.testing.assert_array_equal(got[3], ref[3])          # tabulated: same FFT
+    assert not got[0].any()
+    part = forward_mft_batch(sigs, period, n, eta, n_keep=n // 2 + 1)
+    np.testing.assert_array_equal(part, got[:, : n // 2 + 1])
