@@ -1019,6 +1019,136 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
   R.pos += (unsigned)S;
 }
 
+template <int K, typename Epi>
+__device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
+                            long long r0, long long r1, Epi&& epi) {
+  // 4 row slices x 4 rows; a slice's 128 threads take columns col and
+  // col + 128 of every tile: 4 x K accumulators and 2 x K prefetched x per
+  // thread (K = 3, 4 fit the 128-register budget without spilling).
+  constexpr int kSl = 4, kRw = kRR / kSl, kCols = kSolveThreads / kSl, kCp = kTC / kCols;
+  static_assert(kRR % kSl == 0 && kTC % kCols == 0, "matvec_rows_wide layout");
+  __shared__ cplx s_red[kSolveWarps][kRw][K];
+  __shared__ cplx s_sum[kRR][K];
+  __shared__ int s_rel[kNS];  // warps done with each ring slot
+  const int rows = (int)(r1 - r0);
+  if (rows <= 0) return;
+  const int nblk = (rows + kRR - 1) / kRR;
+  const int ntile = (int)((n + kTC - 1) / kTC);
+  const int S = nblk * ntile;
+  const int last_tc = (int)(n - (long long)(ntile - 1) * kTC);
+  // block q covers rows r0 + [q rows / nblk, (q+1) rows / nblk); stage
+  // u = q ntile + t.  (32-bit arithmetic: rows per CTA << 2^31 / nblk.)
+  // Stage u goes to ring slot (R.pos + u) % kNS; the LAST warp to finish
+  // reading a slot refills it with stage u + kNS, so no warp ever waits for
+  // another except on data arrival (no CTA barrier per stage).
+  auto issue = [&](int u) {
+    const int q = u / ntile, t = u - q * ntile;
+    const int rel0 = q * rows / nblk, nr = (q + 1) * rows / nblk - rel0;
+    const int tc = t == ntile - 1 ? last_tc : kTC;
+    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc,
+               max(0, min(nr, kPinRows - rel0)));
+  };
+  if (threadIdx.x < kNS) s_rel[threadIdx.x] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int u = 0; u < S && u < kNS; ++u) issue(u);
+  }
+  const int col = threadIdx.x % kCols, slice = threadIdx.x / kCols;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  cplx acc[kRw][K];
+#pragma unroll
+  for (int r = 0; r < kRw; ++r)
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
+  cplx xn[kCp][K];  // x of the stage being consumed (loaded after the previous stage's FMAs)
+#pragma unroll
+  for (int m = 0; m < kCp; ++m)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = col + m * kCols;
+      xn[m][k] = c < n ? ldg(x + k * n + c) : cplx{0.0, 0.0};
+    }
+  int q = 0, t = 0;
+  long long row0 = r0;
+  int nrows = rows / nblk;
+  for (int s = 0; s < S; ++s) {
+    const long long c0 = (long long)t * kTC;
+    const int tc = t == ntile - 1 ? last_tc : kTC;
+    const unsigned pos = R.pos + (unsigned)s;
+    ring_wait(R, pos);
+    {
+      const cplx* tile = R.buf + (size_t)(pos % kNS) * kStageElems;
+#pragma unroll
+      for (int m = 0; m < kCp; ++m) {
+        const int c = col + m * kCols;
+        if (c < tc) {
+#pragma unroll
+          for (int r = 0; r < kRw; ++r) {
+            const int row = slice * kRw + r;
+            if (row < nrows) {
+              double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + c);
+              cplx av = {a2.x, a2.y};
+#pragma unroll
+              for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xn[m][k]);
+            }
+          }
+        }
+      }
+    }
+    {  // x for the next stage
+      const long long cb = (t == ntile - 1 ? 0 : c0 + kTC) + col;
+#pragma unroll
+      for (int m = 0; m < kCp; ++m)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const long long cn = cb + m * kCols;
+          xn[m][k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
+        }
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0 &&
+        atomicAdd(&s_rel[pos % kNS], 1) == kSolveWarps - 1) {  // last reader of the slot
+      s_rel[pos % kNS] = 0;
+      if (s + kNS < S) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(s + kNS);
+      }
+    }
+    if (t == ntile - 1) {  // last tile of the block: reduce, then the epilogue
+#pragma unroll
+      for (int r = 0; r < kRw; ++r)
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          warp_sum(acc[r][k]);
+          if (lane == 0) s_red[wid][r][k] = acc[r][k];
+          acc[r][k] = {0.0, 0.0};
+        }
+      __syncthreads();
+      if (threadIdx.x < kRR * K) {
+        const int row = threadIdx.x / K, k = threadIdx.x % K;
+        const int h = row / kRw, r = row % kRw;
+        constexpr int wps = kSolveWarps / kSl;  // warps per row slice
+        cplx sum = {0.0, 0.0};
+        for (int w = 0; w < wps; ++w) sum = sum + s_red[h * wps + w][r][k];
+        s_sum[row][k] = sum;
+      }
+      __syncthreads();
+      epi(row0, nrows, s_sum);
+      __syncthreads();
+      t = 0;
+      if (++q < nblk) {
+        const int rel0 = q * rows / nblk;
+        row0 = r0 + rel0;
+        nrows = (q + 1) * rows / nblk - rel0;
+      }
+    } else {
+      ++t;
+    }
+  }
+  R.pos += (unsigned)S;
+}
+
 // sum over aligned groups of G lanes (result in every lane of the group)
 template <int G>
 __device__ __forceinline__ void group_sum(cplx& v) {
@@ -1757,12 +1887,14 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_multi_gemv(c
   ring_init(ring, 16.0 * (double)n * (double)n > 96e6);
   long long r0, r1;
   cta_rows(n, r0, r1);
-  matvec_rows<K>(ring, A, n, X, r0, r1, [&](long long row0, int nr, cplx (*sum)[K]) {
+  auto store = [&](long long row0, int nr, cplx (*sum)[K]) {
     if (threadIdx.x < nr * K) {
       const int row = threadIdx.x / K, k = threadIdx.x % K;
       Y[k * n + row0 + row] = sum[row][k];
     }
-  });
+  };
+  if constexpr (K <= 2) matvec_rows<K>(ring, A, n, X, r0, r1, store);
+  else matvec_rows_wide<K>(ring, A, n, X, r0, r1, store);
 }
 
 template <int K>
@@ -1781,13 +1913,13 @@ static cudaError_t launch_multi_gemv(const cplx* A, const cplx* X, cplx* Y, long
 }
 
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
-  // Y = A X, at most two columns per pass (more accumulators than that spill
-  // under the 128-register cap of a 512-thread CTA): K = 3 as 2 + 1, 4 as 2 + 2.
-  cudaError_t e = cudaSuccess;
-  for (int c = 0; c < args.K && e == cudaSuccess; c += 2) {
-    const long long off = (long long)c * args.n;
-    if (args.K - c >= 2) e = launch_multi_gemv<2>(args.A, args.X + off, args.Y + off, args.n, s);
-    else e = launch_multi_gemv<1>(args.A, args.X + off, args.Y + off, args.n, s);
+  // Y = A X in one pass over A (K = 3, 4 with the 4-slice layout)
+  cudaError_t e;
+  switch (args.K) {
+    case 1: e = launch_multi_gemv<1>(args.A, args.X, args.Y, args.n, s); break;
+    case 2: e = launch_multi_gemv<2>(args.A, args.X, args.Y, args.n, s); break;
+    case 3: e = launch_multi_gemv<3>(args.A, args.X, args.Y, args.n, s); break;
+    default: e = launch_multi_gemv<4>(args.A, args.X, args.Y, args.n, s); break;
   }
   if (e != cudaSuccess) return e;
   int G = solver_grid_blocks();

@@ -108,8 +108,8 @@ def gather_frequency_results(local: dict, n_freq: int, width: int, dist=None):
 
 
 def n_hist_passes(K: int) -> int:
-    """Passes over A of one SEM product Y = A X (two columns per pass)."""
-    return (K + 1) // 2
+    """Passes over A of one SEM product Y = A X (all K <= 4 columns in one pass)."""
+    return 1 if K > 0 else 0
 
 
 class DeviceSweep:
