@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EWB_ABI_VERSION 2
+#define EWB_ABI_VERSION 3
 
 enum ewb_status {
   EWB_OK = 0,
@@ -112,6 +112,21 @@ int ewb_assemble_tu(ewb_ctx* ctx, double omega_re, double omega_im, void* t_dev,
 int ewb_assemble_system(ewb_ctx* ctx, double omega_re, double omega_im,
                         const uint8_t* kinds_dev, const void* prescribed_dev, void* a_dev,
                         void* b_dev, void* pinv_dev, void* stream);
+
+/* Multi-frequency fused system: nf <= EWB_MAX_BATCH members
+ * of one sweep in one pass over the element pairs; member f equals
+ * ewb_assemble_system at omega[f] to <= 1e-13 of max|A| (the phase factors
+ * e^{-i Re(k) r} are stepped across an equispaced batch instead of being
+ * re-evaluated).  Replaces nf iterations of the per-frequency assembly in
+ * run_sweep (driver.py:128-134).  Host arrays omega_re/omega_im (nf,);
+ * device arrays: prescribed (nf,N), a (nf,N,N), b (nf,N), pinv (nf,n_e,3,3),
+ * flags (nf,4) int32, zeroed by the caller: [f][0] != 0 non-finite entries,
+ * [f][1] singular diagonal blocks (identity fallback). */
+#define EWB_MAX_BATCH 16
+int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* omega_re_host,
+                              const double* omega_im_host, const uint8_t* kinds_dev,
+                              const void* prescribed_dev, void* a_dev, void* b_dev,
+                              void* pinv_dev, int32_t* flags_dev, void* stream);
 
 /* Read and clear the context's fault flags (non-finite entries, singular
  * diagonal blocks) raised by the calls above.  Synchronises. */

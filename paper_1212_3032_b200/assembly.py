@@ -254,6 +254,83 @@ class Assembler:
                 log.warning("%d singular 3x3 diagonal blocks; identity fallback", singular)
         return out
 
+    MAX_BATCH = 16   # EWB_MAX_BATCH
+
+    def assemble_system_multi(self, omegas, bcs: BoundaryConditionSet, prescribed,
+                              out: "SystemBatch | None" = None, flags=None,
+                              check: bool = True) -> "SystemBatch":
+        """``assemble_system`` for nf <= 16 frequencies of one sweep in one pass
+        over the element pairs (ewb_assemble_system_multi).
+
+        ``prescribed`` is (nf, N).  Member f equals ``assemble_system(omegas[f])``
+        to <= 1e-13 of max|A|: pair geometry and the damping factors are shared
+        and, for an equispaced batch (omega_k = k dw - i eta), the phase
+        factors are stepped instead of re-evaluated.  ``flags`` (optional
+        (nf, 4) int32 CUDA tensor, zeroed by the caller) receives the
+        per-member fault words; with ``check`` they are read back and raised on.
+        """
+        torch = _torch()
+        om = np.asarray([complex(w) for w in omegas], dtype=complex)
+        nf = len(om)
+        if not 1 <= nf <= self.MAX_BATCH:
+            raise ValueError(f"batch of {nf} frequencies (1..{self.MAX_BATCH})")
+        if np.any(om == 0):
+            raise ValueError("omega == 0 takes the static path (assemble_system)")
+        kinds = np.ascontiguousarray(bcs.flat_kind(), dtype=np.uint8)
+        n = self.n
+        p = _as_device(prescribed, torch.complex128)
+        if tuple(p.shape) != (nf, n):
+            raise ValueError("prescribed spectra must be (nf, N)")
+        if out is None or out.A.shape[0] < nf:
+            out = SystemBatch.allocate(nf, n)
+        kd = getattr(out, "_kinds_dev", None)
+        if kd is None or not np.array_equal(getattr(out, "_kinds_host", None), kinds):
+            kd = torch.from_numpy(kinds).cuda()
+            out._kinds_dev, out._kinds_host = kd, kinds
+        own_flags = flags is None
+        if own_flags:
+            flags = torch.zeros((nf, 4), dtype=torch.int32, device="cuda")
+        ore = np.ascontiguousarray(om.real)
+        oim = np.ascontiguousarray(om.imag)
+        _lib.check(self._lib.ewb_assemble_system_multi(
+            self._ctx, nf, ore.ctypes.data, oim.ctypes.data, _lib.ptr(kd), _lib.ptr(p),
+            _lib.ptr(out.A), _lib.ptr(out.b), _lib.ptr(out.pinv), _lib.ptr(flags),
+            _lib.stream_handle()), "ewb_assemble_system_multi")
+        out.nf = nf
+        out.unknown_kind = kinds.copy()
+        if check:
+            fl = flags.cpu().numpy()
+            for f in range(nf):
+                if fl[f, 0]:
+                    raise FloatingPointError(f"non-finite entries assembled at omega = {om[f]}")
+                if fl[f, 1]:
+                    log.warning("%d singular 3x3 diagonal blocks; identity fallback", fl[f, 1])
+        return out
+
+
+@dataclass
+class SystemBatch:
+    """nf dense systems of one sweep, stacked: A (nf,N,N), b (nf,N), pinv (nf,n_e,3,3)."""
+
+    A: object
+    b: object
+    pinv: object
+    unknown_kind: np.ndarray | None = None
+    nf: int = 0
+
+    @classmethod
+    def allocate(cls, nf: int, n: int) -> "SystemBatch":
+        torch = _torch()
+        return cls(A=torch.empty((nf, n, n), dtype=torch.complex128, device="cuda"),
+                   b=torch.empty((nf, n), dtype=torch.complex128, device="cuda"),
+                   pinv=torch.empty((nf, n // 3, 3, 3), dtype=torch.complex128, device="cuda"))
+
+    def member(self, f: int) -> DenseSystem:
+        if not 0 <= f < self.nf:
+            raise IndexError(f)
+        return DenseSystem(A=self.A[f], b=self.b[f], unknown_kind=self.unknown_kind,
+                           pinv=self.pinv[f])
+
 
 def assemble_tu(mesh: TriangleMesh, material: Material, omega: complex,
                 quadrature: QuadratureSet | None = None):

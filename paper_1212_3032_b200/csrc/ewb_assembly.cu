@@ -180,6 +180,28 @@ __global__ void k_near_fill(Geo g, const int* near_ptr, int* near_j, int* near_r
   }
 }
 
+// Mid (gauss7) pair list, row-sorted CSR: the multi-frequency path takes
+// mid pairs out of the far kernel so its warps are uniform in Q.
+__global__ void k_mid_fill(Geo g, const int* mid_ptr, int* mid_j, int* mid_row) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= g.n_e) return;
+  int i = warp;
+  double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+  int pos = mid_ptr[i];
+  for (int j0 = 0; j0 < g.n_e; j0 += 32) {
+    int j = j0 + lane;
+    bool md = false;
+    if (j < g.n_e && j != i) md = exact_tier(xi, yi, zi, g.cx[j], g.cy[j], g.cz[j], g.diam[j]) == 1;
+    unsigned m = __ballot_sync(0xffffffffu, md);
+    if (md) {
+      int p = pos + __popc(m & ((1u << lane) - 1u));
+      mid_j[p] = j;
+      mid_row[p] = i;
+    }
+    pos += __popc(m);
+  }
+}
+
 // ---------------------------------------------------------------------
 // pair kernels
 // ---------------------------------------------------------------------
@@ -611,6 +633,306 @@ __global__ void k_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int*
 }
 
 // ---------------------------------------------------------------------
+// multi-frequency system assembly
+//
+// nf frequencies of one sweep share everything but the frequency: the pair
+// geometry, the tier and level decisions, the BC kinds, and — because an
+// exponential-window sweep has omega_k = k dw - i eta — the damping factors
+// e^{-eta r / c}.  The phase factors e^{-i Re(k) r} are stepped across the
+// batch with one complex multiply per point per frequency (the step
+// e^{-i dRe(k) r} is one sincos per point per batch), so far pairs pay
+// 4 sincos + 2 exp per point per BATCH instead of 2 sincos + 2 exp per point
+// per frequency.  The recurrence error after <= 15 steps is a few ulp
+// (|step| = 1 to rounding), far inside the 1e-10 matrix bar; the first
+// member is bit-identical to the single-frequency kernel's phase.
+// Every output element still has exactly one writer and every b sum a fixed
+// order (far tiles, mid list, near list, self), so the batch is
+// bit-reproducible.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ SysArgs sys_member(const SysBatch& o, int f, long long N, int n_e) {
+  return SysArgs{o.kinds, o.p + (size_t)f * N, o.A + (size_t)f * N * N, o.pinv + (size_t)f * 9 * n_e,
+                 o.b + (size_t)f * N};
+}
+
+// Shared-memory loads the compiler may not hoist: the per-member constants
+// are read where they are used instead of occupying ~28 registers across
+// the quadrature loop (a runtime member index cannot use constant-bank
+// operands the way the single-frequency kernels do).
+__device__ __forceinline__ double lds_d(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+// (FreqConst is 8-byte aligned with a 120-byte stride: two scalar loads)
+__device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), lds_d(&p->im)}; }
+
+// The series branch (|k_s r| < 0.1 for far pairs: the lowest members of a
+// batch only) out of line, so its register peak does not shape the hot
+// closed-form loop.
+__device__ __noinline__ Brackets brackets_series_cold(const FreqConst fc, double r) {
+  return brackets_series(fc, r);
+}
+
+__device__ __forceinline__ cplx unit_phase(double a) {
+  double s, c;
+  sincos(a, &s, &c);
+  return {c, -s};
+}
+
+// Far pairs only (tier 0, gauss3): warp = (kFarRows rows, 32-column tile),
+// lane = column.  The per-point phase state (e^{-i z_s}, e^{-i z_p} and their
+// per-member steps) lives in shared memory, [state][q][thread].
+#ifndef EWB_FARMULTI_MINB
+#define EWB_FARMULTI_MINB 3
+#endif
+template <bool RECUR>
+__global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
+                                                                    SysBatch o) {
+  __shared__ cplx sph[4][3][128];
+  __shared__ double syf[9][128];
+  __shared__ FreqConst sfc[kMaxBatch];
+  const int tid = threadIdx.x;
+  for (int k = tid; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
+    ((double*)sfc)[k] = ((const double*)fb.fc)[k];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int ntile = (g.n_e + 31) >> 5;
+  const int ngroups = (g.n_e + kFarRows - 1) / kFarRows;
+  if (warp >= (long long)ngroups * ntile) return;
+  const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
+  const int j = t * 32 + lane;
+  const bool jv = j < g.n_e;
+  const long long N = 3LL * g.n_e;
+  const int jj = jv ? j : 0;
+  const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
+  const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
+#pragma unroll
+  for (int c = 0; c < 9; ++c) syf[c][tid] = g.yfar[(size_t)c * g.n_e + jj];
+  const int nf = fb.nf;
+  for (int r = 0; r < kFarRows; ++r) {
+    const int i = rg * kFarRows + r;
+    if (i >= g.n_e) break;
+    const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+    const bool far = jv && j != i && exact_tier(xi, yi, zi, cxj, cyj, czj, dj) == 0;
+    auto geom = [&](int q, double& rr, double& ir, double& dx, double& dy, double& dz,
+                    double& dn) {
+      dx = syf[3 * q][tid] - xi; dy = syf[3 * q + 1][tid] - yi; dz = syf[3 * q + 2][tid] - zi;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      ir = rsqrt(r2);
+      rr = r2 * ir;
+      dx *= ir; dy *= ir; dz *= ir;
+      dn = fma(dz, nz, fma(dy, ny, dx * nx));
+    };
+    if (RECUR && far) {
+#pragma unroll 1
+      for (int q = 0; q < 3; ++q) {
+        double rr, ir, dx, dy, dz, dn;
+        geom(q, rr, ir, dx, dy, dz, dn);
+        sph[0][q][tid] = phase_factor(fb.fc[0].ks, rr);
+        sph[1][q][tid] = phase_factor(fb.fc[0].kp, rr);
+        sph[2][q][tid] = unit_phase(fb.dks * rr);
+        sph[3][q][tid] = unit_phase(fb.dkp * rr);
+      }
+    }
+    const FreqConst& fc0 = fb.fc[0];   // material constants (member-independent)
+#pragma unroll 1
+    for (int f = 0; f < nf; ++f) {
+      cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+      if (far) {
+        Acc<cplx> acc;
+        acc_zero(acc);
+#pragma unroll 1
+        for (int q = 0; q < 3; ++q) {
+          double rr, ir, dx, dy, dz, dn;
+          geom(q, rr, ir, dx, dy, dz, dn);
+          FreqConst fc;
+          fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
+          fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+          fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
+          fc.ratio = fc0.ratio;
+          Brackets br;
+          if (RECUR) {
+            const cplx Es = sph[0][q][tid], ep = sph[1][q][tid];
+            if (fc.ks_abs * rr < kFarSwitch) br = brackets_series_cold(fc, rr);
+            else br = brackets_phase(fc, rr, ir, Es, ep);
+            sph[0][q][tid] = Es * sph[2][q][tid];
+            sph[1][q][tid] = ep * sph[3][q][tid];
+          } else {
+            br = fc.ks_abs * rr < kFarSwitch ? brackets_series_cold(fc, rr)
+                                             : brackets_closed(fc, rr, ir);
+          }
+          point_contract(acc, fc, br, ir, dx, dy, dz, dn, g.wfar[q] * ar);
+        }
+        cplx U[3][3], T[3][3];
+        acc_finalize(acc, nx, ny, nz, fc0.inv4pimu, fc0.inv4pi, U, T);
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
+        if (!ok) o.flags[4 * f] = 1;
+        sys_block(sys_member(o, f, N, g.n_e), N, i, j, U, T, bc);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        warp_sum(bc[a]);
+        if (lane == 0) o.bpart[((size_t)f * ntile + t) * N + 3 * i + a] = bc[a];
+      }
+    }
+  }
+}
+
+// Mid pairs (tier 1, gauss7) from the CSR list: thread = (pair, member).
+__global__ void __launch_bounds__(128) k_mid_multi(Geo g, FreqBatch fb, SysBatch o, int n_mid) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n_mid * fb.nf) return;
+  const int f = (int)(idx / n_mid), p = (int)(idx % n_mid);
+  const FreqConst& fc = fb.fc[f];
+  const int i = g.mid_row[p], j = g.mid_j[p];
+  const long long N = 3LL * g.n_e;
+  const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+  const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
+  Acc<cplx> acc;
+  acc_zero(acc);
+#pragma unroll 1
+  for (int q = 0; q < 7; ++q) {
+    double dx = g.ymid[(size_t)(3 * q) * g.n_e + j] - xi;
+    double dy = g.ymid[(size_t)(3 * q + 1) * g.n_e + j] - yi;
+    double dz = g.ymid[(size_t)(3 * q + 2) * g.n_e + j] - zi;
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    const double ir = rsqrt(r2);
+    const double rr = r2 * ir;
+    dx *= ir; dy *= ir; dz *= ir;
+    const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+    const Brackets br =
+        fc.ks_abs * rr < kFarSwitch ? brackets_series(fc, rr) : brackets_closed(fc, rr, ir);
+    point_contract(acc, fc, br, ir, dx, dy, dz, dn, g.wmid[q] * ar);
+  }
+  cplx U[3][3], T[3][3];
+  acc_finalize(acc, nx, ny, nz, fc.inv4pimu, fc.inv4pi, U, T);
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
+  if (!ok) o.flags[4 * f] = 1;
+  cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+  sys_block(sys_member(o, f, N, g.n_e), N, i, j, U, T, bc);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) o.bmid[((size_t)f * n_mid + p) * 3 + a] = bc[a];
+}
+
+// Near pairs: warp per pair (lanes split the subdivided rule), members in turn.
+__global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysBatch o,
+                                                       int n_near) {
+  const int lane = threadIdx.x & 31;
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= n_near) return;
+  const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
+  const long long N = 3LL * g.n_e;
+  const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+  const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
+  double v[9];
+  load_corners(g, j, v);
+  const RuleRef rr = g.sub[L];
+  const double* bary = g.rules + rr.off;
+  const double* wq = bary + 3 * rr.q;
+  const int a = lane / 3, c = lane % 3;
+  const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+  const double n[3] = {nx, ny, nz};
+  const int ac = lane < 9 ? sym[a][c] : 0;
+  const int aa = lane < 9 ? a : 0, cc = lane < 9 ? c : 0;
+  const size_t col = 3 * (size_t)j + cc;
+  const bool dir = o.kinds[col] == kDirichlet;
+#pragma unroll 1
+  for (int f = 0; f < fb.nf; ++f) {
+    const FreqConst& fc = fb.fc[f];
+    Acc<cplx> acc;
+    acc_zero(acc);
+    for (int q = lane; q < rr.q; q += 32) {
+      double b0 = bary[3 * q], b1 = bary[3 * q + 1], b2 = bary[3 * q + 2];
+      double dx = fma(b2, v[6], fma(b1, v[3], b0 * v[0])) - xi;
+      double dy = fma(b2, v[7], fma(b1, v[4], b0 * v[1])) - yi;
+      double dz = fma(b2, v[8], fma(b1, v[5], b0 * v[2])) - zi;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      double ir = rsqrt(r2);
+      double r = r2 * ir;
+      dx *= ir; dy *= ir; dz *= ir;
+      double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+      point_dynamic(acc, fc, r, ir, dx, dy, dz, dn, wq[q] * ar);
+    }
+    acc_warp_allsum(acc);
+    cplx u_ac = aa == cc ? acc.su - acc.P[ac] : -acc.P[ac];
+    u_ac = fc.inv4pimu * u_ac;
+    cplx t = acc.B[ac];
+    madd(t, n[aa], acc.va[cc]);
+    madd(t, n[cc], acc.vc[aa]);
+    if (aa == cc) t = t + acc.sa;
+    const cplx t_ac = fc.inv4pi * t;
+    const bool ok = lane >= 9 || (finite(u_ac) && finite(t_ac));
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) o.flags[4 * f] = 1;
+    cplx bt = {0.0, 0.0};
+    if (lane < 9) {
+      const cplx pv = o.p[(size_t)f * N + col];
+      o.A[(size_t)f * N * N + (size_t)(3 * i + a) * N + col] = dir ? -u_ac : t_ac;
+      bt = dir ? -(t_ac * pv) : u_ac * pv;
+    }
+    const cplx b1 = {__shfl_down_sync(0xffffffffu, bt.re, 1), __shfl_down_sync(0xffffffffu, bt.im, 1)};
+    const cplx b2 = {__shfl_down_sync(0xffffffffu, bt.re, 2), __shfl_down_sync(0xffffffffu, bt.im, 2)};
+    if (lane < 9 && c == 0) o.bnear[((size_t)f * n_near + p) * 3 + a] = (cplx{0.0, 0.0} + bt + b1) + b2;
+  }
+}
+
+// Diagonal blocks, b and P^{-1} of every member (as k_self_dyn<OUT_SYS>).
+__global__ void __launch_bounds__(128) k_self_multi(Geo g, FreqBatch fb, SysBatch o,
+                                                    const double* diag_base, int ntile, int n_mid,
+                                                    int n_near) {
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= g.n_e) return;
+  const long long N = 3LL * g.n_e;
+#pragma unroll 1
+  for (int f = 0; f < fb.nf; ++f) {
+    const Phys<true> ph{fb.fc[f]};
+    Acc<cplx> acc;
+    self_accumulate(g, ph, j, acc);
+    cplx U[3][3], T[3][3];
+    acc_finalize(acc, g.nx[j], g.ny[j], g.nz[j], ph.i4pm(), ph.i4p(), U, T);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) T[a][b] = T[a][b] + cplx{diag_base[9 * j + 3 * a + b], 0.0};
+    if (lane == 0) {
+      bool ok = true;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
+      if (!ok) o.flags[4 * f] = 1;
+    }
+    cplx bs[3];
+    const cplx* bp = o.bpart + (size_t)f * ntile * N;
+    for (int a = 0; a < 3; ++a) {
+      cplx s = {0.0, 0.0};
+      for (int t = lane; t < ntile; t += 32) s = s + bp[(size_t)t * N + 3 * j + a];
+      warp_sum(s);
+      bs[a] = s;
+    }
+    if (lane == 0) {
+      for (int p = g.mid_ptr[j]; p < g.mid_ptr[j + 1]; ++p)
+        for (int a = 0; a < 3; ++a) bs[a] = bs[a] + o.bmid[((size_t)f * n_mid + p) * 3 + a];
+      for (int p = g.near_ptr[j]; p < g.near_ptr[j + 1]; ++p)
+        for (int a = 0; a < 3; ++a) bs[a] = bs[a] + o.bnear[((size_t)f * n_near + p) * 3 + a];
+      const SysArgs sa = sys_member(o, f, N, g.n_e);
+      cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+      sys_block(sa, N, j, j, U, T, bc);
+      for (int a = 0; a < 3; ++a) sa.b[3 * j + a] = bs[a] + bc[a];
+      cplx D[3][3];
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) D[a][c] = sa.A[(size_t)(3 * j + a) * N + 3 * j + c];
+      write_pinv(sa.pinv, j, D, o.flags + 4 * f + 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------
 static inline unsigned blocks_for(long long threads, int bs) {
@@ -756,6 +1078,16 @@ cudaError_t setup_context(Context& c, const double* centroids, const double* nor
   g.near_ptr = near_ptr; g.near_j = near_j; g.near_row = near_row; g.near_lvl = near_lvl;
   EWB_NOTE k_near_fill<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, near_ptr, near_j, near_row,
                                                                  near_lvl);
+  // mid CSR (multi-frequency path)
+  std::vector<int> mptr(n + 1, 0);
+  for (int e = 0; e < n; ++e) mptr[e + 1] = mptr[e] + (int)mc[e];
+  int* mid_ptr = dalloc<int>(c, n + 1, err);
+  int* mid_j = dalloc<int>(c, mptr[n] + 1, err);
+  int* mid_row = dalloc<int>(c, mptr[n] + 1, err);
+  if (err) return err;
+  cudaMemcpyAsync(mid_ptr, mptr.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, s);
+  g.mid_ptr = mid_ptr; g.mid_j = mid_j; g.mid_row = mid_row;
+  EWB_NOTE k_mid_fill<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(g, mid_ptr, mid_j, mid_row);
   // near level census
   std::vector<int> lv(c.n_near);
   if (c.n_near) cudaMemcpyAsync(lv.data(), near_lvl, (size_t)c.n_near * 4, cudaMemcpyDeviceToHost, s);
@@ -861,6 +1193,74 @@ cudaError_t set_exterior(Context& c, int on, cudaStream_t s) {
   EWB_NOTE k_diag_shift<<<blocks_for(c.n_e, 128), 128, 0, s>>>(c.n_e, c.diag_base,
                                                                 on ? 1.0 : -1.0);
   c.exterior = on;
+  return cudaGetLastError();
+}
+
+}  // namespace ewb
+
+namespace ewb {
+
+static cudaError_t ensure_multi_scratch(Context& c, int nf) {
+  if (nf <= c.nf_cap) return cudaSuccess;
+  for (void* p : {(void*)c.bpart_m, (void*)c.bmid_m, (void*)c.bnear_m}) {
+    if (!p) continue;
+    cudaFree(p);
+    for (auto& q : c.owned)
+      if (q == p) q = nullptr;
+  }
+  c.bpart_m = c.bmid_m = c.bnear_m = nullptr;
+  c.nf_cap = 0;
+  cudaError_t err = cudaSuccess;
+  const size_t n3 = 3 * (size_t)c.n_e;
+  c.bpart_m = dalloc<cplx>(c, (size_t)nf * c.n_tiles * n3, err);
+  c.bmid_m = dalloc<cplx>(c, (size_t)nf * 3 * c.n_mid + 1, err);
+  c.bnear_m = dalloc<cplx>(c, (size_t)nf * 3 * c.n_near + 1, err);
+  if (err == cudaSuccess) c.nf_cap = nf;
+  return err;
+}
+
+cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
+                                         const double* oim, const uint8_t* kinds,
+                                         const cplx* prescribed, cplx* A, cplx* b, cplx* pinv,
+                                         int* flags, cudaStream_t s) {
+  if (nf < 1 || nf > kMaxBatch) return cudaErrorInvalidValue;
+  cudaError_t err = ensure_multi_scratch(c, nf);
+  if (err) return err;
+  FreqBatch fb{};
+  fb.nf = nf;
+  for (int f = 0; f < nf; ++f) fb.fc[f] = freq_const(c, ore[f], oim[f]);
+  // phase recurrence: one Im(omega), Re(omega) equispaced to a few ulp
+  bool recur = nf >= 2;
+  if (recur) {
+    const double ks0 = fb.fc[0].ks.re, ksl = fb.fc[nf - 1].ks.re;
+    const double kp0 = fb.fc[0].kp.re, kpl = fb.fc[nf - 1].kp.re;
+    fb.dks = (ksl - ks0) / (nf - 1);
+    fb.dkp = (kpl - kp0) / (nf - 1);
+    const double tol = 1e-14 * fmax(fabs(ks0), fabs(ksl));
+    const double tolp = 1e-14 * fmax(fabs(kp0), fabs(kpl));
+    for (int f = 0; f < nf; ++f) {
+      recur = recur && oim[f] == oim[0];
+      recur = recur && fabs(fb.fc[f].ks.re - (ks0 + f * fb.dks)) <= tol;
+      recur = recur && fabs(fb.fc[f].kp.re - (kp0 + f * fb.dkp)) <= tolp;
+    }
+  }
+  fb.recur = recur ? 1 : 0;
+  SysBatch o{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
+  const int n = c.n_e;
+  const long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  const unsigned fb_blocks = blocks_for(warps * 32, 128);
+  if (recur)
+    EWB_NOTE k_far_multi<true><<<fb_blocks, 128, 0, s>>>(c.g, fb, o);
+  else
+    EWB_NOTE k_far_multi<false><<<fb_blocks, 128, 0, s>>>(c.g, fb, o);
+  if (c.n_mid)
+    EWB_NOTE k_mid_multi<<<blocks_for((long long)c.n_mid * nf, 128), 128, 0, s>>>(c.g, fb, o,
+                                                                                (int)c.n_mid);
+  if (c.n_near)
+    EWB_NOTE k_near_multi<<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, fb, o,
+                                                                                  c.n_near);
+  EWB_NOTE k_self_multi<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(
+      c.g, fb, o, c.diag_base, c.n_tiles, (int)c.n_mid, c.n_near);
   return cudaGetLastError();
 }
 

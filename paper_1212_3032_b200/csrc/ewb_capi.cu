@@ -151,6 +151,22 @@ int ewb_assemble_system(ewb_ctx* ctx, double ore, double oim, const uint8_t* kin
   return EWB_OK;
 }
 
+int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* ore, const double* oim,
+                              const uint8_t* kinds, const void* p, void* a, void* b, void* pinv,
+                              int32_t* flags, void* stream) {
+  if (!ctx || !ore || !oim || !kinds || !p || !a || !b || !pinv || !flags)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi: null argument");
+  if (nf < 1 || nf > EWB_MAX_BATCH)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi: nf must be in [1, EWB_MAX_BATCH]");
+  for (int f = 0; f < nf; ++f)
+    if (int rc = check_omega(ore[f], oim[f], "ewb_assemble_system_multi")) return rc;
+  EWB_CUDA(ewb::launch_assemble_system_multi(ctx->c, nf, ore, oim, kinds, (const ewb::cplx*)p,
+                                             (ewb::cplx*)a, (ewb::cplx*)b, (ewb::cplx*)pinv,
+                                             flags, S(stream)),
+           "ewb_assemble_system_multi");
+  return EWB_OK;
+}
+
 int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite, int32_t* singular, void* stream) {
   if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_flags: null argument");
   int h[4] = {0, 0, 0, 0};

@@ -139,6 +139,38 @@ struct Brackets {
 //   f1 = Es + 3Fs - Ep - 3Fp
 //   f2 = Gs - 2Es - 3Fs + Ep + 3Fp
 //   f3 = Gs - 4Es - 9Fs - Gp + 4Ep + 9Fp
+//
+// brackets_phase takes the two phase factors Es = e^{-i z_s}, ep = e^{-i z_p}
+// from the caller (the multi-frequency kernels step them across an
+// equispaced frequency batch instead of calling exp/sincos per frequency).
+__device__ __forceinline__ Brackets brackets_phase(const FreqConst& fc, double r, double ir,
+                                                   cplx Es, cplx ep) {
+  double zs_re = fc.ks.re * r, zs_im = fc.ks.im * r;
+  double zp_re = fc.kp.re * r, zp_im = fc.kp.im * r;
+  cplx Ep = fc.g2 * ep;
+  cplx qs = fc.iks * ir, qp = fc.ikp * ir;      // 1/z
+  cplx qs2 = qs * qs, qp2 = qp * qp;
+  cplx ts = {qs.im - qs2.re, -qs.re - qs2.im};
+  cplx tp = {qp.im - qp2.re, -qp.re - qp2.im};
+  cplx Fs = Es * ts, Fp = Ep * tp;
+  cplx Gs = Es * cplx{zs_im, -zs_re};
+  cplx Gp = Ep * cplx{zp_im, -zp_re};
+  Brackets o;
+  o.f0 = Es + Fs - Fp;
+  o.f1 = Es + 3.0 * (Fs - Fp) - Ep;
+  o.f2 = Gs - 2.0 * Es + Ep + 3.0 * (Fp - Fs);
+  o.f3 = Gs - Gp + 4.0 * (Ep - Es) + 9.0 * (Fp - Fs);
+  return o;
+}
+
+// e^{-i k r} = e^{Im(k) r} (cos(Re(k) r) - i sin(Re(k) r))
+__device__ __forceinline__ cplx phase_factor(cplx k, double r) {
+  double s, c;
+  sincos(k.re * r, &s, &c);
+  double m = exp(k.im * r);
+  return {m * c, -m * s};
+}
+
 __device__ __forceinline__ Brackets brackets_closed(const FreqConst& fc, double r, double ir) {
   // z = k r ;  -i z = (k.im r) - i (k.re r)
   double zs_re = fc.ks.re * r, zs_im = fc.ks.im * r;
@@ -326,6 +358,19 @@ __device__ __forceinline__ void acc_point(Acc<S>& A, S Phi, S Psi, S Aw, S Bw, S
 }
 
 // One dynamic point: r, 1/r, unit d, dn, weight w.
+__device__ __forceinline__ void point_contract(Acc<cplx>& A, const FreqConst& fc,
+                                               const Brackets& f, double ir, double dx,
+                                               double dy, double dz, double dn, double w) {
+  double wr = w * ir, wr2 = wr * ir;
+  cplx Phi = wr * f.f0;
+  cplx Psi = wr * f.f1;
+  cplx Aw = wr2 * (f.f2 - f.f1);
+  cplx Bw = (2.0 * wr2 * dn) * (2.0 * f.f1 - f.f3);
+  cplx dd = f.f2 - f.f3;
+  cplx Cw = wr2 * (fc.ratio * (dd - 2.0 * f.f1) - 2.0 * (dd - f.f1));
+  acc_point(A, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
+}
+
 __device__ __forceinline__ void point_dynamic(Acc<cplx>& A, const FreqConst& fc, double r,
                                               double ir, double dx, double dy, double dz,
                                               double dn, double w) {

@@ -35,6 +35,9 @@ struct Geo {
   const int *near_j;                 // column of each near pair
   const int *near_lvl;               // subdivision level 1..4
   const int *near_row;               // row of each near pair
+  const int *mid_ptr;                // CSR by row of the mid (gauss7) pairs, n_e+1
+  const int *mid_j;                  // column of each mid pair
+  const int *mid_row;                // row of each mid pair
   const double *rules;               // rule tables
   RuleRef sub[kMaxNearLevel + 1];    // sub[L] for L = 1..4
 };
@@ -110,6 +113,31 @@ __device__ __forceinline__ bool finite(cplx v) { return isfinite(v.re) && isfini
 __device__ __forceinline__ cplx to_c(double v) { return {v, 0.0}; }
 __device__ __forceinline__ cplx to_c(cplx v) { return v; }
 
+// Multi-frequency batch: per-frequency constants plus the
+// phase step used when the batch is equispaced in Re(omega) with one
+// Im(omega) (every exponential-window sweep: omega_k = k dw - i eta).
+constexpr int kMaxBatch = 16;
+struct FreqBatch {
+  FreqConst fc[kMaxBatch];
+  int nf;
+  int recur;                         // 1: step the phase factors across the batch
+  double dks, dkp;                   // Re(ks), Re(kp) step between consecutive members
+};
+
+// Outputs of a multi-frequency system assembly; member f of every array
+// starts at f x its per-frequency size.
+struct SysBatch {
+  const uint8_t* kinds;              // (N,)
+  const cplx* p;                     // (nf, N) prescribed values
+  cplx* A;                           // (nf, N, N)
+  cplx* b;                           // (nf, N)
+  cplx* pinv;                        // (nf, n_e, 3, 3)
+  int* flags;                        // (nf, 4): [0] non-finite, [1] singular blocks
+  cplx* bpart;                       // (nf, n_tiles, N) far b partials
+  cplx* bmid;                        // (nf, n_mid, 3)
+  cplx* bnear;                       // (nf, n_near, 3)
+};
+
 struct Context {
   int n_e = 0;
   int n_near = 0;
@@ -130,6 +158,11 @@ struct Context {
   double* spart = nullptr;           // [n_tiles][n_e][9] static row-sum partials
   double* snear = nullptr;           // [n_near][9]
   int* flags = nullptr;              // [0] non-finite seen, [1] singular blocks
+  // multi-frequency scratch, allocated on first use for nf_cap members
+  int nf_cap = 0;
+  cplx* bpart_m = nullptr;
+  cplx* bmid_m = nullptr;
+  cplx* bnear_m = nullptr;
   cudaStream_t stream = nullptr;
 };
 
@@ -153,5 +186,10 @@ cudaError_t launch_apply_bcs(const cplx* T, const cplx* U, const uint8_t* kinds,
 cudaError_t launch_blockdiag_inverse(const cplx* A, long long n, cplx* pinv, int* singular,
                                      cudaStream_t s);
 cudaError_t set_exterior(Context& c, int on, cudaStream_t s);
+// nf frequencies in one pass over the element pairs (batch buffers: SysBatch)
+cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
+                                         const double* oim, const uint8_t* kinds,
+                                         const cplx* prescribed, cplx* A, cplx* b, cplx* pinv,
+                                         int* flags, cudaStream_t s);
 
 }  // namespace ewb

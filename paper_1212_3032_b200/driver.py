@@ -5,8 +5,11 @@
 every history when any solve fails, manifest) while every per-frequency
 array stays in HBM.  The device loop lives in :class:`DeviceSweep`:
 
-    per k:  ewb_assemble_system   (assembly + BCs + b + P^{-1}, no T/U)
-            ewb_sem_guess         (if history: Y = A X, QR, x0)
+    per group of nb (default 8) consecutive k:
+            ewb_assemble_system_multi (assembly + BCs + b + P^{-1} of all nb
+                                  frequencies in one pass over the element
+                                  pairs; no T/U)
+    per k:  ewb_sem_guess         (if history: Y = A X, QR, x0)
             ewb_gmres             (the whole restarted solve, one launch)
             one small read-back   (fault flags + iteration count + residuals)
     end:    ewb_window_idft       (conjugate fill + window + IDFT for the
@@ -23,6 +26,7 @@ from __future__ import annotations
 import ctypes
 import logging
 import math
+import os
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -123,7 +127,7 @@ class DeviceSweep:
     """
 
     def __init__(self, cfg: SweepConfig, assembler: Assembler | None = None,
-                 frequencies: list | None = None):
+                 frequencies: list | None = None, assembly_batch: int | None = None):
         import torch
 
         _lib.require_cuda()
@@ -152,7 +156,27 @@ class DeviceSweep:
         self.x = torch.zeros(n, dtype=torch.complex128, device="cuda")
         self.hist = torch.zeros((cfg.sem_depth, n), dtype=torch.complex128, device="cuda")
         self.system = None
+        self.batch = None
+        self.assembly_batch = assembly_batch
         self.d2h_bytes = 0
+
+    def batch_size(self) -> int:
+        """Frequencies assembled per pass over the element pairs.
+
+        ``assembly_batch`` (constructor) or ``EWB_ASSEMBLY_BATCH`` (default 8),
+        capped at 16 and by free HBM: the batch holds nb dense N x N systems
+        (cfg2: 3.77 GB each) and may take at most half of the free memory."""
+        import torch
+
+        nb = self.assembly_batch
+        if nb is None:
+            nb = int(os.environ.get("EWB_ASSEMBLY_BATCH", "8"))
+        nb = max(1, min(int(nb), 16, len(self.frequencies)))
+        if nb > 1 and self.batch is None:
+            free, _ = torch.cuda.mem_get_info()
+            per = 16 * self.n * self.n + 16 * 4 * self.n
+            nb = max(1, min(nb, int(0.5 * free // per)))
+        return nb
 
     def run_matrix_free(self):
         """Matrix-free sweep (north-star item 2): the operator is recomputed in
@@ -240,44 +264,79 @@ class DeviceSweep:
         hist_all = torch.zeros((nf, cap), dtype=torch.float64, device="cuda")
         flags_all = torch.zeros((nf, 4), dtype=torch.int32, device="cuda")
         ax0 = torch.empty(self.n, dtype=torch.complex128, device="cuda")
-        for idx, k in enumerate(self.frequencies):
-            omega = complex(self.omegas[k])
+        nb = self.batch_size()
+        asm_ev = []
+        idx = 0
+        while idx < nf:
+            # next group: up to nb frequencies assembled in one pass over the
+            # element pairs (omega == 0, the static path, always alone)
+            group = [idx]
+            if complex(self.omegas[self.frequencies[idx]]) != 0:
+                while (len(group) < nb and idx + len(group) < nf
+                       and complex(self.omegas[self.frequencies[idx + len(group)]]) != 0):
+                    group.append(idx + len(group))
+            ks = [self.frequencies[i] for i in group]
             try:
-                if timing:
-                    e_a = torch.cuda.Event(enable_timing=True)
-                    e_a.record()
-                sysm = asm.assemble_system(omega, cfg.bcs, self.P[k],
-                                           out=self.system if omega != 0 else None, check=False)
-                if sysm.pinv is None:   # omega == 0: static path (kappa = 0 sweeps)
-                    sysm.pinv = block_diag_precond(sysm.A).pinv
+                e_a = torch.cuda.Event(enable_timing=True)
+                e_b = torch.cuda.Event(enable_timing=True)
+                e_a.record()
+                if len(group) > 1:
+                    self.batch = asm.assemble_system_multi(
+                        [self.omegas[k] for k in ks], cfg.bcs, self.P[ks[0]:ks[-1] + 1]
+                        if ks == list(range(ks[0], ks[-1] + 1)) else self.P[ks],
+                        out=self.batch, flags=flags_all[group[0]:group[-1] + 1], check=False)
+                    members = [self.batch.member(f) for f in range(len(group))]
                 else:
-                    self.system = sysm
-                _lib.check(lib.ewb_ctx_flags_async(asm.ctx, _lib.ptr(flags_all[idx]),
-                                                   _lib.stream_handle()), "ewb_ctx_flags_async")
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                use_sem = cfg.sem_enabled and n_hist > 0
-                if use_sem:
-                    sem_device(sysm.A, sysm.b, self.hist[:n_hist], 1e-10, self.x, ax0_out=ax0)
-                gmres_device(sysm.A, sysm.b, self.x, use_sem, cfg.tol, cfg.restart, cfg.maxiter,
-                             sysm.pinv, sync=False, ax0=ax0 if use_sem else None,
-                             res=res_all[idx], hist=hist_all[idx])
-                e1.record()
+                    omega = complex(self.omegas[ks[0]])
+                    sysm = asm.assemble_system(omega, cfg.bcs, self.P[ks[0]],
+                                               out=self.system if omega != 0 else None,
+                                               check=False)
+                    if sysm.pinv is None:   # omega == 0: static path (kappa = 0 sweeps)
+                        sysm.pinv = block_diag_precond(sysm.A).pinv
+                    else:
+                        self.system = sysm
+                    _lib.check(lib.ewb_ctx_flags_async(asm.ctx, _lib.ptr(flags_all[group[0]]),
+                                                       _lib.stream_handle()),
+                               "ewb_ctx_flags_async")
+                    members = [sysm]
+                e_b.record()
+                asm_ev.append((e_a, e_b))
             except SweepError:
                 raise
             except Exception as exc:
-                raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
-            ev.append((idx, k, omega, e_a if timing else None, e0, e1, n_hist if use_sem else 0))
-            self.sol[k] = self.x
-            if cfg.sem_enabled:
-                self.hist[1:] = self.hist[:-1].clone()
-                self.hist[0] = self.x
-                n_hist = min(n_hist + 1, K)
+                omega = complex(self.omegas[ks[0]])
+                raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
+            for i, k, sysm in zip(group, ks, members):
+                omega = complex(self.omegas[k])
+                try:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    use_sem = cfg.sem_enabled and n_hist > 0
+                    if use_sem:
+                        sem_device(sysm.A, sysm.b, self.hist[:n_hist], 1e-10, self.x, ax0_out=ax0)
+                    gmres_device(sysm.A, sysm.b, self.x, use_sem, cfg.tol, cfg.restart,
+                                 cfg.maxiter, sysm.pinv, sync=False,
+                                 ax0=ax0 if use_sem else None, res=res_all[i], hist=hist_all[i])
+                    e1.record()
+                except SweepError:
+                    raise
+                except Exception as exc:
+                    raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
+                ev.append((i, k, omega, e0, e1, n_hist if use_sem else 0))
+                self.sol[k] = self.x
+                if cfg.sem_enabled:
+                    self.hist[1:] = self.hist[:-1].clone()
+                    self.hist[0] = self.x
+                    n_hist = min(n_hist + 1, K)
+            idx += len(group)
         torch.cuda.synchronize()
         flags = flags_all.cpu().numpy()
         res_host = res_all.cpu().numpy()
-        for idx, k, omega, ea, e0, e1, sem_cols in ev:
+        if timing:
+            for e_a, e_b in asm_ev:
+                self.phase["assembly_ms"] += e_a.elapsed_time(e_b)
+        for idx, k, omega, e0, e1, sem_cols in ev:
             if flags[idx, 0]:
                 raise SweepError(f"frequency index {k} (omega={omega:.6g}): non-finite entries "
                                  f"assembled at omega = {omega}")
@@ -296,11 +355,7 @@ class DeviceSweep:
             st.seconds = e0.elapsed_time(e1) * 1e-3
             stats[k] = st
             if timing:
-                self.phase["assembly_ms"] += ea.elapsed_time(e0)
                 self.phase["solve_ms"] += e0.elapsed_time(e1)
-                if idx + 1 < len(ev):
-                    self.phase["gap_ms"] = self.phase.get("gap_ms", 0.0) + \
-                        e1.elapsed_time(ev[idx + 1][3])
             # passes over A: the solver's own count + SEM's Y = A X pass(es)
             self.phase["matvecs"] += st.matvecs + (n_hist_passes(sem_cols) if sem_cols else 0)
             self.phase["solves"] += 1

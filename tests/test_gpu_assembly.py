@@ -188,3 +188,91 @@ def test_apply_bcs_device_matches_oracle(cube):
     kinds = bcs.flat_kind()
     assert np.array_equal(u.cpu().numpy()[kinds == 1], p[kinds == 1])
     assert np.array_equal(t.cpu().numpy()[kinds == 0], p[kinds == 0])
+
+
+# ---------------------------------------------------------------------------
+# multi-frequency system assembly (ewb_assemble_system_multi)
+# ---------------------------------------------------------------------------
+def _cfg1_bcs(mesh):
+    from paper_1212_3032_b200 import DIRICHLET, NEUMANN, BoundaryConditionSet
+
+    bcs = BoundaryConditionSet.traction_free(mesh.n_elements)
+    bcs.set_region(mesh, 4, (0, 1, 2), DIRICHLET, 0)
+    bcs.set_region(mesh, 5, (2,), NEUMANN, 1)
+    return bcs
+
+
+def _cfg1_omegas():
+    from paper_1212_3032_b200.transform import eta_from_kappa, frequency_grid
+
+    period = 8.0 / _unit().c_s
+    return frequency_grid(period, 128, eta_from_kappa(6.0 / np.log(10.0), period))
+
+
+@pytest.mark.parametrize("ks", [list(range(0, 8)), list(range(57, 65)), [1, 2, 3, 4],
+                                [3, 9, 10, 40, 41], [20]])
+def test_multi_frequency_system_equals_single(cfg1_asm, ks):
+    """Each batch member == the single-frequency fused system (phase recurrence for
+    the equispaced batches, direct evaluation for the others)."""
+    import torch
+
+    om = _cfg1_omegas()
+    mesh = cfg1_asm.mesh
+    bcs = _cfg1_bcs(mesh)
+    rng = np.random.default_rng(11)
+    n = cfg1_asm.n
+    P = rng.normal(size=(len(ks), n)) + 1j * rng.normal(size=(len(ks), n))
+    batch = cfg1_asm.assemble_system_multi([om[k] for k in ks], bcs, P)
+    for f, k in enumerate(ks):
+        ref = cfg1_asm.assemble_system(om[k], bcs, P[f])
+        m = batch.member(f)
+        amax = torch.abs(ref.A).max().item()
+        assert torch.abs(m.A - ref.A).max().item() <= 1e-13 * amax, (k, f)
+        assert torch.abs(m.b - ref.b).max().item() <= 1e-12 * torch.abs(ref.b).max().item()
+        assert torch.abs(m.pinv - ref.pinv).max().item() <= 1e-10 * torch.abs(ref.pinv).max().item()
+
+
+def test_multi_frequency_rows_match_reference_golden(cfg1_asm):
+    """Batch members at k = 1 and k = 64 against the live reference's T/U rows."""
+    g = golden("cfg1_rows")
+    om = _cfg1_omegas()
+    bcs = _cfg1_bcs(cfg1_asm.mesh)
+    kinds = bcs.flat_kind()
+    n = cfg1_asm.n
+    elems = g["elements"]
+    rows = (3 * elems[:, None] + np.arange(3)).ravel()
+    p = np.zeros(n, complex)
+    p[kinds == 0] = 0.3 - 0.1j
+    for ks in ([1, 2, 3, 4, 5, 6, 7, 8], [57, 58, 59, 60, 61, 62, 63, 64]):
+        batch = cfg1_asm.assemble_system_multi([om[k] for k in ks], bcs, np.tile(p, (8, 1)))
+        for k in (1, 64):
+            if k not in ks:
+                continue
+            f = ks.index(k)
+            a_rows = batch.A[f].cpu().numpy()[rows]
+            t_rows, u_rows = g[f"T_rows_k{k}"], g[f"U_rows_k{k}"]
+            a_ref = np.where(kinds[None, :] == 1, -u_rows, t_rows)
+            amax = max(float(g[f"Tmax_k{k}"]), float(g[f"Umax_k{k}"]))
+            assert np.abs(a_rows - a_ref).max() <= TOL * amax, k
+            neu, dirc = kinds == 0, kinds == 1
+            b_ref = u_rows[:, neu] @ p[neu] - t_rows[:, dirc] @ p[dirc]   # assembly.py:295-296
+            b_rows = batch.b[f].cpu().numpy()[rows]
+            assert rel_max(b_rows, b_ref) <= TOL
+
+
+def test_multi_frequency_is_bit_deterministic_and_validates(cfg1_asm):
+    om = _cfg1_omegas()
+    bcs = _cfg1_bcs(cfg1_asm.mesh)
+    P = np.ones((4, cfg1_asm.n), complex)
+    a = cfg1_asm.assemble_system_multi(om[10:14], bcs, P)
+    A1, b1 = a.A.cpu().numpy(), a.b.cpu().numpy()
+    a = cfg1_asm.assemble_system_multi(om[10:14], bcs, P, out=a)
+    assert np.array_equal(A1, a.A.cpu().numpy()) and np.array_equal(b1, a.b.cpu().numpy())
+    with pytest.raises(ValueError, match="static path"):
+        cfg1_asm.assemble_system_multi([0.0, 1.0 - 0.1j], bcs, P[:2])
+    with pytest.raises(ValueError, match="positive imaginary"):
+        cfg1_asm.assemble_system_multi([1.0 + 0.5j], bcs, P[:1])
+    with pytest.raises(ValueError, match="batch of 17"):
+        cfg1_asm.assemble_system_multi(om[:17], bcs, np.ones((17, cfg1_asm.n), complex))
+    with pytest.raises(ValueError, match=r"\(nf, N\)"):
+        cfg1_asm.assemble_system_multi(om[1:3], bcs, P)
