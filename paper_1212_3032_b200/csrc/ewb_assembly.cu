@@ -666,13 +666,6 @@ __device__ __forceinline__ double lds_d(const double* p) {
 // (FreqConst is 8-byte aligned with a 120-byte stride: two scalar loads)
 __device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), lds_d(&p->im)}; }
 
-// The series branch (|k_s r| < 0.1 for far pairs: the lowest members of a
-// batch only) out of line, so its register peak does not shape the hot
-// closed-form loop.
-__device__ __noinline__ Brackets brackets_series_cold(const FreqConst fc, double r) {
-  return brackets_series(fc, r);
-}
-
 __device__ __forceinline__ cplx unit_phase(double a) {
   double s, c;
   sincos(a, &s, &c);
@@ -680,17 +673,59 @@ __device__ __forceinline__ cplx unit_phase(double a) {
 }
 
 // Far pairs only (tier 0, gauss3): warp = (kFarRows rows, 32-column tile),
-// lane = column.  The per-point phase state (e^{-i z_s}, e^{-i z_p} and their
-// per-member steps) lives in shared memory, [state][q][thread].
+// lane = column.  Per row, each of the 3 field points keeps in shared
+// memory (layout [slot][q][thread], conflict-free):
+//   geometry  r, 1/r, d (3), d.n, w/(4 pi mu r), w/(4 pi r^2)   (8 doubles)
+//   phase     e^{-i z_s}, g2 e^{-i z_p} and their per-member steps (4 cplx)
+// so a member costs the closed-form brackets, the weights and the
+// contraction only (no geometry, no transcendentals).  1/(4 pi mu) and
+// 1/(4 pi) ride in the weights; g2 = (k_p/k_s)^2 (real to rounding for a
+// real material; the reference's complex value differs by < 1e-16) rides
+// in the P phase.
 #ifndef EWB_FARMULTI_MINB
 #define EWB_FARMULTI_MINB 3
 #endif
+#ifndef EWB_FAR_QUNROLL
+#define EWB_FAR_QUNROLL 3
+#endif
+constexpr int kFarQUnroll = EWB_FAR_QUNROLL;
+constexpr int kFarGeo = 8;
+constexpr size_t kFarMultiSmem = sizeof(double) * (kFarGeo * 3 * 128 + 4 * 3 * 2 * 128) +
+                                 sizeof(FreqConst) * kMaxBatch;
+
+// closed-form brackets from the phase factors, g2 already inside Ep
+__device__ __forceinline__ Brackets brackets_phase_g(cplx ks, cplx kp, cplx iks, cplx ikp, double r,
+                                                     double ir, cplx Es, cplx Ep) {
+  const double zs_re = ks.re * r, zs_im = ks.im * r;
+  const double zp_re = kp.re * r, zp_im = kp.im * r;
+  const cplx qs = iks * ir, qp = ikp * ir;
+  const cplx qs2 = qs * qs, qp2 = qp * qp;
+  const cplx ts = {qs.im - qs2.re, -qs.re - qs2.im};
+  const cplx tp = {qp.im - qp2.re, -qp.re - qp2.im};
+  const cplx Fs = Es * ts, Fp = Ep * tp;
+  const cplx Gs = Es * cplx{zs_im, -zs_re};
+  const cplx Gp = Ep * cplx{zp_im, -zp_re};
+  Brackets o;
+  o.f0 = Es + Fs - Fp;
+  o.f1 = Es + 3.0 * (Fs - Fp) - Ep;
+  o.f2 = Gs - 2.0 * Es + Ep + 3.0 * (Fp - Fs);
+  o.f3 = Gs - Gp + 4.0 * (Ep - Es) + 9.0 * (Fp - Fs);
+  return o;
+}
+
+// exponent bits: all ones <=> Inf or NaN (integer pipe, not FP64)
+__device__ __forceinline__ unsigned expo(double v) {
+  return (unsigned)__double2hiint(v) & 0x7ff00000u;
+}
+__device__ __forceinline__ unsigned expo(cplx v) { return max(expo(v.re), expo(v.im)); }
+
 template <bool RECUR>
 __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
                                                                     SysBatch o) {
-  __shared__ cplx sph[4][3][128];
-  __shared__ double syf[9][128];
-  __shared__ FreqConst sfc[kMaxBatch];
+  extern __shared__ double sm_far[];
+  double (*sgeo)[3][128] = reinterpret_cast<double (*)[3][128]>(sm_far);
+  cplx (*sph)[3][128] = reinterpret_cast<cplx (*)[3][128]>(sm_far + kFarGeo * 3 * 128);
+  FreqConst* sfc = reinterpret_cast<FreqConst*>(sm_far + kFarGeo * 3 * 128 + 4 * 3 * 2 * 128);
   const int tid = threadIdx.x;
   for (int k = tid; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
     ((double*)sfc)[k] = ((const double*)fb.fc)[k];
@@ -707,72 +742,125 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
   const int jj = jv ? j : 0;
   const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
   const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
-#pragma unroll
-  for (int c = 0; c < 9; ++c) syf[c][tid] = g.yfar[(size_t)c * g.n_e + jj];
+  const FreqConst& fc0 = fb.fc[0];   // material constants (member-independent)
   const int nf = fb.nf;
+  // BC kinds of column j's three DOFs (member-independent), bit c = Dirichlet
+  const unsigned kbits = (o.kinds[3 * jj] == kDirichlet ? 1u : 0u) |
+                         (o.kinds[3 * jj + 1] == kDirichlet ? 2u : 0u) |
+                         (o.kinds[3 * jj + 2] == kDirichlet ? 4u : 0u);
   for (int r = 0; r < kFarRows; ++r) {
     const int i = rg * kFarRows + r;
     if (i >= g.n_e) break;
     const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
     const bool far = jv && j != i && exact_tier(xi, yi, zi, cxj, cyj, czj, dj) == 0;
-    auto geom = [&](int q, double& rr, double& ir, double& dx, double& dy, double& dz,
-                    double& dn) {
-      dx = syf[3 * q][tid] - xi; dy = syf[3 * q + 1][tid] - yi; dz = syf[3 * q + 2][tid] - zi;
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      ir = rsqrt(r2);
-      rr = r2 * ir;
-      dx *= ir; dy *= ir; dz *= ir;
-      dn = fma(dz, nz, fma(dy, ny, dx * nx));
-    };
-    if (RECUR && far) {
+    if (far) {
 #pragma unroll 1
       for (int q = 0; q < 3; ++q) {
-        double rr, ir, dx, dy, dz, dn;
-        geom(q, rr, ir, dx, dy, dz, dn);
-        sph[0][q][tid] = phase_factor(fb.fc[0].ks, rr);
-        sph[1][q][tid] = phase_factor(fb.fc[0].kp, rr);
-        sph[2][q][tid] = unit_phase(fb.dks * rr);
-        sph[3][q][tid] = unit_phase(fb.dkp * rr);
+        double dx = g.yfar[(size_t)(3 * q) * g.n_e + j] - xi;
+        double dy = g.yfar[(size_t)(3 * q + 1) * g.n_e + j] - yi;
+        double dz = g.yfar[(size_t)(3 * q + 2) * g.n_e + j] - zi;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const double ir = rsqrt(r2);
+        const double rr = r2 * ir;
+        dx *= ir; dy *= ir; dz *= ir;
+        const double w = g.wfar[q] * ar * ir;
+        sgeo[0][q][tid] = rr;
+        sgeo[1][q][tid] = ir;
+        sgeo[2][q][tid] = dx;
+        sgeo[3][q][tid] = dy;
+        sgeo[4][q][tid] = dz;
+        sgeo[5][q][tid] = fma(dz, nz, fma(dy, ny, dx * nx));
+        sgeo[6][q][tid] = w * fc0.inv4pimu;
+        sgeo[7][q][tid] = w * ir * fc0.inv4pi;
+        if (RECUR) {
+          sph[0][q][tid] = phase_factor(fc0.ks, rr);
+          sph[1][q][tid] = fc0.g2 * phase_factor(fc0.kp, rr);
+          sph[2][q][tid] = unit_phase(fb.dks * rr);
+          sph[3][q][tid] = unit_phase(fb.dkp * rr);
+        }
       }
     }
-    const FreqConst& fc0 = fb.fc[0];   // material constants (member-independent)
 #pragma unroll 1
     for (int f = 0; f < nf; ++f) {
       cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
       if (far) {
+        // prescribed values of this member, loaded ahead of the quadrature loop
+        cplx pv[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pv[c] = o.p[(size_t)f * N + 3 * j + c];
         Acc<cplx> acc;
         acc_zero(acc);
-#pragma unroll 1
+        const double ratio = fc0.ratio;
+#pragma unroll kFarQUnroll
         for (int q = 0; q < 3; ++q) {
-          double rr, ir, dx, dy, dz, dn;
-          geom(q, rr, ir, dx, dy, dz, dn);
-          FreqConst fc;
-          fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
-          fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
-          fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
-          fc.ratio = fc0.ratio;
+          const double rr = sgeo[0][q][tid], ir = sgeo[1][q][tid];
+          const double dx = sgeo[2][q][tid], dy = sgeo[3][q][tid], dz = sgeo[4][q][tid];
+          const double dn = sgeo[5][q][tid], wu = sgeo[6][q][tid], wt = sgeo[7][q][tid];
+          const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
+          const cplx iks = lds_c(&sfc[f].iks), ikp = lds_c(&sfc[f].ikp);
           Brackets br;
+          cplx Es, Ep;
           if (RECUR) {
-            const cplx Es = sph[0][q][tid], ep = sph[1][q][tid];
-            if (fc.ks_abs * rr < kFarSwitch) br = brackets_series_cold(fc, rr);
-            else br = brackets_phase(fc, rr, ir, Es, ep);
+            Es = sph[0][q][tid];
+            Ep = sph[1][q][tid];
             sph[0][q][tid] = Es * sph[2][q][tid];
-            sph[1][q][tid] = ep * sph[3][q][tid];
+            sph[1][q][tid] = Ep * sph[3][q][tid];
           } else {
-            br = fc.ks_abs * rr < kFarSwitch ? brackets_series_cold(fc, rr)
-                                             : brackets_closed(fc, rr, ir);
+            Es = phase_factor(ks, rr);
+            Ep = lds_c(&sfc[f].g2) * phase_factor(kp, rr);
           }
-          point_contract(acc, fc, br, ir, dx, dy, dz, dn, g.wfar[q] * ar);
+          if (lds_d(&sfc[f].ks_abs) * rr < kFarSwitch) {
+            FreqConst fc = fc0;
+            fc.ks = ks; fc.kp = kp; fc.g2 = lds_c(&sfc[f].g2);
+            br = brackets_series_cold(fc, rr);
+          } else {
+            br = brackets_phase_g(ks, kp, iks, ikp, rr, ir, Es, Ep);
+          }
+          // weighted scalars (kernels.py:330-333), 1/(4 pi mu), 1/(4 pi) inside
+          const cplx Phi = wu * br.f0;
+          const cplx Psi = wu * br.f1;
+          const cplx Aw = wt * (br.f2 - br.f1);
+          const cplx Bw = (2.0 * wt * dn) * (2.0 * br.f1 - br.f3);
+          const cplx dd = br.f2 - br.f3;
+          const cplx Cw = wt * (ratio * (dd - 2.0 * br.f1) - 2.0 * (dd - br.f1));
+          acc_point(acc, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
         }
+        // blocks (kernels.py:336-356): U symmetric, T = B + n va^T + vc n^T + sa I
         cplx U[3][3], T[3][3];
-        acc_finalize(acc, nx, ny, nz, fc0.inv4pimu, fc0.inv4pi, U, T);
-        bool ok = true;
+        const double n[3] = {nx, ny, nz};
+        const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+        unsigned ex = 0;
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
-          for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
-        if (!ok) o.flags[4 * f] = 1;
-        sys_block(sys_member(o, f, N, g.n_e), N, i, j, U, T, bc);
+          for (int b = 0; b < 3; ++b) {
+            if (b >= a) U[a][b] = a == b ? acc.su - acc.P[sym[a][b]] : -acc.P[sym[a][b]];
+            else U[a][b] = U[b][a];
+            cplx tv = acc.B[sym[a][b]];
+            madd(tv, n[a], acc.va[b]);
+            madd(tv, n[b], acc.vc[a]);
+            if (a == b) tv = tv + acc.sa;
+            T[a][b] = tv;
+            ex = max(ex, max(expo(U[a][b]), expo(tv)));
+          }
+        if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
+        // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
+        // Dirichlet column A = -U, b -= T p
+        cplx* Af = o.A + (size_t)f * N * N;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (kbits & (1u << c)) {
+              row[c] = -U[a][c];
+              bc[a] = bc[a] - T[a][c] * pv[c];
+            } else {
+              row[c] = T[a][c];
+              bc[a] = bc[a] + U[a][c] * pv[c];
+            }
+          }
+        }
       }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
@@ -907,19 +995,23 @@ __global__ void __launch_bounds__(128) k_self_multi(Geo g, FreqBatch fb, SysBatc
         for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
       if (!ok) o.flags[4 * f] = 1;
     }
+    // b_j: far tile partials, then the row's mid and near partials, each
+    // lane-strided in a fixed order and tree-reduced (deterministic)
     cplx bs[3];
     const cplx* bp = o.bpart + (size_t)f * ntile * N;
+    const int m0 = g.mid_ptr[j], m1 = g.mid_ptr[j + 1];
+    const int q0 = g.near_ptr[j], q1 = g.near_ptr[j + 1];
     for (int a = 0; a < 3; ++a) {
-      cplx s = {0.0, 0.0};
+      cplx s = {0.0, 0.0}, sm = {0.0, 0.0}, sn = {0.0, 0.0};
       for (int t = lane; t < ntile; t += 32) s = s + bp[(size_t)t * N + 3 * j + a];
+      for (int p = m0 + lane; p < m1; p += 32) sm = sm + o.bmid[((size_t)f * n_mid + p) * 3 + a];
+      for (int p = q0 + lane; p < q1; p += 32) sn = sn + o.bnear[((size_t)f * n_near + p) * 3 + a];
       warp_sum(s);
-      bs[a] = s;
+      warp_sum(sm);
+      warp_sum(sn);
+      bs[a] = (s + sm) + sn;
     }
     if (lane == 0) {
-      for (int p = g.mid_ptr[j]; p < g.mid_ptr[j + 1]; ++p)
-        for (int a = 0; a < 3; ++a) bs[a] = bs[a] + o.bmid[((size_t)f * n_mid + p) * 3 + a];
-      for (int p = g.near_ptr[j]; p < g.near_ptr[j + 1]; ++p)
-        for (int a = 0; a < 3; ++a) bs[a] = bs[a] + o.bnear[((size_t)f * n_near + p) * 3 + a];
       const SysArgs sa = sys_member(o, f, N, g.n_e);
       cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
       sys_block(sa, N, j, j, U, T, bc);
@@ -1249,10 +1341,18 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
   const int n = c.n_e;
   const long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
   const unsigned fb_blocks = blocks_for(warps * 32, 128);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_far_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kFarMultiSmem);
+    cudaFuncSetAttribute(k_far_multi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kFarMultiSmem);
+    attr = true;
+  }
   if (recur)
-    EWB_NOTE k_far_multi<true><<<fb_blocks, 128, 0, s>>>(c.g, fb, o);
+    EWB_NOTE k_far_multi<true><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
   else
-    EWB_NOTE k_far_multi<false><<<fb_blocks, 128, 0, s>>>(c.g, fb, o);
+    EWB_NOTE k_far_multi<false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
   if (c.n_mid)
     EWB_NOTE k_mid_multi<<<blocks_for((long long)c.n_mid * nf, 128), 128, 0, s>>>(c.g, fb, o,
                                                                                 (int)c.n_mid);

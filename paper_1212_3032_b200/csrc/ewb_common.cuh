@@ -265,6 +265,13 @@ __device__ __forceinline__ Brackets brackets_series_n(const FreqConst& fc, doubl
   return o;
 }
 
+// The series branch out of line, for kernels whose series points are rare
+// (far pairs switch at |k_s r| < 0.1): its register peak then does not
+// shape the hot closed-form loop.
+static __device__ __noinline__ Brackets brackets_series_cold(const FreqConst fc, double r) {
+  return brackets_series(fc, r);
+}
+
 // Strict per-point switch exactly as kernels.py:79-95 (|k_s r| < 0.35).
 // The far/mid (and matrix-free far) kernels run with fc.sw = kFarSwitch:
 // between 0.1 and 0.35 the closed form agrees with the series to <= 2e-13
@@ -382,6 +389,24 @@ __device__ __forceinline__ void point_dynamic(Acc<cplx>& A, const FreqConst& fc,
   cplx Bw = (2.0 * wr2 * dn) * (2.0 * f.f1 - f.f3);
   cplx dd = f.f2 - f.f3;
   cplx Cw = wr2 * (fc.ratio * (dd - 2.0 * f.f1) - 2.0 * (dd - f.f1));
+  acc_point(A, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
+}
+
+// One dynamic point with the block constants folded into the weights:
+// wu = w / (4 pi mu r), wt = w / (4 pi r^2); series below |k_s r| < sw taken
+// out of line.  The accumulators then hold U and T contributions directly.
+__device__ __forceinline__ void point_dynamic_scaled(Acc<cplx>& A, const FreqConst& fc,
+                                                     double sw, double r, double ir, double dx,
+                                                     double dy, double dz, double dn, double wu,
+                                                     double wt) {
+  const Brackets f =
+      fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
+  const cplx Phi = wu * f.f0;
+  const cplx Psi = wu * f.f1;
+  const cplx Aw = wt * (f.f2 - f.f1);
+  const cplx Bw = (2.0 * wt * dn) * (2.0 * f.f1 - f.f3);
+  const cplx dd = f.f2 - f.f3;
+  const cplx Cw = wt * (fc.ratio * (dd - 2.0 * f.f1) - 2.0 * (dd - f.f1));
   acc_point(A, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
 }
 

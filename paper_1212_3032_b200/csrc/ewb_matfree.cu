@@ -77,10 +77,14 @@ struct MfArgs {
   int K, nchunk, chunk_cols;
 };
 
-template <int K, bool USE_U>
 #ifndef EWB_MF_MINB
 #define EWB_MF_MINB 3
 #endif
+#ifndef EWB_MF_QUNROLL
+#define EWB_MF_QUNROLL 1
+#endif
+constexpr int kMfQUnroll = EWB_MF_QUNROLL;
+template <int K, bool USE_U>
 __global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
   __shared__ double s_geo[kMfTile][8];        // cx cy cz diam nx ny nz area
   __shared__ double s_y[kMfTile][30];         // 3 far + 7 mid points
@@ -131,24 +135,31 @@ __global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true
                                   s_geo[jj][3]);
       if (tier == 2) continue;
       const double nx = s_geo[jj][4], ny = s_geo[jj][5], nz = s_geo[jj][6], ar = s_geo[jj][7];
-      const int Q = tier == 0 ? 3 : 7;
-      const double* yq = tier == 0 ? &s_y[jj][0] : &s_y[jj][9];
-      const double* wq = tier == 0 ? g.wfar : g.wmid;
+      // 1/(4 pi mu) and 1/(4 pi) ride in the weights; series out of line
+      const double cu = ar * ph.fc.inv4pimu, ct = ar * ph.fc.inv4pi;
       Acc<cplx> acc;
       acc_zero(acc);
-      for (int q = 0; q < Q; ++q) {
-        double dx = yq[3 * q] - xi, dy = yq[3 * q + 1] - yi, dz = yq[3 * q + 2] - zi;
+      auto point = [&](const double* yq, double wq) {
+        double dx = yq[0] - xi, dy = yq[1] - yi, dz = yq[2] - zi;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        double ir = rsqrt(r2);
-        double r = r2 * ir;
+        const double ir = rsqrt(r2);
+        const double r = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
-        double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-        ph.point(acc, r, ir, dx, dy, dz, dn, wq[q] * ar);
+        const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+        const double wi = wq * ir;
+        point_dynamic_scaled(acc, ph.fc, kFarSwitch, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
+      };
+      if (tier == 0) {
+#pragma unroll kMfQUnroll
+        for (int q = 0; q < 3; ++q) point(&s_y[jj][3 * q], g.wfar[q]);
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < 7; ++q) point(&s_y[jj][9 + 3 * q], g.wmid[q]);
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        acc_apply_T(acc, nx, ny, nz, ph.fc.inv4pi, s_vt[jj][k], y[k]);
-        if (USE_U) acc_apply_U(acc, ph.fc.inv4pimu, s_vu[jj][k], y[k]);
+        acc_apply_T(acc, nx, ny, nz, 1.0, s_vt[jj][k], y[k]);
+        if (USE_U) acc_apply_U(acc, 1.0, s_vu[jj][k], y[k]);
       }
     }
   }
