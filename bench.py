@@ -312,7 +312,9 @@ def run_ours_sweep(args, rank, world, local_rank):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     pair_evals_per_s = (counts["far"] + counts["mid"] + counts["near"] + counts["n_elements"]) / \
         (asm_per_freq_ms * 1e-3)
-    rl_asm = {"bound": "fp64", "kernel": "assembly (k_farmid+k_near+k_self_dyn, fused BCs)",
+    rl_asm = {"bound": "fp64",
+              "kernel": "multi-frequency assembly (k_far_multi+k_mid_multi+k_near_multi+"
+                        "k_self_multi, %d frequencies per pass, fused BCs)" % ds.batch_size(),
               "achieved": round(asm_tflops, 3), "peak": round(peak64, 3), "unit": "TFLOP/s",
               "frac": round(asm_tflops / peak64, 4),
               "peak_source": "measured DFMA probe in this run (MEASURED_PEAKS.json has no FP64)",

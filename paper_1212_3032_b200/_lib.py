@@ -93,7 +93,8 @@ def load(path: os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # EWB_LIB: an A/B build variant (tools/build_variant.py) instead of the default
+    p = Path(path) if path else Path(os.environ.get("EWB_LIB", LIB_PATH))
     if not p.exists():
         raise NativeUnavailable(
             f"{p} is not built; run `python -m paper_1212_3032_b200.build` "

@@ -654,17 +654,6 @@ __device__ __forceinline__ SysArgs sys_member(const SysBatch& o, int f, long lon
                  o.b + (size_t)f * N};
 }
 
-// Shared-memory loads the compiler may not hoist: the per-member constants
-// are read where they are used instead of occupying ~28 registers across
-// the quadrature loop (a runtime member index cannot use constant-bank
-// operands the way the single-frequency kernels do).
-__device__ __forceinline__ double lds_d(const double* p) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
-  return v;
-}
-// (FreqConst is 8-byte aligned with a 120-byte stride: two scalar loads)
-__device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), lds_d(&p->im)}; }
 
 __device__ __forceinline__ cplx unit_phase(double a) {
   double s, c;
@@ -872,15 +861,21 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
 }
 
 // Mid pairs (tier 1, gauss7) from the CSR list: thread = (pair, member).
-__global__ void __launch_bounds__(128) k_mid_multi(Geo g, FreqBatch fb, SysBatch o, int n_mid) {
+// Constants folded into the weights; series (|k_s r| < 0.1) out of line.
+__global__ void __launch_bounds__(128, 3) k_mid_multi(Geo g, FreqBatch fb, SysBatch o, int n_mid) {
+  __shared__ FreqConst sfc[kMaxBatch];
+  for (int k = threadIdx.x; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
+    ((double*)sfc)[k] = ((const double*)fb.fc)[k];
+  __syncthreads();
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)n_mid * fb.nf) return;
   const int f = (int)(idx / n_mid), p = (int)(idx % n_mid);
-  const FreqConst& fc = fb.fc[f];
+  const FreqConst& fc0 = fb.fc[0];
   const int i = g.mid_row[p], j = g.mid_j[p];
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
   const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
+  const double cu = ar * fc0.inv4pimu, ct = ar * fc0.inv4pi;
   Acc<cplx> acc;
   acc_zero(acc);
 #pragma unroll 1
@@ -893,28 +888,80 @@ __global__ void __launch_bounds__(128) k_mid_multi(Geo g, FreqBatch fb, SysBatch
     const double rr = r2 * ir;
     dx *= ir; dy *= ir; dz *= ir;
     const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-    const Brackets br =
-        fc.ks_abs * rr < kFarSwitch ? brackets_series(fc, rr) : brackets_closed(fc, rr, ir);
-    point_contract(acc, fc, br, ir, dx, dy, dz, dn, g.wmid[q] * ar);
+    FreqConst fc;
+    fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
+    fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+    fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
+    fc.ratio = fc0.ratio;
+    const double wi = g.wmid[q] * ir;
+    point_dynamic_scaled(acc, fc, kFarSwitch, rr, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
   }
   cplx U[3][3], T[3][3];
-  acc_finalize(acc, nx, ny, nz, fc.inv4pimu, fc.inv4pi, U, T);
-  bool ok = true;
+  acc_finalize(acc, nx, ny, nz, 1.0, 1.0, U, T);
+  unsigned ex = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int b = 0; b < 3; ++b) ok = ok && finite(U[a][b]) && finite(T[a][b]);
-  if (!ok) o.flags[4 * f] = 1;
+    for (int b = 0; b < 3; ++b) ex = max(ex, max(expo(U[a][b]), expo(T[a][b])));
+  if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
   cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
   sys_block(sys_member(o, f, N, g.n_e), N, i, j, U, T, bc);
 #pragma unroll
   for (int a = 0; a < 3; ++a) o.bmid[((size_t)f * n_mid + p) * 3 + a] = bc[a];
 }
 
-// Near pairs: warp per pair (lanes split the subdivided rule), members in turn.
+// Near pairs: warp per pair (lanes split the subdivided rule), members in
+// turn.  The per-member constants come from shared memory (a runtime member
+// index cannot use constant-bank operands); the 40 accumulator words are
+// reduced across the warp through shared memory (lane l sums word l over
+// the 32 lanes in lane order: 31 adds per word instead of a 5-level
+// butterfly over all 40 words in every lane), deterministic.
+constexpr int kAccWords = (int)(sizeof(Acc<cplx>) / sizeof(double));   // 40
+// Visit the 40 accumulator words with compile-time indices (no address of
+// the accumulator is taken, so it stays in registers).
+template <typename F>
+__device__ __forceinline__ void acc_words(Acc<cplx>& A, F&& f) {
+  f(0, A.su.re); f(1, A.su.im);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { f(2 + 2 * k, A.P[k].re); f(3 + 2 * k, A.P[k].im); }
+  f(14, A.sa.re); f(15, A.sa.im);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { f(16 + 2 * k, A.va[k].re); f(17 + 2 * k, A.va[k].im); }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) { f(22 + 2 * k, A.B[k].re); f(23 + 2 * k, A.B[k].im); }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { f(34 + 2 * k, A.vc[k].re); f(35 + 2 * k, A.vc[k].im); }
+}
+
+// Warp totals of the accumulator words into red[k][32] (word k summed over
+// lanes 0..31 in order); with `back`, every lane's acc also ends with them.
+__device__ __forceinline__ void acc_reduce_smem(Acc<cplx>& acc, double (*red)[33], int lane,
+                                                bool back = true) {
+  acc_words(acc, [&](int k, double& w) { red[k][lane] = w; });
+  __syncwarp();
+  double s1 = 0.0, s2 = 0.0;
+#pragma unroll 8
+  for (int m = 0; m < 32; ++m) s1 += red[lane][m];
+  if (lane < kAccWords - 32)
+#pragma unroll 8
+    for (int m = 0; m < 32; ++m) s2 += red[32 + lane][m];
+  __syncwarp();
+  red[lane][32] = s1;
+  if (lane < kAccWords - 32) red[32 + lane][32] = s2;
+  __syncwarp();
+  if (!back) return;
+  acc_words(acc, [&](int k, double& w) { w = red[k][32]; });
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysBatch o,
                                                        int n_near) {
-  const int lane = threadIdx.x & 31;
+  __shared__ double sred[4][kAccWords][33];
+  __shared__ FreqConst sfc[kMaxBatch];
+  for (int k = threadIdx.x; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
+    ((double*)sfc)[k] = ((const double*)fb.fc)[k];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n_near) return;
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
@@ -933,9 +980,11 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
   const int aa = lane < 9 ? a : 0, cc = lane < 9 ? c : 0;
   const size_t col = 3 * (size_t)j + cc;
   const bool dir = o.kinds[col] == kDirichlet;
+  const FreqConst& fc0 = fb.fc[0];
+  const double cu = ar * fc0.inv4pimu, ct = ar * fc0.inv4pi;
+  double (*red)[33] = sred[wid];
 #pragma unroll 1
   for (int f = 0; f < fb.nf; ++f) {
-    const FreqConst& fc = fb.fc[f];
     Acc<cplx> acc;
     acc_zero(acc);
     for (int q = lane; q < rr.q; q += 32) {
@@ -944,20 +993,28 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
       double dy = fma(b2, v[7], fma(b1, v[4], b0 * v[1])) - yi;
       double dz = fma(b2, v[8], fma(b1, v[5], b0 * v[2])) - zi;
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      double ir = rsqrt(r2);
-      double r = r2 * ir;
+      const double ir = rsqrt(r2);
+      const double r = r2 * ir;
       dx *= ir; dy *= ir; dz *= ir;
-      double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-      point_dynamic(acc, fc, r, ir, dx, dy, dz, dn, wq[q] * ar);
+      const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+      FreqConst fc;
+      fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
+      fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+      fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
+      fc.ratio = fc0.ratio;
+      const double wi = wq[q] * ir;
+      point_dynamic_scaled(acc, fc, kSeriesSwitch, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
     }
-    acc_warp_allsum(acc);
-    cplx u_ac = aa == cc ? acc.su - acc.P[ac] : -acc.P[ac];
-    u_ac = fc.inv4pimu * u_ac;
-    cplx t = acc.B[ac];
-    madd(t, n[aa], acc.va[cc]);
-    madd(t, n[cc], acc.vc[aa]);
-    if (aa == cc) t = t + acc.sa;
-    const cplx t_ac = fc.inv4pi * t;
+    acc_reduce_smem(acc, red, lane, false);
+    // totals by complex word (Acc order: su, P[6], sa, va[3], B[6], vc[3])
+    auto tot = [&](int w) { return cplx{red[2 * w][32], red[2 * w + 1][32]}; };
+    const cplx u_ac = aa == cc ? tot(0) - tot(1 + ac) : -tot(1 + ac);
+    cplx t = tot(11 + ac);
+    madd(t, n[aa], tot(8 + cc));
+    madd(t, n[cc], tot(17 + aa));
+    if (aa == cc) t = t + tot(7);
+    const cplx t_ac = t;
+    __syncwarp();
     const bool ok = lane >= 9 || (finite(u_ac) && finite(t_ac));
     if (!__all_sync(0xffffffffu, ok) && lane == 0) o.flags[4 * f] = 1;
     cplx bt = {0.0, 0.0};
@@ -973,20 +1030,48 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
 }
 
 // Diagonal blocks, b and P^{-1} of every member (as k_self_dyn<OUT_SYS>).
-__global__ void __launch_bounds__(128) k_self_multi(Geo g, FreqBatch fb, SysBatch o,
+__global__ void __launch_bounds__(128, 3) k_self_multi(Geo g, FreqBatch fb, SysBatch o,
                                                     const double* diag_base, int ntile, int n_mid,
                                                     int n_near) {
+  __shared__ double sred[4][kAccWords][33];
+  __shared__ FreqConst sfc[kMaxBatch];
+  for (int k = threadIdx.x; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
+    ((double*)sfc)[k] = ((const double*)fb.fc)[k];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= g.n_e) return;
   const long long N = 3LL * g.n_e;
+  const double xi = g.cx[j], yi = g.cy[j], zi = g.cz[j];
+  const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j];
+  const FreqConst& fc0 = fb.fc[0];
+  const double4* sp = g.self_pts + (size_t)j * kSelfQ;
+  double (*red)[33] = sred[threadIdx.x >> 5];
 #pragma unroll 1
   for (int f = 0; f < fb.nf; ++f) {
-    const Phys<true> ph{fb.fc[f]};
+    // 384-point self rule (quadrature.py:135-185), constants in the weights
     Acc<cplx> acc;
-    self_accumulate(g, ph, j, acc);
+    acc_zero(acc);
+    for (int q = lane; q < kSelfQ; q += 32) {
+      const double4 y = sp[q];
+      double dx = y.x - xi, dy = y.y - yi, dz = y.z - zi;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      const double ir = rsqrt(r2);
+      const double r = r2 * ir;
+      dx *= ir; dy *= ir; dz *= ir;
+      const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+      FreqConst fc;
+      fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
+      fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+      fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
+      fc.ratio = fc0.ratio;
+      const double wi = y.w * ir;
+      point_dynamic_scaled(acc, fc, kSeriesSwitch, r, ir, dx, dy, dz, dn, wi * fc0.inv4pimu,
+                           wi * ir * fc0.inv4pi);
+    }
+    acc_reduce_smem(acc, red, lane);
     cplx U[3][3], T[3][3];
-    acc_finalize(acc, g.nx[j], g.ny[j], g.nz[j], ph.i4pm(), ph.i4p(), U, T);
+    acc_finalize(acc, nx, ny, nz, 1.0, 1.0, U, T);
     for (int a = 0; a < 3; ++a)
       for (int b = 0; b < 3; ++b) T[a][b] = T[a][b] + cplx{diag_base[9 * j + 3 * a + b], 0.0};
     if (lane == 0) {

@@ -128,6 +128,18 @@ static inline cudaError_t upload_series(cudaStream_t st) {
   return e;
 }
 
+// Shared-memory loads the compiler may not hoist: the per-member constants
+// are read where they are used instead of occupying ~28 registers across
+// the quadrature loop (a runtime frequency index cannot use constant-bank
+// operands the way the single-frequency kernels do).
+__device__ __forceinline__ double lds_d(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+// (FreqConst is 8-byte aligned with a 120-byte stride: two scalar loads)
+__device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), lds_d(&p->im)}; }
+
 // Four radial brackets  phi*r, psi*r, dphi/dr*r^2, dpsi/dr*r^2.
 struct Brackets {
   cplx f0, f1, f2, f3;

@@ -81,7 +81,7 @@ struct MfArgs {
 #define EWB_MF_MINB 3
 #endif
 #ifndef EWB_MF_QUNROLL
-#define EWB_MF_QUNROLL 1
+#define EWB_MF_QUNROLL 3
 #endif
 constexpr int kMfQUnroll = EWB_MF_QUNROLL;
 template <int K, bool USE_U>
@@ -435,7 +435,10 @@ __global__ void k_pair_blocks(const double* x, long long P, const double* tri, l
 // point, CTA stages 32 triangles (field points, normal, weight*area, x_m)
 // in shared memory; blockIdx.y = frequency, blockIdx.z = triangle chunk.
 constexpr int kPkTile = 32;
-__global__ void __launch_bounds__(128) k_pair_reduce(const double* x, long long P,
+#ifndef EWB_PK_MINB
+#define EWB_PK_MINB 3
+#endif
+__global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* x, long long P,
                                                      const double* tri, long long M,
                                                      const cplx* xv, const FreqConst* fcs,
                                                      const double* b7, const double* w7,
@@ -443,9 +446,12 @@ __global__ void __launch_bounds__(128) k_pair_reduce(const double* x, long long 
   __shared__ double s_y[kPkTile][21];
   __shared__ double s_n[kPkTile][4];   // nx ny nz area
   __shared__ cplx s_x[kPkTile][3];
+  __shared__ FreqConst s_fc;
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int f = blockIdx.y;
-  const FreqConst fc = fcs[f];
+  if (threadIdx.x < sizeof(FreqConst) / 8)
+    ((double*)&s_fc)[threadIdx.x] = ((const double*)(fcs + f))[threadIdx.x];
+  __syncthreads();
   const long long m0 = (long long)blockIdx.z * chunk, m1 = min(M, m0 + chunk);
   const bool ok = p < P;
   const double xi = ok ? x[3 * p] : 0.0, yi = ok ? x[3 * p + 1] : 0.0, zi = ok ? x[3 * p + 2] : 0.0;
@@ -472,20 +478,30 @@ __global__ void __launch_bounds__(128) k_pair_reduce(const double* x, long long 
     if (!ok) continue;
     for (int jj = 0; jj < tc; ++jj) {
       const double nx = s_n[jj][0], ny = s_n[jj][1], nz = s_n[jj][2], ar = s_n[jj][3];
+      // 1/(4 pi mu), 1/(4 pi) folded into the weights; per-frequency
+      // constants read from shared memory where used (not held in registers)
+      const double cu = ar * s_fc.inv4pimu, ct = ar * s_fc.inv4pi;
       Acc<cplx> acc;
       acc_zero(acc);
 #pragma unroll 1
       for (int q = 0; q < 7; ++q) {
         double dx = s_y[jj][3 * q] - xi, dy = s_y[jj][3 * q + 1] - yi, dz = s_y[jj][3 * q + 2] - zi;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        double ir = rsqrt(r2);
-        double r = r2 * ir;
+        const double ir = rsqrt(r2);
+        const double r = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
-        double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-        point_dynamic(acc, fc, r, ir, dx, dy, dz, dn, w7r[q] * ar);
+        const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+        FreqConst fc;
+        fc.ks = lds_c(&s_fc.ks); fc.kp = lds_c(&s_fc.kp);
+        fc.iks = lds_c(&s_fc.iks); fc.ikp = lds_c(&s_fc.ikp);
+        fc.g2 = lds_c(&s_fc.g2); fc.ks_abs = lds_d(&s_fc.ks_abs);
+        fc.ratio = lds_d(&s_fc.ratio);
+        const double wi = w7r[q] * ir;
+        point_dynamic_scaled(acc, fc, lds_d(&s_fc.sw), r, ir, dx, dy, dz, dn, wi * cu,
+                             wi * ir * ct);
       }
-      acc_apply_U(acc, fc.inv4pimu, s_x[jj], yu);
-      acc_apply_T(acc, nx, ny, nz, fc.inv4pi, s_x[jj], yt);
+      acc_apply_U(acc, 1.0, s_x[jj], yu);
+      acc_apply_T(acc, nx, ny, nz, 1.0, s_x[jj], yt);
     }
   }
   if (!ok) return;

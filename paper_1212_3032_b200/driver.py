@@ -5,7 +5,7 @@
 every history when any solve fails, manifest) while every per-frequency
 array stays in HBM.  The device loop lives in :class:`DeviceSweep`:
 
-    per group of nb (default 8) consecutive k:
+    per group of nb (default 16) consecutive k:
             ewb_assemble_system_multi (assembly + BCs + b + P^{-1} of all nb
                                   frequencies in one pass over the element
                                   pairs; no T/U)
@@ -163,14 +163,14 @@ class DeviceSweep:
     def batch_size(self) -> int:
         """Frequencies assembled per pass over the element pairs.
 
-        ``assembly_batch`` (constructor) or ``EWB_ASSEMBLY_BATCH`` (default 8),
+        ``assembly_batch`` (constructor) or ``EWB_ASSEMBLY_BATCH`` (default 16),
         capped at 16 and by free HBM: the batch holds nb dense N x N systems
         (cfg2: 3.77 GB each) and may take at most half of the free memory."""
         import torch
 
         nb = self.assembly_batch
         if nb is None:
-            nb = int(os.environ.get("EWB_ASSEMBLY_BATCH", "8"))
+            nb = int(os.environ.get("EWB_ASSEMBLY_BATCH", "16"))
         nb = max(1, min(int(nb), 16, len(self.frequencies)))
         if nb > 1 and self.batch is None:
             free, _ = torch.cuda.mem_get_info()
