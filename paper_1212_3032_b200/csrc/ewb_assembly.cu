@@ -357,8 +357,9 @@ template <bool DYN, int OUT>
 __global__ void __launch_bounds__(128, 3) k_near(Geo g, Phys<DYN> ph, PairOut o, int n_near) {
   using S = typename Phys<DYN>::S;
   const int lane = threadIdx.x & 31;
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_near) return;
+  const int wp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wp >= n_near) return;
+  const int p = g.near_order[wp];
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
@@ -696,9 +697,9 @@ __device__ __forceinline__ Brackets brackets_phase_g(cplx ks, cplx kp, cplx iks,
   const cplx Gp = Ep * cplx{zp_im, -zp_re};
   Brackets o;
   o.f0 = Es + Fs - Fp;
-  o.f1 = Es + 3.0 * (Fs - Fp) - Ep;
-  o.f2 = Gs - 2.0 * Es + Ep + 3.0 * (Fp - Fs);
-  o.f3 = Gs - Gp + 4.0 * (Ep - Es) + 9.0 * (Fp - Fs);
+  o.f1 = Es + c_num.three * (Fs - Fp) - Ep;
+  o.f2 = Gs - c_num.two * Es + Ep + c_num.three * (Fp - Fs);
+  o.f3 = Gs - Gp + c_num.four * (Ep - Es) + c_num.nine * (Fp - Fs);
   return o;
 }
 
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
             Es = phase_factor(ks, rr);
             Ep = lds_c(&sfc[f].g2) * phase_factor(kp, rr);
           }
-          if (lds_d(&sfc[f].ks_abs) * rr < kFarSwitch) {
+          if (lds_d(&sfc[f].ks_abs) * rr < c_num.far_sw) {
             FreqConst fc = fc0;
             fc.ks = ks; fc.kp = kp; fc.g2 = lds_c(&sfc[f].g2);
             br = brackets_series_cold(fc, rr);
@@ -809,9 +810,9 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
           const cplx Phi = wu * br.f0;
           const cplx Psi = wu * br.f1;
           const cplx Aw = wt * (br.f2 - br.f1);
-          const cplx Bw = (2.0 * wt * dn) * (2.0 * br.f1 - br.f3);
+          const cplx Bw = (c_num.two * wt * dn) * (c_num.two * br.f1 - br.f3);
           const cplx dd = br.f2 - br.f3;
-          const cplx Cw = wt * (ratio * (dd - 2.0 * br.f1) - 2.0 * (dd - br.f1));
+          const cplx Cw = wt * (ratio * (dd - c_num.two * br.f1) - c_num.two * (dd - br.f1));
           acc_point(acc, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
         }
         // blocks (kernels.py:336-356): U symmetric, T = B + n va^T + vc n^T + sa I
@@ -894,7 +895,7 @@ __global__ void __launch_bounds__(128, 3) k_mid_multi(Geo g, FreqBatch fb, SysBa
     fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
     fc.ratio = fc0.ratio;
     const double wi = g.wmid[q] * ir;
-    point_dynamic_scaled(acc, fc, kFarSwitch, rr, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
+    point_dynamic_scaled(acc, fc, c_num.far_sw, rr, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
   }
   cplx U[3][3], T[3][3];
   acc_finalize(acc, nx, ny, nz, 1.0, 1.0, U, T);
@@ -962,8 +963,9 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
     ((double*)sfc)[k] = ((const double*)fb.fc)[k];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_near) return;
+  const int wp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wp >= n_near) return;
+  const int p = g.near_order[wp];
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
@@ -1003,7 +1005,7 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
       fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
       fc.ratio = fc0.ratio;
       const double wi = wq[q] * ir;
-      point_dynamic_scaled(acc, fc, kSeriesSwitch, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
+      point_dynamic_scaled(acc, fc, c_num.series_sw, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
     }
     acc_reduce_smem(acc, red, lane, false);
     // totals by complex word (Acc order: su, P[6], sa, va[3], B[6], vc[3])
@@ -1066,7 +1068,7 @@ __global__ void __launch_bounds__(128, 3) k_self_multi(Geo g, FreqBatch fb, SysB
       fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
       fc.ratio = fc0.ratio;
       const double wi = y.w * ir;
-      point_dynamic_scaled(acc, fc, kSeriesSwitch, r, ir, dx, dy, dz, dn, wi * fc0.inv4pimu,
+      point_dynamic_scaled(acc, fc, c_num.series_sw, r, ir, dx, dy, dz, dn, wi * fc0.inv4pimu,
                            wi * ir * fc0.inv4pi);
     }
     acc_reduce_smem(acc, red, lane);
@@ -1272,6 +1274,22 @@ cudaError_t setup_context(Context& c, const double* centroids, const double* nor
   if (err) return err;
   for (int L = 0; L <= kMaxNearLevel; ++L) c.n_near_lvl[L] = 0;
   for (int v : lv) c.n_near_lvl[v]++;
+  // launch order of the near-pair warps: deepest subdivision first, so the
+  // warps of a CTA carry similar work (a 1792- or 448-point pair next to
+  // 28-point pairs idles its CTA's other warps); outputs stay in CSR order
+  {
+    std::vector<int> order(c.n_near);
+    int pos = 0;
+    for (int L = kMaxNearLevel; L >= 1; --L)
+      for (int p = 0; p < c.n_near; ++p)
+        if (lv[p] == L) order[pos++] = p;
+    int* near_order = dalloc<int>(c, c.n_near + 1, err);
+    if (err) return err;
+    if (c.n_near)
+      err = cudaMemcpy(near_order, order.data(), (size_t)c.n_near * 4, cudaMemcpyHostToDevice);
+    if (err) return err;
+    g.near_order = near_order;
+  }
   c.n_tiles = (n + 31) / 32;
   c.rowsums = dalloc<double>(c, (size_t)9 * n, err);
   c.u_sta_self = dalloc<double>(c, (size_t)9 * n, err);

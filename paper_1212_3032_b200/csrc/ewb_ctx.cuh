@@ -35,6 +35,7 @@ struct Geo {
   const int *near_j;                 // column of each near pair
   const int *near_lvl;               // subdivision level 1..4
   const int *near_row;               // row of each near pair
+  const int *near_order;             // launch order of the near pairs (deepest level first)
   const int *mid_ptr;                // CSR by row of the mid (gauss7) pairs, n_e+1
   const int *mid_j;                  // column of each mid pair
   const int *mid_row;                // row of each mid pair

@@ -903,13 +903,28 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresA
 // already in flight.
 // ---------------------------------------------------------------------
 __device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& r1) {
-  r0 = (long long)blockIdx.x * n / gridDim.x;
-  r1 = (long long)(blockIdx.x + 1) * n / gridDim.x;
+#ifdef EWB_ROWS_REVERSED   // experiment: is a slow CTA slow because of its SM or its rows?
+  const long long b = gridDim.x - 1 - blockIdx.x;
+#else
+  const long long b = blockIdx.x;
+#endif
+  r0 = b * n / gridDim.x;
+  r1 = (b + 1) * n / gridDim.x;
 }
 
-template <int K, typename Epi>
+struct NoPre {
+  __device__ __forceinline__ void operator()(long long, int) const {}
+};
+#ifndef EWB_EPI_PREFETCH
+#define EWB_EPI_PREFETCH 12
+#endif
+// pre(row0, nrows) runs EWB_EPI_PREFETCH tiles before a block's epilogue:
+// the GMRES kernel prefetches the basis rows its dot products will read
+// into L1 there, so the epilogue (during which this CTA consumes no ring
+// stage) does not wait on L2.
+template <int K, typename Epi, typename Pre = NoPre>
 __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
-                            long long r0, long long r1, Epi&& epi) {
+                            long long r0, long long r1, Epi&& epi, Pre&& pre = Pre{}) {
   __shared__ cplx s_red[kSolveWarps][kRpt][K];
   __shared__ cplx s_sum[kRR][K];
   __shared__ int s_rel[kNS];  // warps done with each ring slot
@@ -961,6 +976,7 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
 #pragma unroll
       for (int k = 0; k < K; ++k) xn[k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
     }
+    if (t == max(0, ntile - 1 - EWB_EPI_PREFETCH)) pre(row0, nrows);
     const unsigned pos = R.pos + (unsigned)s;
     ring_wait(R, pos);
     if (col < tc) {
@@ -1401,14 +1417,26 @@ k_gmres_f(GmresArgs a) {
             if (tb <= j) s_dacc[tb] = s_dacc[tb] + sb;
           }
         }
+      }, [&](long long row0, int nr) {
+        // the same V entries the dot loop above reads, into L1 ahead of time
+        const int sub = threadIdx.x % kGrp;
+        if (sub < nr)
+          for (int ta = threadIdx.x / kGrp; ta <= j; ta += kSolveThreads / kGrp)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.V + (size_t)ta * n + row0 + sub));
       });
       ++n_mv;
       cplx* part = part_buf(dpar);
       for (int t = threadIdx.x; t <= j; t += blockDim.x)
         part[(size_t)blockIdx.x * kMaxDots + t] = s_dacc[t];
       EWB_PROBE(3);
-      if (a.probe && threadIdx.x == 0 && j < 100 && its == j)  // per-CTA matvec finish (cycle 0)
+      if (a.probe && threadIdx.x == 0 && j < 100 && its == j) {  // per-CTA matvec finish (cycle 0)
         a.probe[32768 + j * gridDim.x + blockIdx.x] = gtimer();
+        if (j == 0) {
+          unsigned sm;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+          a.probe[32768 + 100 * gridDim.x + blockIdx.x] = sm;   // which SM ran this CTA
+        }
+      }
       // Gram rows 1..j-1 (written in earlier steps) staged into the idle
       // ring while other CTAs finish their matvec
       cplx* gsm = scr;

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true
         dx *= ir; dy *= ir; dz *= ir;
         const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
         const double wi = wq * ir;
-        point_dynamic_scaled(acc, ph.fc, kFarSwitch, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
+        point_dynamic_scaled(acc, ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
       };
       if (tier == 0) {
 #pragma unroll kMfQUnroll
@@ -174,8 +174,9 @@ __global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true
 template <int K, bool USE_U>
 __global__ void __launch_bounds__(128) k_mf_near(Geo g, Phys<true> ph, MfArgs m, int n_near) {
   const int lane = threadIdx.x & 31;
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n_near) return;
+  const int wp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wp >= n_near) return;
+  const int p = g.near_order[wp];   // deepest level first (uniform CTAs)
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];

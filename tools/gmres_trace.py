@@ -61,3 +61,7 @@ if rows:
     order = np.argsort(-lag)
     print("slowest CTAs (mean lag us):", [(int(b), round(float(lag[b]), 2)) for b in order[:12]])
     print("fastest CTAs:", [(int(b), round(float(lag[b]), 2)) for b in order[-6:]])
+
+    sm = P[100 * G:101 * G]
+    print("smid of the 12 slowest CTAs:", [int(sm[b]) for b, _ in sorted(enumerate(lag), key=lambda t: -t[1])[:12]])
+    np.save(os.environ.get("TRACE_OUT", "/tmp/trace_lag.npy"), np.stack([np.arange(G), sm, lag]))
