@@ -157,6 +157,16 @@ int ewb_gemv_batched(const void* a_dev, const void* x_dev, void* y_dev, int64_t 
  * Process-wide; not thread-safe. */
 int ewb_set_solver_ctas(int32_t ctas);
 int32_t ewb_solver_ctas(void);
+/* Row balance of the solver kernels (no reference counterpart: a B200
+ * scheduling detail under gmres, linsolve.py:107).  Streams `a_dev` (n x n
+ * complex128) iters+1 times, measuring each solver CTA's matvec speed, and
+ * from then on splits rows in proportion to it (the slow SMs of a B200 under
+ * full-GPU contention finish ~5 % later with equal splits).  stats_host
+ * (double[4], may be NULL): per-CTA matvec time spread and mean in us, equal
+ * split then calibrated split.  ewb_reset_row_balance restores equal splits. */
+int ewb_calibrate_rows(const void* a_dev, int64_t n, int32_t iters, double* stats_host,
+                       void* stream);
+int ewb_reset_row_balance(void* stream);
 
 /* Whole restarted right-preconditioned GMRES solve in one cooperative launch
  * (linsolve.py:107-210).  pinv_dev may be NULL (no preconditioner); x_dev

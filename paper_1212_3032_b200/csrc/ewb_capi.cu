@@ -224,6 +224,18 @@ int ewb_set_solver_ctas(int32_t ctas) {
 
 int32_t ewb_solver_ctas(void) { return ewb::solver_grid_blocks(); }
 
+int ewb_calibrate_rows(const void* a, int64_t n, int32_t iters, double* stats, void* stream) {
+  if (!a || n < 1 || iters < 0) return fail(EWB_ERR_INVALID, "ewb_calibrate_rows: bad argument");
+  EWB_CUDA(ewb::calibrate_rows((const ewb::cplx*)a, n, iters, stats, S(stream)),
+           "ewb_calibrate_rows");
+  return EWB_OK;
+}
+
+int ewb_reset_row_balance(void* stream) {
+  EWB_CUDA(ewb::reset_row_balance(S(stream)), "ewb_reset_row_balance");
+  return EWB_OK;
+}
+
 // workspace layout: r, w, z (3n), V ((restart+1) n), H, partial
 int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart) {
   int64_t cpl = 16;

@@ -16,6 +16,7 @@
 // (not CGS) for iteration-count parity: step i of the orthogonalisation
 // fuses "w -= h_i v_i" with the partial dot of step i+1, one barrier each.
 #include <cooperative_groups.h>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "ewb_common.cuh"
@@ -902,14 +903,38 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresA
 // residuals, partial dot products) happens while the next stages are
 // already in flight.
 // ---------------------------------------------------------------------
+//
+// Row balance.  The matvec bandwidth of an SM under full-GPU contention is
+// not uniform: with equal row counts some SMs finish ~25 us (5 %) after the
+// others, every pass, and the grid barrier waits for them.  The slowness
+// follows the SM, not the rows (swapping the row chunks keeps the slow set:
+// tools/gmres_trace.py), and the CTA -> SM map of the solver launches is
+// fixed, so ewb_calibrate_rows measures each CTA's rows per second once and
+// the row split follows those speeds: CTA b owns [cumw[b] n, cumw[b+1] n).
+// Results stay bit-identical for a given split; splits from different
+// calibrations change only the grouping of the dot-product partials
+// (rounding level).  c_bal_g == 0 (default) or a different grid: equal split.
+constexpr int kMaxBalGrid = 512;
+__constant__ double c_cumw[kMaxBalGrid + 1];
+__constant__ int c_bal_g;
+
 __device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& r1) {
 #ifdef EWB_ROWS_REVERSED   // experiment: is a slow CTA slow because of its SM or its rows?
   const long long b = gridDim.x - 1 - blockIdx.x;
 #else
   const long long b = blockIdx.x;
 #endif
-  r0 = b * n / gridDim.x;
-  r1 = (b + 1) * n / gridDim.x;
+  if (c_bal_g == (int)gridDim.x) {
+    r0 = llrint(c_cumw[b] * (double)n);
+    r1 = llrint(c_cumw[b + 1] * (double)n);
+  } else {
+    r0 = b * n / gridDim.x;
+    r1 = (b + 1) * n / gridDim.x;
+  }
+}
+// host mirror of cta_rows' balanced split
+static inline long long host_split(const double* cumw, int b, long long n) {
+  return llrint(cumw[b] * (double)n);
 }
 
 struct NoPre {
@@ -1830,6 +1855,37 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gemv_tma(con
                  });
 }
 
+// Row-balance calibration: one matvec over the current split, all CTAs
+// released together (cooperative launch), per-CTA duration recorded.
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_calib(const cplx* A,
+                                                                         const cplx* x, cplx* y,
+                                                                         long long n,
+                                                                         unsigned long long* t) {
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  __shared__ uint64_t ring_bar[kNS];
+  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
+  ring_init(ring, true);
+  long long r0, r1;
+  cta_rows(n, r0, r1);
+  cg::this_grid().sync();
+  const unsigned long long t0 = gtimer();
+  // rate mark: time and rows done when the CTA passes half of its rows, i.e.
+  // while (nearly) every CTA is still streaming; a finish-time measure would
+  // credit the last CTAs with the bandwidth the early finishers released
+  long long done = 0;
+  const long long half = (r1 - r0) / 2;
+  matvec_rows<1>(ring, A, n, x, r0, r1, [&](long long row0, int nr, cplx (*sum)[1]) {
+    if (threadIdx.x < nr) y[row0 + threadIdx.x] = sum[threadIdx.x][0];
+    if (done < half && done + nr >= half && threadIdx.x == 0) {
+      t[gridDim.x + blockIdx.x] = gtimer() - t0;
+      t[2 * gridDim.x + blockIdx.x] = (unsigned long long)(done + nr);
+    }
+    done += nr;
+  });
+  __syncthreads();
+  if (threadIdx.x == 0) t[blockIdx.x] = gtimer() - t0;
+}
+
 // Plain batched GEMV y_b = A_b x_b (one launch, `batch` systems of size n).
 template <int RR>
 __global__ void __launch_bounds__(512) k_gemv_batched(const cplx* A, const cplx* x, cplx* y,
@@ -1955,6 +2011,88 @@ cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
   note_launch();
   return cudaLaunchCooperativeKernel((const void*)k_sem, dim3(G), dim3(kSolveThreads), params,
                                      kRingBytes, s);
+}
+
+#ifndef EWB_BAL_DAMP
+#define EWB_BAL_DAMP 0.7
+#endif
+constexpr double kBalDamp = EWB_BAL_DAMP;
+
+cudaError_t calibrate_rows(const cplx* A, long long n, int iters, double* stats,
+                           cudaStream_t s) {
+  const int G = solver_grid_blocks();
+  if (G > kMaxBalGrid || n < 2LL * G) return cudaErrorInvalidValue;
+  cudaFuncSetAttribute((const void*)k_calib, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kRingBytes);
+  cplx *x = nullptr, *y = nullptr;
+  unsigned long long* t = nullptr;
+  cudaError_t e = cudaMalloc(&x, sizeof(cplx) * n);
+  if (!e) e = cudaMalloc(&y, sizeof(cplx) * n);
+  if (!e) e = cudaMalloc(&t, sizeof(unsigned long long) * 3 * G);
+  if (!e) e = cudaMemsetAsync(x, 0, sizeof(cplx) * n, s);
+  std::vector<double> cumw(G + 1), speed(G, 0.0);
+  std::vector<unsigned long long> th(3 * G);
+  for (int b = 0; b <= G; ++b) cumw[b] = (double)b / G;
+  int zero = 0;
+  if (!e) e = cudaMemcpyToSymbolAsync(c_bal_g, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+  void* params[] = {(void*)&A, (void*)&x, (void*)&y, (void*)&n, (void*)&t};
+  double spread0 = 0.0, spread1 = 0.0, mean0 = 0.0, mean1 = 0.0;
+  for (int it = 0; !e && it <= iters; ++it) {
+    // two launches per split: the first warms up, the second is measured
+    for (int rep = 0; !e && rep < 2; ++rep) {
+      note_launch();
+      e = cudaLaunchCooperativeKernel((const void*)k_calib, dim3(G), dim3(kSolveThreads), params,
+                                      kRingBytes, s);
+    }
+    if (!e) e = cudaMemcpyAsync(th.data(), t, sizeof(unsigned long long) * 3 * G,
+                                cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) break;
+    double tmax = 0.0, tmin = 1e30, tsum = 0.0;
+    for (int b = 0; b < G; ++b) {
+      const double tb = (double)th[b];
+      tmax = tb > tmax ? tb : tmax;
+      tmin = tb < tmin ? tb : tmin;
+      tsum += tb;
+    }
+    if (it == 0) { spread0 = tmax - tmin; mean0 = tsum / G; }
+    spread1 = tmax - tmin;
+    mean1 = tsum / G;
+    if (it == iters) break;   // last pass only measures the final split
+    // damped fixed-point step on the finish times: a CTA that finishes
+    // later than the mean gives rows away in proportion (the rates depend
+    // on the split through the contention pattern, so no one-shot solve)
+    const double tmean = tsum / G;
+    double fsum = 0.0;
+    for (int b = 0; b < G; ++b) {
+      const double f = cumw[b + 1] - cumw[b];
+      speed[b] = f * (1.0 + kBalDamp * (tmean - (double)th[b]) / tmean);
+      fsum += speed[b];
+    }
+    double acc = 0.0;
+    for (int b = 0; b < G; ++b) {
+      cumw[b] = acc;
+      acc += speed[b] / fsum;
+    }
+    cumw[G] = 1.0;
+    e = cudaMemcpyToSymbolAsync(c_cumw, cumw.data(), sizeof(double) * (G + 1), 0,
+                                cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyToSymbolAsync(c_bal_g, &G, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+  }
+  if (stats) {
+    stats[0] = spread0 * 1e-3; stats[1] = mean0 * 1e-3;   // us, equal split
+    stats[2] = spread1 * 1e-3; stats[3] = mean1 * 1e-3;   // us, calibrated split
+  }
+  cudaStreamSynchronize(s);
+  cudaFree(x);
+  cudaFree(y);
+  cudaFree(t);
+  return e;
+}
+
+cudaError_t reset_row_balance(cudaStream_t s) {
+  int zero = 0;
+  return cudaMemcpyToSymbolAsync(c_bal_g, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s);
 }
 
 cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long n, int batch,

@@ -69,6 +69,11 @@ int solver_grid_blocks();   // CTAs the solver launches use (<= max, see set_sol
 void set_solver_ctas(int ctas);
 cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s);
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s);
+// Row balance (see cta_rows): measure per-CTA matvec speed on A (n x n) and
+// split rows accordingly for every later solver launch; stats (us): spread
+// and mean of the per-CTA matvec time, equal split then calibrated split.
+cudaError_t calibrate_rows(const cplx* A, long long n, int iters, double* stats, cudaStream_t s);
+cudaError_t reset_row_balance(cudaStream_t s);
 cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long n, int batch,
                                 cudaStream_t s);
 

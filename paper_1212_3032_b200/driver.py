@@ -306,6 +306,14 @@ class DeviceSweep:
             except Exception as exc:
                 omega = complex(self.omegas[ks[0]])
                 raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
+            if (os.environ.get("EWB_ROW_BALANCE") == "1" and self.n >= 4096
+                    and not getattr(self, "_balanced", False)):
+                # opt-in: split the solver rows by measured per-SM speed
+                # (measured slower on cfg2; kept as an experiment)
+                from .linsolve import calibrate_row_balance
+
+                calibrate_row_balance(members[0].A)
+                self._balanced = True
             for i, k, sysm in zip(group, ks, members):
                 omega = complex(self.omegas[k])
                 try:

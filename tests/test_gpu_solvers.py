@@ -324,3 +324,41 @@ def test_solver_cta_budget_same_result(cuda):
     assert rel_max(x1.cpu().numpy(), x2.cpu().numpy()) <= 1e-6
     with pytest.raises(ValueError):
         _lib.check(lib.ewb_set_solver_ctas(-1))
+
+
+def test_row_balance_split_same_solution(cuda, monkeypatch):
+    """ewb_calibrate_rows: rows split by measured per-SM speed; the solve is
+    bit-reproducible for a given split and agrees with the equal split to
+    rounding (only the grouping of the dot-product partials changes)."""
+    import torch
+
+    from paper_1212_3032_b200.linsolve import (calibrate_row_balance, gmres_device,
+                                               reset_row_balance)
+
+    monkeypatch.delenv("EWB_ROW_BALANCE", raising=False)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    n = 6000
+    a = torch.randn((n, n), dtype=torch.complex128, device="cuda", generator=gen)
+    a.diagonal().add_(3 * n ** 0.5)
+    b = torch.randn(n, dtype=torch.complex128, device="cuda", generator=gen)
+
+    def solve():
+        x = torch.zeros_like(b)
+        st = gmres_device(a, b, x, False, 1e-10, 50, 200, None)
+        return x.cpu().numpy(), st.iterations
+
+    try:
+        reset_row_balance()
+        x0, i0 = solve()
+        stats = calibrate_row_balance(a, force=True)
+        assert stats is not None and stats[1] > 0 and stats[3] > 0
+        x1, i1 = solve()
+        x1b, _ = solve()
+        reset_row_balance()
+        x2, _ = solve()
+    finally:
+        reset_row_balance()
+    assert np.array_equal(x1, x1b) and np.array_equal(x0, x2)
+    assert i0 == i1
+    assert rel_max(x1, x0) <= 1e-12

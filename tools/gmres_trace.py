@@ -27,6 +27,10 @@ A.diagonal().add_(0.5 * n ** 0.5)
 b = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
 x = torch.zeros(n, dtype=torch.complex128, device="cuda")
 ws = _Workspace()
+if os.environ.get("TRACE_BALANCE"):
+    from paper_1212_3032_b200.linsolve import calibrate_row_balance
+
+    print("row balance stats (us):", calibrate_row_balance(A))
 gmres_device(A, b, x, False, 1e-15, 60, m, None, ws=ws)
 probe.zero_()
 x.zero_()
