@@ -176,6 +176,9 @@ struct Ring {
 // stay in L2 across passes.  Measured (n = 15360): 2 rows lift a standalone
 // GEMV from 6.76 to 6.88 TB/s but slow the cfg2 sweep from 4.02 to 4.09 s
 // (the pinned rows crowd the Krylov basis out of L2), so it is off.
+#ifndef EWB_L2_PREFETCH_TILES
+#define EWB_L2_PREFETCH_TILES 0
+#endif
 #ifndef EWB_PIN_ROWS
 #define EWB_PIN_ROWS 0
 #endif
@@ -1450,6 +1453,23 @@ k_gmres_f(GmresArgs a) {
             asm volatile("prefetch.global.L1 [%0];" ::"l"(a.V + (size_t)ta * n + row0 + sub));
       });
       ++n_mv;
+#if EWB_L2_PREFETCH_TILES > 0
+      {  // the next pass's first tiles of this CTA's rows into L2 while the
+         // grid waits at S1 and reduces (HBM otherwise idle)
+        const int rows = (int)(k1 - k0), nblk = (rows + kRR - 1) / kRR;
+        const int nr = rows / nblk;
+        const int ntile = (int)((n + kTC - 1) / kTC);
+        const int nt = min(EWB_L2_PREFETCH_TILES, ntile);
+        for (int idx = threadIdx.x; idx < nr * nt; idx += blockDim.x) {
+          const int r = idx % nr, t = idx / nr;
+          const long long c0 = (long long)t * kTC;
+          const uint32_t bytes = (uint32_t)(min((long long)kTC, n - c0) * 16);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.A + (k0 + r) * n + c0),
+                       "r"(bytes)
+                       : "memory");
+        }
+      }
+#endif
       cplx* part = part_buf(dpar);
       for (int t = threadIdx.x; t <= j; t += blockDim.x)
         part[(size_t)blockIdx.x * kMaxDots + t] = s_dacc[t];

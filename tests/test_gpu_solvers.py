@@ -362,3 +362,66 @@ def test_row_balance_split_same_solution(cuda, monkeypatch):
     assert np.array_equal(x1, x1b) and np.array_equal(x0, x2)
     assert i0 == i1
     assert rel_max(x1, x0) <= 1e-12
+
+
+def test_cfg1_stepwise_iterations_with_batched_assembly(cuda):
+    """As the stepwise test, with every system from the 16-member
+    multi-frequency assembly the sweep uses (phase recurrence)."""
+    import torch
+
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.linsolve import gmres_device, sem_device
+    from paper_1212_3032_b200.transform import eta_from_kappa, forward_mft, frequency_grid
+    from paper_1212_3032_b200.workloads import cfg1
+
+    g = golden("cfg1_solutions")
+    cfg = cfg1()
+    asm = Assembler(cfg.mesh, cfg.material)
+    eta = eta_from_kappa(cfg.kappa, cfg.period)
+    om = frequency_grid(cfg.period, cfg.n_omega, eta)
+    spectra = np.stack([forward_mft(s, cfg.period, cfg.n_omega, eta).values for s in cfg.signals])
+    sig = cfg.bcs.flat_signal()
+    xref = g["x"]
+    x = torch.zeros(cfg.mesh.n_dofs, dtype=torch.complex128, device="cuda")
+    diffs = []
+    batch = None
+    for k0 in range(0, len(om), 16):
+        ks = list(range(k0, min(len(om), k0 + 16)))
+        P = np.stack([spectra[sig, k] for k in ks])
+        batch = asm.assemble_system_multi([om[k] for k in ks], cfg.bcs, P, out=batch)
+        for f, k in enumerate(ks):
+            sysm = batch.member(f)
+            if k:
+                hist = torch.from_numpy(xref[max(0, k - 2):k][::-1].copy()).cuda()
+                sem_device(sysm.A, sysm.b, hist, 1e-10, x)
+            st = gmres_device(sysm.A, sysm.b, x, k > 0, cfg.tol, cfg.restart, cfg.maxiter,
+                              sysm.pinv)
+            diffs.append(st.iterations - int(g["its"][k]))
+            assert rel_max(x.cpu().numpy(), xref[k]) <= 1e-6
+    assert max(abs(d) for d in diffs) <= 1, diffs
+
+
+def test_device_sweep_strided_frequencies_sem_off(cuda):
+    """A rank's round-robin share (k = 1, 3, 5, ...: batches equispaced with
+    step 2 dw) solved through the batched path equals per-frequency solves."""
+    import dataclasses
+
+    import torch
+
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.linsolve import gmres_device
+    from paper_1212_3032_b200.workloads import cfg1
+
+    cfg = dataclasses.replace(cfg1(), sem_enabled=False)
+    ks = list(range(1, 40, 2))
+    ds = DeviceSweep(cfg, frequencies=ks)
+    stats = ds.run()
+    ref = DeviceSweep(cfg, assembler=ds.asm, frequencies=ks, assembly_batch=1)
+    ref_stats = ref.run()
+    for k in ks:
+        assert abs(stats[k].iterations - ref_stats[k].iterations) <= 1
+        assert rel_max(ds.sol[k].cpu().numpy(), ref.sol[k].cpu().numpy()) <= 1e-8
+    x = torch.zeros_like(ds.sol[ks[3]])
+    sysm = ds.asm.assemble_system(ds.omegas[ks[3]], cfg.bcs, ds.P[ks[3]])
+    gmres_device(sysm.A, sysm.b, x, False, cfg.tol, cfg.restart, cfg.maxiter, sysm.pinv)
+    assert rel_max(ds.sol[ks[3]].cpu().numpy(), x.cpu().numpy()) <= 1e-8
