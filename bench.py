@@ -326,6 +326,18 @@ def run_ours_sweep(args, rank, world, local_rank):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)", "traffic": None,
                 "algorithmic_bytes_per_pass": bytes_per_pass,
                 "passes_per_sweep": matvecs / max(args.steps, 1)}
+    # DRAM traffic of the dominant kernels from the committed ncu capture
+    tr_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
+                           "traffic.json")
+    if os.path.exists(tr_path):
+        with open(tr_path) as fh:
+            tr = json.load(fh)
+        rl_solve["traffic"] = tr["k_gmres_f"]["bytes_per_pass"]
+        rl_solve["traffic_unit"] = "bytes per pass over A (ncu dram read+write)"
+        rl_solve["traffic_source"] = tr["k_gmres_f"]["source"]
+        rl_asm["traffic"] = tr["k_far_multi"]["bytes_per_freq"]
+        rl_asm["traffic_unit"] = "bytes per frequency (ncu dram read+write of k_far_multi)"
+        rl_asm["traffic_source"] = tr["k_far_multi"]["source"]
     asm_share = asm_ms / max(asm_ms + solve_ms, 1e-9)
     # the same multi-frequency assembly outside the sweep (clocks not pulled
     # down by the power-capped GMRES phase): one batch of mid-sweep members
