@@ -207,8 +207,10 @@ class DeviceSweep:
                 hist = self.hist[:n_hist] if use_sem else None
                 b, Y = op.rhs_and_apply(self.P[k], hist, want_pinv=True)
                 pc = BlockDiagPreconditioner(op.pinv)
-                x0 = sem_operator(op, b, hist, 1e-10, Y=Y) if use_sem else None
-                x, st = gmres_operator(op, b, x0, cfg.tol, cfg.restart, cfg.maxiter, pc)
+                x0, ax0 = (sem_operator(op, b, hist, 1e-10, Y=Y, return_ax0=True) if use_sem
+                           else (None, None))
+                x, st = gmres_operator(op, b, x0, cfg.tol, cfg.restart, cfg.maxiter, pc,
+                                       ax0=ax0)
                 nf, sg = ctypes.c_int32(), ctypes.c_int32()
                 _lib.check(self.asm._lib.ewb_ctx_flags(self.asm.ctx, ctypes.byref(nf),
                                                        ctypes.byref(sg), _lib.stream_handle()))
@@ -280,7 +282,7 @@ class DeviceSweep:
                 e_a = torch.cuda.Event(enable_timing=True)
                 e_b = torch.cuda.Event(enable_timing=True)
                 e_a.record()
-                if len(group) > 1:
+                if complex(self.omegas[ks[0]]) != 0:
                     self.batch = asm.assemble_system_multi(
                         [self.omegas[k] for k in ks], cfg.bcs, self.P[ks[0]:ks[-1] + 1]
                         if ks == list(range(ks[0], ks[-1] + 1)) else self.P[ks],

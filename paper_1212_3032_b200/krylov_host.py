@@ -24,7 +24,10 @@ def _torch():
     return torch
 
 
-def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond):
+def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond, ax0=None):
+    """``ax0``: A x0 when the caller already has it (SEM's (A X) s), so the
+    initial residual costs no operator application (the dense path's ax0,
+    DESIGN.md §8); otherwise r0 = b - A x0 as linsolve.py:144."""
     from .linsolve import SolveStats
 
     torch = _torch()
@@ -36,7 +39,10 @@ def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond):
         return torch.zeros(n, dtype=torch.complex128, device="cuda"), st
     x = (torch.zeros(n, dtype=torch.complex128, device="cuda") if x0 is None
          else x0.to(device="cuda", dtype=torch.complex128).clone())
-    r = b - apply_a(x) if bool((x != 0).any()) else b.clone()
+    if ax0 is not None and x0 is not None:
+        r = b - ax0
+    else:
+        r = b - apply_a(x) if bool((x != 0).any()) else b.clone()
     rnorm = float(torch.linalg.vector_norm(r))
     res = rnorm / nb
     st.init_residual = res
@@ -104,8 +110,9 @@ def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond):
     return x, st
 
 
-def sem_operator(apply_a, b, xcols, rank_tol, Y=None):
-    """SEM guess for an operator; Y = A X computed in one multi-vector pass."""
+def sem_operator(apply_a, b, xcols, rank_tol, Y=None, return_ax0=False):
+    """SEM guess for an operator; Y = A X computed in one multi-vector pass.
+    With ``return_ax0`` also returns A x0 = Y s (no extra application)."""
     torch = _torch()
     K = xcols.shape[0]
     if Y is None:
@@ -121,8 +128,9 @@ def sem_operator(apply_a, b, xcols, rank_tol, Y=None):
         good = dg >= rank_tol * dg.max() if dg.max() > 0 else dg > 0
         if good.all():
             s = torch.linalg.solve(r, q.conj().T @ b)
-            return (xcols[keep].T @ s).to(torch.complex128)
+            x0 = (xcols[keep].T @ s).to(torch.complex128)
+            return (x0, (Yt[:, keep] @ s).to(torch.complex128)) if return_ax0 else x0
         keep = keep[good]
         if keep.size == 0:
             break
-    return xcols[0].clone()
+    return (xcols[0].clone(), Y[0].clone()) if return_ax0 else xcols[0].clone()

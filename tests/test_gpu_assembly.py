@@ -276,3 +276,28 @@ def test_multi_frequency_is_bit_deterministic_and_validates(cfg1_asm):
         cfg1_asm.assemble_system_multi(om[:17], bcs, np.ones((17, cfg1_asm.n), complex))
     with pytest.raises(ValueError, match=r"\(nf, N\)"):
         cfg1_asm.assemble_system_multi(om[1:3], bcs, P)
+
+
+def test_non_finite_entries_raise_per_member(cuda):
+    """A duplicated element puts a quadrature node on a collocation point
+    (r = 0; the reference's pair_geometry raises there, kernels.py:196-203):
+    every member of a batch flags non-finite entries -> FloatingPointError,
+    and the sweep reports the first frequency (driver.py:141-145)."""
+    import dataclasses
+
+    from paper_1212_3032_b200 import Assembler, SweepError, generate_box_mesh, run_sweep
+    from paper_1212_3032_b200.mesh import TriangleMesh
+    from paper_1212_3032_b200.workloads import cfg1
+
+    m = generate_box_mesh((1, 1, 1), (2, 2, 2))
+    tris = np.vstack([m.triangles, m.triangles[:1]])
+    tags = np.concatenate([m.region_tag, m.region_tag[:1]])
+    mesh = TriangleMesh(m.vertices, tris, tags, closed=False)
+    asm = Assembler(mesh, _unit())
+    bcs = _cfg1_bcs(mesh)
+    P = np.ones((3, mesh.n_dofs), complex)
+    with pytest.raises(FloatingPointError, match="non-finite"):
+        asm.assemble_system_multi([1.0 - 0.2j, 1.5 - 0.2j, 2.0 - 0.2j], bcs, P)
+    cfg = dataclasses.replace(cfg1(), mesh=mesh, bcs=bcs, probes=[], allow_floating=True)
+    with pytest.raises(SweepError, match="frequency index 0"):
+        run_sweep(cfg)
