@@ -815,42 +815,35 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
           const cplx Cw = wt * (ratio * (dd - c_num.two * br.f1) - c_num.two * (dd - br.f1));
           acc_point(acc, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
         }
-        // blocks (kernels.py:336-356): U symmetric, T = B + n va^T + vc n^T + sa I
-        cplx U[3][3], T[3][3];
+        // blocks (kernels.py:336-356) entry by entry straight into A and b:
+        // U_ac = su d_ac - P_ac, T_ac = B_ac + n_a va_c + vc_a n_c + sa d_ac;
+        // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
+        // Dirichlet column A = -U, b -= T p
         const double n[3] = {nx, ny, nz};
         const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
         unsigned ex = 0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            if (b >= a) U[a][b] = a == b ? acc.su - acc.P[sym[a][b]] : -acc.P[sym[a][b]];
-            else U[a][b] = U[b][a];
-            cplx tv = acc.B[sym[a][b]];
-            madd(tv, n[a], acc.va[b]);
-            madd(tv, n[b], acc.vc[a]);
-            if (a == b) tv = tv + acc.sa;
-            T[a][b] = tv;
-            ex = max(ex, max(expo(U[a][b]), expo(tv)));
-          }
-        if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
-        // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
-        // Dirichlet column A = -U, b -= T p
         cplx* Af = o.A + (size_t)f * N * N;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
+            const cplx u = a == c ? acc.su - acc.P[sym[a][c]] : -acc.P[sym[a][c]];
+            cplx tv = acc.B[sym[a][c]];
+            madd(tv, n[a], acc.va[c]);
+            madd(tv, n[c], acc.vc[a]);
+            if (a == c) tv = tv + acc.sa;
+            ex = max(ex, max(expo(u), expo(tv)));
             if (kbits & (1u << c)) {
-              row[c] = -U[a][c];
-              bc[a] = bc[a] - T[a][c] * pv[c];
+              row[c] = -u;
+              bc[a] = bc[a] - tv * pv[c];
             } else {
-              row[c] = T[a][c];
-              bc[a] = bc[a] + U[a][c] * pv[c];
+              row[c] = tv;
+              bc[a] = bc[a] + u * pv[c];
             }
           }
         }
+        if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
       }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {

@@ -17,7 +17,7 @@
 #include <cuda_runtime.h>
 
 #ifndef EWB_SERIES_TERMS
-#define EWB_SERIES_TERMS 20
+#define EWB_SERIES_TERMS 16
 #endif
 
 namespace ewb {
