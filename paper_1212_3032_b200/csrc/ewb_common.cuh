@@ -435,6 +435,37 @@ __device__ __forceinline__ void point_dynamic_scaled(Acc<cplx>& A, const FreqCon
   acc_point(A, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
 }
 
+// One dynamic point applied straight to a vector (T only, one vector: the
+// matrix-free GMRES product).  With s = d.v and nv = n.v the point's share of
+// T v (kernels.py:345-356) is
+//   (T v)_a += e v_a + n_a h + d_a g,   e = Aw dn, h = Aw s, g = Bw s + Cw nv
+// (~44 DP instead of 40 accumulator updates plus a third of a block apply),
+// and no 20-word accumulator is live: far fewer registers per thread.
+__device__ __forceinline__ void point_apply_T(cplx y[3], const FreqConst& fc, double sw, double r,
+                                              double ir, double dx, double dy, double dz,
+                                              double dn, double wt, const cplx v[3], cplx nv,
+                                              double nx, double ny, double nz) {
+  const Brackets f =
+      fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
+  const cplx Aw = wt * (f.f2 - f.f1);
+  const cplx Bw = (c_num.two * wt * dn) * (c_num.two * f.f1 - f.f3);
+  const cplx dd = f.f2 - f.f3;
+  const cplx Cw = wt * (fc.ratio * (dd - c_num.two * f.f1) - c_num.two * (dd - f.f1));
+  cplx sv = dx * v[0];
+  axpy(sv, dy, v[1]);
+  axpy(sv, dz, v[2]);
+  const cplx e = dn * Aw, h = Aw * sv;
+  cplx gg = Bw * sv;
+  cfma(gg, Cw, nv);
+  const double n[3] = {nx, ny, nz}, d[3] = {dx, dy, dz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cfma(y[a], e, v[a]);
+    axpy(y[a], n[a], h);
+    axpy(y[a], d[a], gg);
+  }
+}
+
 // One static point (Kelvin), kernels.py:141-152 + 327-357.
 __device__ __forceinline__ void point_static(Acc<double>& A, const StaticConst& sc, double ir,
                                              double dx, double dy, double dz, double dn,

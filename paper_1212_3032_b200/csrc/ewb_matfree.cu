@@ -84,8 +84,13 @@ struct MfArgs {
 #define EWB_MF_QUNROLL 3
 #endif
 constexpr int kMfQUnroll = EWB_MF_QUNROLL;
+// the accumulator-free K = 1 product needs ~130 registers instead of 168
+#ifndef EWB_MF1_MINB
+#define EWB_MF1_MINB 4
+#endif
 template <int K, bool USE_U>
-__global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
+__global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_MF_MINB)
+    k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
   __shared__ double s_geo[kMfTile][8];        // cx cy cz diam nx ny nz area
   __shared__ double s_y[kMfTile][30];         // 3 far + 7 mid points
   __shared__ cplx s_vt[kMfTile][K][3];
@@ -137,6 +142,31 @@ __global__ void __launch_bounds__(128, EWB_MF_MINB) k_mf_farmid(Geo g, Phys<true
       const double nx = s_geo[jj][4], ny = s_geo[jj][5], nz = s_geo[jj][6], ar = s_geo[jj][7];
       // 1/(4 pi mu) and 1/(4 pi) ride in the weights; series out of line
       const double cu = ar * ph.fc.inv4pimu, ct = ar * ph.fc.inv4pi;
+      if constexpr (K == 1 && !USE_U) {
+        // GMRES product: each point applied straight to v (no accumulator)
+        const cplx v[3] = {s_vt[jj][0][0], s_vt[jj][0][1], s_vt[jj][0][2]};
+        cplx nv = nx * v[0];
+        axpy(nv, ny, v[1]);
+        axpy(nv, nz, v[2]);
+        auto point1 = [&](const double* yq, double wq) {
+          double dx = yq[0] - xi, dy = yq[1] - yi, dz = yq[2] - zi;
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const double ir = rsqrt(r2);
+          const double r = r2 * ir;
+          dx *= ir; dy *= ir; dz *= ir;
+          const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+          point_apply_T(y[0], ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn, wq * ir * ir * ct, v,
+                        nv, nx, ny, nz);
+        };
+        if (tier == 0) {
+#pragma unroll kMfQUnroll
+          for (int q = 0; q < 3; ++q) point1(&s_y[jj][3 * q], g.wfar[q]);
+        } else {
+#pragma unroll 1
+          for (int q = 0; q < 7; ++q) point1(&s_y[jj][9 + 3 * q], g.wmid[q]);
+        }
+        continue;
+      }
       Acc<cplx> acc;
       acc_zero(acc);
       auto point = [&](const double* yq, double wq) {
