@@ -466,6 +466,38 @@ __device__ __forceinline__ void point_apply_T(cplx y[3], const FreqConst& fc, do
   }
 }
 
+// One dynamic point applied straight to one vector for both operators (the
+// cfg3 fused reduction y_U = U x, y_T = T x): with s = d.x,
+//   (U x)_a += Phi x_a - Psi d_a s,   (T x)_a as in point_apply_T.
+__device__ __forceinline__ void point_apply_UT(cplx yu[3], cplx yt[3], const FreqConst& fc,
+                                               double sw, double r, double ir, double dx,
+                                               double dy, double dz, double dn, double wu,
+                                               double wt, const cplx v[3], cplx nv, double nx,
+                                               double ny, double nz) {
+  const Brackets f =
+      fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
+  const cplx Phi = wu * f.f0, Psi = wu * f.f1;
+  const cplx Aw = wt * (f.f2 - f.f1);
+  const cplx Bw = (c_num.two * wt * dn) * (c_num.two * f.f1 - f.f3);
+  const cplx dd = f.f2 - f.f3;
+  const cplx Cw = wt * (fc.ratio * (dd - c_num.two * f.f1) - c_num.two * (dd - f.f1));
+  cplx sv = dx * v[0];
+  axpy(sv, dy, v[1]);
+  axpy(sv, dz, v[2]);
+  const cplx e = dn * Aw, h = Aw * sv, ps = Psi * sv;
+  cplx gg = Bw * sv;
+  cfma(gg, Cw, nv);
+  const double n[3] = {nx, ny, nz}, d[3] = {dx, dy, dz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cfma(yt[a], e, v[a]);
+    axpy(yt[a], n[a], h);
+    axpy(yt[a], d[a], gg);
+    cfma(yu[a], Phi, v[a]);
+    axpy(yu[a], -d[a], ps);
+  }
+}
+
 // One static point (Kelvin), kernels.py:141-152 + 327-357.
 __device__ __forceinline__ void point_static(Acc<double>& A, const StaticConst& sc, double ir,
                                              double dx, double dy, double dz, double dn,

@@ -512,6 +512,33 @@ __global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* 
       // 1/(4 pi mu), 1/(4 pi) folded into the weights; per-frequency
       // constants read from shared memory where used (not held in registers)
       const double cu = ar * s_fc.inv4pimu, ct = ar * s_fc.inv4pi;
+#ifndef EWB_PK_ACC
+      // points applied straight to x_m (no 20-word accumulator)
+      {
+        const cplx v[3] = {s_x[jj][0], s_x[jj][1], s_x[jj][2]};
+        cplx nv = nx * v[0];
+        axpy(nv, ny, v[1]);
+        axpy(nv, nz, v[2]);
+#pragma unroll 1
+        for (int q = 0; q < 7; ++q) {
+          double dx = s_y[jj][3 * q] - xi, dy = s_y[jj][3 * q + 1] - yi, dz = s_y[jj][3 * q + 2] - zi;
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const double ir = rsqrt(r2);
+          const double r = r2 * ir;
+          dx *= ir; dy *= ir; dz *= ir;
+          const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+          FreqConst fc;
+          fc.ks = lds_c(&s_fc.ks); fc.kp = lds_c(&s_fc.kp);
+          fc.iks = lds_c(&s_fc.iks); fc.ikp = lds_c(&s_fc.ikp);
+          fc.g2 = lds_c(&s_fc.g2); fc.ks_abs = lds_d(&s_fc.ks_abs);
+          fc.ratio = lds_d(&s_fc.ratio);
+          const double wi = w7r[q] * ir;
+          point_apply_UT(yu, yt, fc, lds_d(&s_fc.sw), r, ir, dx, dy, dz, dn, wi * cu,
+                         wi * ir * ct, v, nv, nx, ny, nz);
+        }
+        continue;
+      }
+#endif
       Acc<cplx> acc;
       acc_zero(acc);
 #pragma unroll 1
