@@ -156,6 +156,62 @@ def run_cfg4(args, rank, world, local_rank):
                           gmres_passes=passes, gmres_solve_gbs=solve_gbs)
         del A, b, y
         torch.cuda.empty_cache()
+    # cfg4-ii: assembled BEM operators, 8 consecutive frequencies from one
+    # multi-frequency assembly pass, the same batched GEMV + per-system GMRES
+    # (restart 50, tol 1e-8, the sweep's block preconditioner)
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.transform import eta_from_kappa, frequency_grid
+    from paper_1212_3032_b200.workloads import cfg4_assembled
+
+    assembled = {}
+    for name, cfg in cfg4_assembled():
+        asm = Assembler(cfg.mesh, cfg.material)
+        om = frequency_grid(cfg.period, cfg.n_omega, eta_from_kappa(cfg.kappa, cfg.period))
+        n = asm.n
+        ks = list(range(40, 40 + batch))
+        gP = torch.Generator(device="cuda")
+        gP.manual_seed(n)
+        P = torch.complex(torch.randn((batch, n), generator=gP, device="cuda", dtype=torch.float64),
+                          torch.randn((batch, n), generator=gP, device="cuda", dtype=torch.float64))
+        sb = asm.assemble_system_multi([om[k] for k in ks], cfg.bcs, P)
+        xb = sb.b.clone()
+        y = torch.empty_like(xb)
+
+        def step():
+            _lib.check(lib.ewb_gemv_batched(_lib.ptr(sb.A), _lib.ptr(xb), _lib.ptr(y), n, batch,
+                                            _lib.stream_handle()))
+
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        gbs = batch * (16.0 * n * n + 32.0 * n) / (ms * 1e-3) / 1e9
+        ref = sb.A[batch - 1] @ xb[batch - 1]
+        err = float((y[batch - 1] - ref).abs().max() / ref.abs().max())
+        ws = _Workspace()
+        its, t_solve, passes = [], 0.0, 0
+        for s_ in range(batch):
+            xs = torch.zeros(n, dtype=torch.complex128, device="cuda")
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            st = gmres_device(sb.A[s_], sb.b[s_], xs, False, 1e-8, 50, 1000, sb.pinv[s_], ws=ws)
+            f1.record()
+            torch.cuda.synchronize()
+            t_solve += f0.elapsed_time(f1)
+            its.append(st.iterations)
+            passes += st.matvecs
+        assembled[name] = dict(n=n, frequencies=ks, gemv_ms=ms, gemv_gbs=gbs,
+                               gemv_frac=gbs / hbm, gemv_relerr=err, gmres_iterations=its,
+                               gmres_ms_total=t_solve, gmres_passes=passes,
+                               gmres_solve_gbs=passes * 16.0 * n * n / (t_solve * 1e-3) / 1e9)
+        del sb, xb, y, P, asm
+        torch.cuda.empty_cache()
     top = results[16384]
     line = {
         "metric": "complex matvec HBM GB/s", "value": top["gemv_gbs"], "unit": "GB/s",
@@ -168,7 +224,7 @@ def run_cfg4(args, rank, world, local_rank):
                      "frac": top["gemv_frac"], "traffic": None,
                      "algorithmic_bytes_per_launch": 8 * (16.0 * 16384 ** 2 + 32 * 16384),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
-        "metrics": {str(k): v for k, v in results.items()},
+        "metrics": {**{str(k): v for k, v in results.items()}, "assembled": assembled},
     }
     print(json.dumps(line), flush=True)
 

@@ -97,3 +97,16 @@ def cfg4_random_system(n: int, seed: int):
     a[np.diag_indices(n)] += 3.0 * math.sqrt(n)
     b = (rng.normal(size=n) + 1j * rng.normal(size=n)) / math.sqrt(2.0)
     return a, b
+
+
+def cfg4_assembled():
+    """cfg4-ii: BEM operators of the nearest mesh sizes —
+    ico3 cavity (3,840 DOF), box 16 x 16 x 12 (7,680 DOF), ico4 cavity
+    (15,360 DOF) — at 8 consecutive sweep frequencies, SEM off."""
+    out = []
+    for name, cfg in (("ico3", sphere_pressure(3, 256)),
+                      ("box16x16x12", cfg1(divisions=(16, 16, 12))),
+                      ("ico4", sphere_pressure(4, 256))):
+        cfg.sem_enabled = False
+        out.append((name, cfg))
+    return out
