@@ -90,6 +90,29 @@ def run_cfg3(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def _concurrent_gmres(As, bs, pinvs, n):
+    """The batch's independent solves side by side (gmres_device_concurrent)."""
+    import torch
+
+    from paper_1212_3032_b200.linsolve import gmres_device_concurrent
+
+    xs = [torch.zeros(n, dtype=torch.complex128, device="cuda") for _ in bs]
+    gmres_device_concurrent(As, bs, xs, 1e-8, 50, 1000, pinvs)   # warm-up (workspaces)
+    xs = [torch.zeros(n, dtype=torch.complex128, device="cuda") for _ in bs]
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st = gmres_device_concurrent(As, bs, xs, 1e-8, 50, 1000, pinvs, sync=False)
+    e1.record()
+    torch.cuda.synchronize()
+    st = gmres_device_concurrent(As, bs, [torch.zeros_like(x) for x in xs], 1e-8, 50, 1000, pinvs)
+    ms = e0.elapsed_time(e1)
+    passes = sum(s.matvecs for s in st)
+    return dict(gmres_concurrent_ms_total=ms,
+                gmres_concurrent_iterations=[s.iterations for s in st],
+                gmres_concurrent_solve_gbs=passes * 16.0 * n * n / (ms * 1e-3) / 1e9)
+
+
 def run_cfg4(args, rank, world, local_rank):
     import torch
 
@@ -151,9 +174,11 @@ def run_cfg4(args, rank, world, local_rank):
             its.append(st.iterations)
             passes += st.matvecs
         solve_gbs = passes * 16.0 * n * n / (t_solve * 1e-3) / 1e9
+        conc = _concurrent_gmres([A[s] for s in range(batch)],
+                                 [b[s].contiguous() for s in range(batch)], None, n)
         results[n] = dict(gemv_ms=ms, gemv_gbs=gbs, gemv_frac=gbs / hbm, gemv_relerr=err,
                           gmres_iterations=its, gmres_ms_total=t_solve,
-                          gmres_passes=passes, gmres_solve_gbs=solve_gbs)
+                          gmres_passes=passes, gmres_solve_gbs=solve_gbs, **conc)
         del A, b, y
         torch.cuda.empty_cache()
     # cfg4-ii: assembled BEM operators, 8 consecutive frequencies from one
@@ -206,10 +231,14 @@ def run_cfg4(args, rank, world, local_rank):
             t_solve += f0.elapsed_time(f1)
             its.append(st.iterations)
             passes += st.matvecs
+        conc = _concurrent_gmres([sb.A[s_] for s_ in range(batch)],
+                                 [sb.b[s_] for s_ in range(batch)],
+                                 [sb.pinv[s_] for s_ in range(batch)], n)
         assembled[name] = dict(n=n, frequencies=ks, gemv_ms=ms, gemv_gbs=gbs,
                                gemv_frac=gbs / hbm, gemv_relerr=err, gmres_iterations=its,
                                gmres_ms_total=t_solve, gmres_passes=passes,
-                               gmres_solve_gbs=passes * 16.0 * n * n / (t_solve * 1e-3) / 1e9)
+                               gmres_solve_gbs=passes * 16.0 * n * n / (t_solve * 1e-3) / 1e9,
+                               **conc)
         del sb, xb, y, P, asm
         torch.cuda.empty_cache()
     top = results[16384]

@@ -316,6 +316,31 @@ class DeviceSweep:
 
                 calibrate_row_balance(members[0].A)
                 self._balanced = True
+            conc = os.environ.get("EWB_CONCURRENT_SOLVES", "auto")
+            if (not cfg.sem_enabled and len(group) > 1
+                    and (conc == "1" or (conc == "auto" and self.n < 12000))):
+                # independent members (no SEM chain): solved side by side
+                # (measured: 1.4-1.8x faster at N = 3840-4096, 1.06-1.1x at
+                # 7680-8192, 4 % slower at 15360-16384, hence the size cut)
+                from .linsolve import gmres_device_concurrent
+
+                try:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    gmres_device_concurrent([m.A for m in members], [m.b for m in members],
+                                            [self.sol[k] for k in ks], cfg.tol, cfg.restart,
+                                            cfg.maxiter, [m.pinv for m in members],
+                                            ress=[res_all[i] for i in group],
+                                            hists=[hist_all[i] for i in group], sync=False)
+                    e1.record()
+                except Exception as exc:
+                    omega = complex(self.omegas[ks[0]])
+                    raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
+                for j_, (i, k) in enumerate(zip(group, ks)):
+                    ev.append((i, k, complex(self.omegas[k]), e0, e1, 0, len(group), j_ == 0))
+                idx += len(group)
+                continue
             for i, k, sysm in zip(group, ks, members):
                 omega = complex(self.omegas[k])
                 try:
@@ -333,7 +358,7 @@ class DeviceSweep:
                     raise
                 except Exception as exc:
                     raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
-                ev.append((i, k, omega, e0, e1, n_hist if use_sem else 0))
+                ev.append((i, k, omega, e0, e1, n_hist if use_sem else 0, 1, True))
                 self.sol[k] = self.x
                 if cfg.sem_enabled:
                     self.hist[1:] = self.hist[:-1].clone()
@@ -346,7 +371,7 @@ class DeviceSweep:
         if timing:
             for e_a, e_b in asm_ev:
                 self.phase["assembly_ms"] += e_a.elapsed_time(e_b)
-        for idx, k, omega, e0, e1, sem_cols in ev:
+        for idx, k, omega, e0, e1, sem_cols, share, first in ev:
             if flags[idx, 0]:
                 raise SweepError(f"frequency index {k} (omega={omega:.6g}): non-finite entries "
                                  f"assembled at omega = {omega}")
@@ -362,10 +387,11 @@ class DeviceSweep:
             if not st.converged:
                 log.warning("GMRES stalled at residual %.3e after %d iterations (k=%d)",
                             st.final_residual, st.iterations, k)
-            st.seconds = e0.elapsed_time(e1) * 1e-3
+            st.seconds = e0.elapsed_time(e1) * 1e-3 / share   # concurrent group: its mean
             stats[k] = st
             if timing:
-                self.phase["solve_ms"] += e0.elapsed_time(e1)
+                if first:
+                    self.phase["solve_ms"] += e0.elapsed_time(e1)
             # passes over A: the solver's own count + SEM's Y = A X pass(es)
             self.phase["matvecs"] += st.matvecs + (n_hist_passes(sem_cols) if sem_cols else 0)
             self.phase["solves"] += 1
