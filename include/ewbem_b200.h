@@ -128,6 +128,23 @@ int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* omega_re_h
                               const void* prescribed_dev, void* a_dev, void* b_dev,
                               void* pinv_dev, int32_t* flags_dev, void* stream);
 
+/* The same batch assembled in three steps so that it can overlap the
+ * previous batch's solves (the sweep):
+ *   _begin   (stream A): a persistent far-pair grid of n_sms CTAs, one per SM
+ *            (run it beside solver launches restricted to the other SMs with
+ *            ewb_set_solver_ctas), then the mid and near pairs;
+ *   _finish  (stream B): a full-GPU grid that takes the far pairs left;
+ *   _self    (stream B, ordered after stream A's work by the caller):
+ *            diagonal blocks, b and P^{-1}.
+ * Arguments of _begin as ewb_assemble_system_multi; results identical. */
+int ewb_assemble_system_multi_begin(ewb_ctx* ctx, int32_t nf, const double* omega_re_host,
+                                    const double* omega_im_host, const uint8_t* kinds_dev,
+                                    const void* prescribed_dev, void* a_dev, void* b_dev,
+                                    void* pinv_dev, int32_t* flags_dev, int32_t n_sms,
+                                    void* stream);
+int ewb_assemble_system_multi_finish(ewb_ctx* ctx, void* stream);
+int ewb_assemble_system_multi_self(ewb_ctx* ctx, void* stream);
+
 /* Read and clear the context's fault flags (non-finite entries, singular
  * diagonal blocks) raised by the calls above.  Synchronises. */
 int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite_host, int32_t* singular_host, void* stream);

@@ -21,7 +21,8 @@ EXPORTS = (
     "ewb_abi_version", "ewb_last_error", "ewb_launch_count", "ewb_ctx_create", "ewb_ctx_destroy",
     "ewb_ctx_set_exterior", "ewb_ctx_counts", "ewb_static_rowsums", "ewb_static_tu",
     "ewb_assemble_tu",
-    "ewb_assemble_system", "ewb_assemble_system_multi", "ewb_calibrate_rows",
+    "ewb_assemble_system", "ewb_assemble_system_multi", "ewb_assemble_system_multi_begin",
+    "ewb_assemble_system_multi_finish", "ewb_assemble_system_multi_self", "ewb_calibrate_rows",
     "ewb_reset_row_balance", "ewb_ctx_flags", "ewb_ctx_flags_async", "ewb_apply_bcs", "ewb_blockdiag_inverse",
     "ewb_gemv_batched", "ewb_set_solver_ctas", "ewb_solver_ctas",
     "ewb_gmres_workspace_bytes", "ewb_gmres",
@@ -68,6 +69,9 @@ _SIGS = {
     "ewb_assemble_tu": (I32, [P, D, D, P, P, P]),
     "ewb_assemble_system": (I32, [P, D, D, P, P, P, P, P, P]),
     "ewb_assemble_system_multi": (I32, [P, I32, P, P, P, P, P, P, P, P, P]),
+    "ewb_assemble_system_multi_begin": (I32, [P, I32, P, P, P, P, P, P, P, P, I32, P]),
+    "ewb_assemble_system_multi_finish": (I32, [P, P]),
+    "ewb_assemble_system_multi_self": (I32, [P, P]),
     "ewb_calibrate_rows": (I32, [P, I64, I32, P, P]),
     "ewb_reset_row_balance": (I32, [P]),
     "ewb_ctx_flags": (I32, [P, P, P, P]),

@@ -307,6 +307,48 @@ class Assembler:
                     log.warning("%d singular 3x3 diagonal blocks; identity fallback", fl[f, 1])
         return out
 
+    # The batch assembly in three steps so that it can overlap the previous
+    # batch's solves (DeviceSweep.run): begin on a side stream beside a solver
+    # restricted to the other SMs, finish + self on the solver's stream.
+    def assemble_system_multi_begin(self, omegas, bcs, prescribed, out, flags, n_sms: int, stream):
+        """Persistent far-pair grid on ``n_sms`` SMs + mid/near pairs, on ``stream``."""
+        torch = _torch()
+        om = np.asarray([complex(w) for w in omegas], dtype=complex)
+        nf = len(om)
+        if not 1 <= nf <= self.MAX_BATCH:
+            raise ValueError(f"batch of {nf} frequencies (1..{self.MAX_BATCH})")
+        if np.any(om == 0):
+            raise ValueError("omega == 0 takes the static path (assemble_system)")
+        kinds = np.ascontiguousarray(bcs.flat_kind(), dtype=np.uint8)
+        n = self.n
+        p = _as_device(prescribed, torch.complex128)
+        if tuple(p.shape) != (nf, n):
+            raise ValueError("prescribed spectra must be (nf, N)")
+        kd = getattr(out, "_kinds_dev", None)
+        if kd is None or not np.array_equal(getattr(out, "_kinds_host", None), kinds):
+            kd = torch.from_numpy(kinds).cuda()
+            out._kinds_dev, out._kinds_host = kd, kinds
+        out._keep_p = p   # alive until the kernels that read it have run
+        ore = np.ascontiguousarray(om.real)
+        oim = np.ascontiguousarray(om.imag)
+        _lib.check(self._lib.ewb_assemble_system_multi_begin(
+            self._ctx, nf, ore.ctypes.data, oim.ctypes.data, _lib.ptr(kd), _lib.ptr(p),
+            _lib.ptr(out.A), _lib.ptr(out.b), _lib.ptr(out.pinv), _lib.ptr(flags), int(n_sms),
+            _lib.stream_handle(stream)), "ewb_assemble_system_multi_begin")
+        out.nf = nf
+        out.unknown_kind = kinds.copy()
+        return out
+
+
+    def assemble_system_multi_finish(self, stream=None):
+        _lib.check(self._lib.ewb_assemble_system_multi_finish(self._ctx, _lib.stream_handle(stream)),
+                   "ewb_assemble_system_multi_finish")
+
+
+    def assemble_system_multi_self(self, stream=None):
+        _lib.check(self._lib.ewb_assemble_system_multi_self(self._ctx, _lib.stream_handle(stream)),
+                   "ewb_assemble_system_multi_self")
+
 
 @dataclass
 class SystemBatch:

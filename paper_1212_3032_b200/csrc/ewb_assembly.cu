@@ -680,8 +680,10 @@ __device__ __forceinline__ cplx unit_phase(double a) {
 #endif
 constexpr int kFarQUnroll = EWB_FAR_QUNROLL;
 constexpr int kFarGeo = 8;
-constexpr size_t kFarMultiSmem = sizeof(double) * (kFarGeo * 3 * 128 + 4 * 3 * 2 * 128) +
-                                 sizeof(FreqConst) * kMaxBatch;
+constexpr size_t far_smem(int bd) {
+  return sizeof(double) * (kFarGeo * 3 * bd + 4 * 3 * 2 * bd) + sizeof(FreqConst) * kMaxBatch;
+}
+constexpr size_t kFarMultiSmem = far_smem(128);
 
 // closed-form brackets from the phase factors, g2 already inside Ep
 __device__ __forceinline__ Brackets brackets_phase_g(cplx ks, cplx kp, cplx iks, cplx ikp, double r,
@@ -709,31 +711,48 @@ __device__ __forceinline__ unsigned expo(double v) {
 }
 __device__ __forceinline__ unsigned expo(cplx v) { return max(expo(v.re), expo(v.im)); }
 
-template <bool RECUR>
-__global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
-                                                                    SysBatch o) {
+// PERSIST: warps pull items (row group x column tile) from a global counter
+// until none is left, so a small resident grid (a few SMs next to the
+// solver) and a later full-GPU grid can share one batch's far pairs
+// (ewb_assemble_system_multi_begin / _finish).  Every item writes the same
+// values whichever warp takes it: results stay deterministic.
+constexpr int kFarPersistThreads = 384;   // one block per SM (smem-limited)
+template <bool RECUR, bool PERSIST>
+__global__ void __launch_bounds__(PERSIST ? kFarPersistThreads : 128,
+                                  PERSIST ? 1 : EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
+                                                                    SysBatch o,
+                                                                    unsigned long long* counter) {
   extern __shared__ double sm_far[];
-  double (*sgeo)[3][128] = reinterpret_cast<double (*)[3][128]>(sm_far);
-  cplx (*sph)[3][128] = reinterpret_cast<cplx (*)[3][128]>(sm_far + kFarGeo * 3 * 128);
-  FreqConst* sfc = reinterpret_cast<FreqConst*>(sm_far + kFarGeo * 3 * 128 + 4 * 3 * 2 * 128);
+  const int BD = blockDim.x;
   const int tid = threadIdx.x;
+  // [slot][q][thread] with a block-size stride (conflict-free)
+  auto SG = [&](int slot, int q) -> double& { return sm_far[(slot * 3 + q) * BD + tid]; };
+  cplx* sph_base = reinterpret_cast<cplx*>(sm_far + kFarGeo * 3 * BD);
+  auto SP = [&](int slot, int q) -> cplx& { return sph_base[(slot * 3 + q) * BD + tid]; };
+  FreqConst* sfc = reinterpret_cast<FreqConst*>(sm_far + kFarGeo * 3 * BD + 4 * 3 * 2 * BD);
   for (int k = tid; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
     ((double*)sfc)[k] = ((const double*)fb.fc)[k];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int ntile = (g.n_e + 31) >> 5;
   const int ngroups = (g.n_e + kFarRows - 1) / kFarRows;
-  if (warp >= (long long)ngroups * ntile) return;
+  const long long nitems = (long long)ngroups * ntile;
+  const long long N = 3LL * g.n_e;
+  const FreqConst& fc0 = fb.fc[0];   // material constants (member-independent)
+  const int nf = fb.nf;
+  long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (PERSIST) {
+    unsigned long long w0 = 0;
+    if (lane == 0) w0 = atomicAdd(counter, 1ull);
+    warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
+  }
+  while (warp < nitems) {
   const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
   const int j = t * 32 + lane;
   const bool jv = j < g.n_e;
-  const long long N = 3LL * g.n_e;
   const int jj = jv ? j : 0;
   const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
   const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
-  const FreqConst& fc0 = fb.fc[0];   // material constants (member-independent)
-  const int nf = fb.nf;
   // BC kinds of column j's three DOFs (member-independent), bit c = Dirichlet
   const unsigned kbits = (o.kinds[3 * jj] == kDirichlet ? 1u : 0u) |
                          (o.kinds[3 * jj + 1] == kDirichlet ? 2u : 0u) |
@@ -754,19 +773,19 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
         const double rr = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
         const double w = g.wfar[q] * ar * ir;
-        sgeo[0][q][tid] = rr;
-        sgeo[1][q][tid] = ir;
-        sgeo[2][q][tid] = dx;
-        sgeo[3][q][tid] = dy;
-        sgeo[4][q][tid] = dz;
-        sgeo[5][q][tid] = fma(dz, nz, fma(dy, ny, dx * nx));
-        sgeo[6][q][tid] = w * fc0.inv4pimu;
-        sgeo[7][q][tid] = w * ir * fc0.inv4pi;
+        SG(0, q) = rr;
+        SG(1, q) = ir;
+        SG(2, q) = dx;
+        SG(3, q) = dy;
+        SG(4, q) = dz;
+        SG(5, q) = fma(dz, nz, fma(dy, ny, dx * nx));
+        SG(6, q) = w * fc0.inv4pimu;
+        SG(7, q) = w * ir * fc0.inv4pi;
         if (RECUR) {
-          sph[0][q][tid] = phase_factor(fc0.ks, rr);
-          sph[1][q][tid] = fc0.g2 * phase_factor(fc0.kp, rr);
-          sph[2][q][tid] = unit_phase(fb.dks * rr);
-          sph[3][q][tid] = unit_phase(fb.dkp * rr);
+          SP(0, q) = phase_factor(fc0.ks, rr);
+          SP(1, q) = fc0.g2 * phase_factor(fc0.kp, rr);
+          SP(2, q) = unit_phase(fb.dks * rr);
+          SP(3, q) = unit_phase(fb.dkp * rr);
         }
       }
     }
@@ -783,18 +802,18 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
         const double ratio = fc0.ratio;
 #pragma unroll kFarQUnroll
         for (int q = 0; q < 3; ++q) {
-          const double rr = sgeo[0][q][tid], ir = sgeo[1][q][tid];
-          const double dx = sgeo[2][q][tid], dy = sgeo[3][q][tid], dz = sgeo[4][q][tid];
-          const double dn = sgeo[5][q][tid], wu = sgeo[6][q][tid], wt = sgeo[7][q][tid];
+          const double rr = SG(0, q), ir = SG(1, q);
+          const double dx = SG(2, q), dy = SG(3, q), dz = SG(4, q);
+          const double dn = SG(5, q), wu = SG(6, q), wt = SG(7, q);
           const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
           const cplx iks = lds_c(&sfc[f].iks), ikp = lds_c(&sfc[f].ikp);
           Brackets br;
           cplx Es, Ep;
           if (RECUR) {
-            Es = sph[0][q][tid];
-            Ep = sph[1][q][tid];
-            sph[0][q][tid] = Es * sph[2][q][tid];
-            sph[1][q][tid] = Ep * sph[3][q][tid];
+            Es = SP(0, q);
+            Ep = SP(1, q);
+            SP(0, q) = Es * SP(2, q);
+            SP(1, q) = Ep * SP(3, q);
           } else {
             Es = phase_factor(ks, rr);
             Ep = lds_c(&sfc[f].g2) * phase_factor(kp, rr);
@@ -852,6 +871,13 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
       }
     }
   }
+  if (!PERSIST) break;
+  {
+    unsigned long long w0 = 0;
+    if (lane == 0) w0 = atomicAdd(counter, 1ull);
+    warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
+  }
+  }  // item loop
 }
 
 // Mid pairs (tier 1, gauss7) from the CSR list: thread = (pair, member).
@@ -1400,12 +1426,31 @@ static cudaError_t ensure_multi_scratch(Context& c, int nf) {
   c.nf_cap = 0;
   cudaError_t err = cudaSuccess;
   const size_t n3 = 3 * (size_t)c.n_e;
+  if (!c.far_counter) c.far_counter = dalloc<unsigned long long>(c, 1, err);
   c.bpart_m = dalloc<cplx>(c, (size_t)nf * c.n_tiles * n3, err);
   c.bmid_m = dalloc<cplx>(c, (size_t)nf * 3 * c.n_mid + 1, err);
   c.bnear_m = dalloc<cplx>(c, (size_t)nf * 3 * c.n_near + 1, err);
   if (err == cudaSuccess) c.nf_cap = nf;
   return err;
 }
+
+static void far_attrs() {
+  static bool attr = false;
+  if (attr) return;
+  cudaFuncSetAttribute(k_far_multi<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kFarMultiSmem);
+  cudaFuncSetAttribute(k_far_multi<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kFarMultiSmem);
+  cudaFuncSetAttribute(k_far_multi<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)far_smem(kFarPersistThreads));
+  cudaFuncSetAttribute(k_far_multi<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)far_smem(kFarPersistThreads));
+  attr = true;
+}
+
+static FreqBatch make_batch(Context& c, int nf, const double* ore, const double* oim);
+static cudaError_t launch_multi_rest(Context& c, const FreqBatch& fb, const SysBatch& o,
+                                     bool midnear, bool self, cudaStream_t s);
 
 cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
                                          const double* oim, const uint8_t* kinds,
@@ -1414,6 +1459,21 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
   if (nf < 1 || nf > kMaxBatch) return cudaErrorInvalidValue;
   cudaError_t err = ensure_multi_scratch(c, nf);
   if (err) return err;
+  FreqBatch fb = make_batch(c, nf, ore, oim);
+  const bool recur = fb.recur != 0;
+  SysBatch o{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
+  const int n = c.n_e;
+  const long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
+  const unsigned fb_blocks = blocks_for(warps * 32, 128);
+  far_attrs();
+  if (recur)
+    EWB_NOTE k_far_multi<true, false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o, nullptr);
+  else
+    EWB_NOTE k_far_multi<false, false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o, nullptr);
+  return launch_multi_rest(c, fb, o, true, true, s);
+}
+
+static FreqBatch make_batch(Context& c, int nf, const double* ore, const double* oim) {
   FreqBatch fb{};
   fb.nf = nf;
   for (int f = 0; f < nf; ++f) fb.fc[f] = freq_const(c, ore[f], oim[f]);
@@ -1433,31 +1493,69 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
     }
   }
   fb.recur = recur ? 1 : 0;
-  SysBatch o{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
-  const int n = c.n_e;
-  const long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
-  const unsigned fb_blocks = blocks_for(warps * 32, 128);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_far_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kFarMultiSmem);
-    cudaFuncSetAttribute(k_far_multi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kFarMultiSmem);
-    attr = true;
-  }
-  if (recur)
-    EWB_NOTE k_far_multi<true><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
-  else
-    EWB_NOTE k_far_multi<false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
-  if (c.n_mid)
+  return fb;
+}
+
+// mid / near (and self) kernels of a batch
+static cudaError_t launch_multi_rest(Context& c, const FreqBatch& fb, const SysBatch& o,
+                                     bool midnear, bool self, cudaStream_t s) {
+  const int n = c.n_e, nf = fb.nf;
+  if (midnear && c.n_mid)
     EWB_NOTE k_mid_multi<<<blocks_for((long long)c.n_mid * nf, 128), 128, 0, s>>>(c.g, fb, o,
                                                                                 (int)c.n_mid);
-  if (c.n_near)
+  if (midnear && c.n_near)
     EWB_NOTE k_near_multi<<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, fb, o,
                                                                                   c.n_near);
-  EWB_NOTE k_self_multi<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(
-      c.g, fb, o, c.diag_base, c.n_tiles, (int)c.n_mid, c.n_near);
+  if (self)
+    EWB_NOTE k_self_multi<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(
+        c.g, fb, o, c.diag_base, c.n_tiles, (int)c.n_mid, c.n_near);
   return cudaGetLastError();
+}
+
+static cudaError_t launch_far_persistent(Context& c, int blocks, cudaStream_t s) {
+  far_attrs();
+  const size_t sm = far_smem(kFarPersistThreads);
+  if (c.pend_fb.recur)
+    EWB_NOTE k_far_multi<true, true><<<blocks, kFarPersistThreads, sm, s>>>(c.g, c.pend_fb,
+                                                                           c.pend_o, c.far_counter);
+  else
+    EWB_NOTE k_far_multi<false, true><<<blocks, kFarPersistThreads, sm, s>>>(c.g, c.pend_fb,
+                                                                            c.pend_o, c.far_counter);
+  return cudaGetLastError();
+}
+
+// Overlapped batch assembly (the sweep assembles batch b+1 while it solves
+// batch b): begin() puts a persistent far-pair grid of `n_sms` one-block-per-
+// SM CTAs on stream `s` (next to a solver restricted to the other SMs, see
+// ewb_set_solver_ctas), followed by the mid and near kernels; finish() runs
+// a full-GPU grid on the same work counter (it takes whatever far items are
+// left); self() builds the diagonal blocks, b and P^{-1} once both streams'
+// work is done (the caller orders it after begin's stream).
+cudaError_t launch_assemble_multi_begin(Context& c, int nf, const double* ore, const double* oim,
+                                        const uint8_t* kinds, const cplx* prescribed, cplx* A,
+                                        cplx* b, cplx* pinv, int* flags, int n_sms,
+                                        cudaStream_t s) {
+  if (nf < 1 || nf > kMaxBatch || n_sms < 1) return cudaErrorInvalidValue;
+  cudaError_t err = ensure_multi_scratch(c, nf);
+  if (err) return err;
+  c.pend_fb = make_batch(c, nf, ore, oim);
+  c.pend_o = SysBatch{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
+  err = cudaMemsetAsync(c.far_counter, 0, sizeof(unsigned long long), s);
+  if (err) return err;
+  err = launch_far_persistent(c, n_sms, s);
+  if (err) return err;
+  return launch_multi_rest(c, c.pend_fb, c.pend_o, true, false, s);
+}
+
+cudaError_t launch_assemble_multi_finish(Context& c, cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return launch_far_persistent(c, sms, s);
+}
+
+cudaError_t launch_assemble_multi_self(Context& c, cudaStream_t s) {
+  return launch_multi_rest(c, c.pend_fb, c.pend_o, false, true, s);
 }
 
 }  // namespace ewb

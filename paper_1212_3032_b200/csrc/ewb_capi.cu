@@ -167,6 +167,37 @@ int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* ore, const
   return EWB_OK;
 }
 
+int ewb_assemble_system_multi_begin(ewb_ctx* ctx, int32_t nf, const double* ore,
+                                    const double* oim, const uint8_t* kinds, const void* p,
+                                    void* a, void* b, void* pinv, int32_t* flags, int32_t n_sms,
+                                    void* stream) {
+  if (!ctx || !ore || !oim || !kinds || !p || !a || !b || !pinv || !flags)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_begin: null argument");
+  if (nf < 1 || nf > EWB_MAX_BATCH || n_sms < 1)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_begin: bad nf or n_sms");
+  for (int f = 0; f < nf; ++f)
+    if (int rc = check_omega(ore[f], oim[f], "ewb_assemble_system_multi_begin")) return rc;
+  EWB_CUDA(ewb::launch_assemble_multi_begin(ctx->c, nf, ore, oim, kinds, (const ewb::cplx*)p,
+                                            (ewb::cplx*)a, (ewb::cplx*)b, (ewb::cplx*)pinv, flags,
+                                            n_sms, S(stream)),
+           "ewb_assemble_system_multi_begin");
+  return EWB_OK;
+}
+
+int ewb_assemble_system_multi_finish(ewb_ctx* ctx, void* stream) {
+  if (!ctx || ctx->c.pend_fb.nf < 1)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_finish: no batch begun");
+  EWB_CUDA(ewb::launch_assemble_multi_finish(ctx->c, S(stream)), "ewb_assemble_system_multi_finish");
+  return EWB_OK;
+}
+
+int ewb_assemble_system_multi_self(ewb_ctx* ctx, void* stream) {
+  if (!ctx || ctx->c.pend_fb.nf < 1)
+    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_self: no batch begun");
+  EWB_CUDA(ewb::launch_assemble_multi_self(ctx->c, S(stream)), "ewb_assemble_system_multi_self");
+  return EWB_OK;
+}
+
 int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite, int32_t* singular, void* stream) {
   if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_flags: null argument");
   int h[4] = {0, 0, 0, 0};

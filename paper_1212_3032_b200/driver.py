@@ -160,6 +160,29 @@ class DeviceSweep:
         self.assembly_batch = assembly_batch
         self.d2h_bytes = 0
 
+    def _p_rows(self, ks):
+        """Prescribed spectra of frequencies ks as an (nf, N) device view/copy."""
+        return (self.P[ks[0]:ks[-1] + 1] if ks == list(range(ks[0], ks[-1] + 1))
+                else self.P[ks].contiguous())
+
+    def _overlap_buffers(self, nb: int) -> bool:
+        """Two batch buffers for the overlapped assembly, if HBM allows."""
+        import torch
+
+        from .assembly import SystemBatch
+
+        if getattr(self, "_bufs", None) is not None and self._bufs[0].A.shape[0] >= nb:
+            return True
+        self._bufs = None
+        self.batch = None
+        torch.cuda.empty_cache()
+        free, _ = torch.cuda.mem_get_info()
+        need = 2 * nb * (16 * self.n * self.n + 16 * 4 * self.n)
+        if need > 0.8 * free:
+            return False
+        self._bufs = [SystemBatch.allocate(nb, self.n), SystemBatch.allocate(nb, self.n)]
+        return True
+
     def batch_size(self) -> int:
         """Frequencies assembled per pass over the element pairs.
 
@@ -268,44 +291,84 @@ class DeviceSweep:
         ax0 = torch.empty(self.n, dtype=torch.complex128, device="cuda")
         nb = self.batch_size()
         asm_ev = []
-        idx = 0
-        while idx < nf:
-            # next group: up to nb frequencies assembled in one pass over the
-            # element pairs (omega == 0, the static path, always alone)
-            group = [idx]
-            if complex(self.omegas[self.frequencies[idx]]) != 0:
-                while (len(group) < nb and idx + len(group) < nf
-                       and complex(self.omegas[self.frequencies[idx + len(group)]]) != 0):
-                    group.append(idx + len(group))
+        # groups: up to nb consecutive frequencies assembled in one pass over
+        # the element pairs (omega == 0, the static path, always alone)
+        groups = []
+        i0 = 0
+        while i0 < nf:
+            g_ = [i0]
+            if complex(self.omegas[self.frequencies[i0]]) != 0:
+                while (len(g_) < nb and i0 + len(g_) < nf
+                       and complex(self.omegas[self.frequencies[i0 + len(g_)]]) != 0):
+                    g_.append(i0 + len(g_))
+            groups.append(g_)
+            i0 += len(g_)
+        conc_env = os.environ.get("EWB_CONCURRENT_SOLVES", "auto")
+        concurrent = (not cfg.sem_enabled
+                      and (conc_env == "1" or (conc_env == "auto" and self.n < 12000)))
+        # overlap (opt-in, EWB_OVERLAP_ASSEMBLY=1): batch g+1's far pairs are
+        # assembled on a few SMs while batch g is solved on the others; needs
+        # two batch buffers.  Measured on cfg2: it hides half
+        # the assembly but the concurrent FP64 work slows every GMRES pass by
+        # 2.6-3.9 %, a net loss, so it is off by default.
+        n_ovl = int(os.environ.get("EWB_OVERLAP_SMS", "8"))
+        overlap = (os.environ.get("EWB_OVERLAP_ASSEMBLY", "0") == "1" and not concurrent
+                   and len(groups) > 1 and n_ovl > 0 and self._overlap_buffers(nb))
+        stream_a = torch.cuda.Stream() if overlap else None
+        full_ctas = int(lib.ewb_solver_ctas())
+        pending = None   # index of the group whose assembly was begun on stream_a
+        for gi, group in enumerate(groups):
             ks = [self.frequencies[i] for i in group]
+            idx = group[0]
             try:
                 e_a = torch.cuda.Event(enable_timing=True)
                 e_b = torch.cuda.Event(enable_timing=True)
                 e_a.record()
-                if complex(self.omegas[ks[0]]) != 0:
-                    self.batch = asm.assemble_system_multi(
-                        [self.omegas[k] for k in ks], cfg.bcs, self.P[ks[0]:ks[-1] + 1]
-                        if ks == list(range(ks[0], ks[-1] + 1)) else self.P[ks],
-                        out=self.batch, flags=flags_all[group[0]:group[-1] + 1], check=False)
-                    members = [self.batch.member(f) for f in range(len(group))]
+                if pending == gi:
+                    buf = self._bufs[gi % 2]
+                    asm.assemble_system_multi_finish()
+                    torch.cuda.current_stream().wait_stream(stream_a)
+                    asm.assemble_system_multi_self()
+                    members = [buf.member(f) for f in range(len(group))]
+                    pending = None
+                elif complex(self.omegas[ks[0]]) != 0:
+                    out = self._bufs[gi % 2] if overlap else self.batch
+                    out = asm.assemble_system_multi(
+                        [self.omegas[k] for k in ks], cfg.bcs, self._p_rows(ks), out=out,
+                        flags=flags_all[group[0]:group[-1] + 1], check=False)
+                    if overlap:
+                        self._bufs[gi % 2] = out
+                    else:
+                        self.batch = out
+                    members = [out.member(f) for f in range(len(group))]
                 else:
                     omega = complex(self.omegas[ks[0]])
-                    sysm = asm.assemble_system(omega, cfg.bcs, self.P[ks[0]],
-                                               out=self.system if omega != 0 else None,
-                                               check=False)
-                    if sysm.pinv is None:   # omega == 0: static path (kappa = 0 sweeps)
-                        sysm.pinv = block_diag_precond(sysm.A).pinv
-                    else:
-                        self.system = sysm
+                    sysm = asm.assemble_system(omega, cfg.bcs, self.P[ks[0]], check=False)
+                    sysm.pinv = block_diag_precond(sysm.A).pinv   # static path (kappa = 0)
                     _lib.check(lib.ewb_ctx_flags_async(asm.ctx, _lib.ptr(flags_all[group[0]]),
                                                        _lib.stream_handle()),
                                "ewb_ctx_flags_async")
                     members = [sysm]
                 e_b.record()
                 asm_ev.append((e_a, e_b))
+                nxt = groups[gi + 1] if gi + 1 < len(groups) else None
+                if (overlap and nxt is not None
+                        and complex(self.omegas[self.frequencies[nxt[0]]]) != 0):
+                    # batch gi+1 starts on n_ovl SMs once batch gi's diagonal
+                    # kernel (shared scratch) and batch gi-1's solves (its buffer)
+                    # are done; batch gi's solves use the other SMs
+                    kn = [self.frequencies[i] for i in nxt]
+                    stream_a.wait_stream(torch.cuda.current_stream())
+                    self._bufs[(gi + 1) % 2] = asm.assemble_system_multi_begin(
+                        [self.omegas[k] for k in kn], cfg.bcs, self._p_rows(kn),
+                        self._bufs[(gi + 1) % 2], flags_all[nxt[0]:nxt[-1] + 1], n_ovl,
+                        stream_a)
+                    pending = gi + 1
+                    _lib.check(lib.ewb_set_solver_ctas(max(1, full_ctas - n_ovl)))
             except SweepError:
                 raise
             except Exception as exc:
+                _lib.check(lib.ewb_set_solver_ctas(0))
                 omega = complex(self.omegas[ks[0]])
                 raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
             if (os.environ.get("EWB_ROW_BALANCE") == "1" and self.n >= 4096
@@ -316,9 +379,7 @@ class DeviceSweep:
 
                 calibrate_row_balance(members[0].A)
                 self._balanced = True
-            conc = os.environ.get("EWB_CONCURRENT_SOLVES", "auto")
-            if (not cfg.sem_enabled and len(group) > 1
-                    and (conc == "1" or (conc == "auto" and self.n < 12000))):
+            if concurrent and len(group) > 1:
                 # independent members (no SEM chain): solved side by side
                 # (measured: 1.4-1.8x faster at N = 3840-4096, 1.06-1.1x at
                 # 7680-8192, 4 % slower at 15360-16384, hence the size cut)
@@ -339,7 +400,6 @@ class DeviceSweep:
                     raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
                 for j_, (i, k) in enumerate(zip(group, ks)):
                     ev.append((i, k, complex(self.omegas[k]), e0, e1, 0, len(group), j_ == 0))
-                idx += len(group)
                 continue
             for i, k, sysm in zip(group, ks, members):
                 omega = complex(self.omegas[k])
@@ -357,6 +417,7 @@ class DeviceSweep:
                 except SweepError:
                     raise
                 except Exception as exc:
+                    _lib.check(lib.ewb_set_solver_ctas(0))
                     raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
                 ev.append((i, k, omega, e0, e1, n_hist if use_sem else 0, 1, True))
                 self.sol[k] = self.x
@@ -364,7 +425,7 @@ class DeviceSweep:
                     self.hist[1:] = self.hist[:-1].clone()
                     self.hist[0] = self.x
                     n_hist = min(n_hist + 1, K)
-            idx += len(group)
+            _lib.check(lib.ewb_set_solver_ctas(0))   # (the overlap's reduced budget)
         torch.cuda.synchronize()
         flags = flags_all.cpu().numpy()
         res_host = res_all.cpu().numpy()

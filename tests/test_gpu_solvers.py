@@ -452,3 +452,23 @@ def test_concurrent_solves_equal_sequential(cuda):
     for (xr, ir), x, st in zip(seq, xs, stats):
         assert abs(st.iterations - ir) <= 1 and st.converged
         assert rel_max(x.cpu().numpy(), xr) <= 1e-8
+
+
+def test_overlapped_batch_assembly_sweep_equals_default(cuda, monkeypatch):
+    """EWB_OVERLAP_ASSEMBLY=1 (batch g+1 assembled on a few SMs beside batch
+    g's solves, then finished on the full GPU) gives the default sweep."""
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.workloads import cfg1
+
+    cfg = cfg1()
+    ks = list(range(0, 40))
+    ref = DeviceSweep(cfg, frequencies=ks)
+    st_ref = ref.run()
+    monkeypatch.setenv("EWB_OVERLAP_ASSEMBLY", "1")
+    monkeypatch.setenv("EWB_OVERLAP_SMS", "8")
+    ds = DeviceSweep(cfg, assembler=ref.asm, frequencies=ks)
+    st = ds.run()
+    assert getattr(ds, "_bufs", None) is not None      # the overlapped path ran
+    for k in ks:
+        assert abs(st[k].iterations - st_ref[k].iterations) <= 1
+        assert rel_max(ds.sol[k].cpu().numpy(), ref.sol[k].cpu().numpy()) <= 1e-6
