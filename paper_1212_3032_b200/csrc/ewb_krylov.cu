@@ -230,6 +230,19 @@ __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cp
 __device__ __forceinline__ void ring_wait(const Ring& R, unsigned pos) {
   const uint32_t bar = smem_u32(&R.bar[pos % kNS]);
   const uint32_t parity = (pos / kNS) & 1u;
+#ifdef EWB_WAIT_HINT   // experiment: suspend-time hint (ns) for the waiting warps
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "n"(EWB_WAIT_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -241,6 +254,7 @@ __device__ __forceinline__ void ring_wait(const Ring& R, unsigned pos) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // y[k] = A x[k] for K vectors (x, y: vector k at +k n), all CTAs cooperate;

@@ -1,5 +1,5 @@
-"""cfg2 sweep solve-phase time vs the solver CTA budget (SMs left free for
-concurrent work).  python tools/solver_ctas_sweep.py 148 140 136 132 128"""
+"""Sweep solve-phase time vs the solver CTA budget (SMs left free for
+concurrent work).  python tools/solver_ctas_sweep.py [cfg1|cfg2] 148 140 136 132 128"""
 import sys
 
 sys.path.insert(0, ".")
@@ -9,9 +9,11 @@ from paper_1212_3032_b200 import _lib, workloads  # noqa: E402
 from paper_1212_3032_b200.driver import DeviceSweep  # noqa: E402
 
 lib = _lib.load()
-ds = DeviceSweep(workloads.cfg2())
+args = sys.argv[1:]
+wl = args.pop(0) if args and args[0].startswith("cfg") else "cfg2"
+ds = DeviceSweep(getattr(workloads, wl)())
 ds.run()
-for g in [int(a) for a in sys.argv[1:]]:
+for g in [int(a) for a in args]:
     _lib.check(lib.ewb_set_solver_ctas(g))
     ds.run(timing=True)
     st = ds.run(timing=True)
