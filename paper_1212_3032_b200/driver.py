@@ -368,7 +368,7 @@ class DeviceSweep:
             except SweepError:
                 raise
             except Exception as exc:
-                _lib.check(lib.ewb_set_solver_ctas(0))
+                _lib.check(lib.ewb_set_solver_ctas(full_ctas))
                 omega = complex(self.omegas[ks[0]])
                 raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
             if (os.environ.get("EWB_ROW_BALANCE") == "1" and self.n >= 4096
@@ -417,7 +417,7 @@ class DeviceSweep:
                 except SweepError:
                     raise
                 except Exception as exc:
-                    _lib.check(lib.ewb_set_solver_ctas(0))
+                    _lib.check(lib.ewb_set_solver_ctas(full_ctas))
                     raise SweepError(f"frequency index {k} (omega={omega:.6g}): {exc}") from exc
                 ev.append((i, k, omega, e0, e1, n_hist if use_sem else 0, 1, True))
                 self.sol[k] = self.x
@@ -425,7 +425,7 @@ class DeviceSweep:
                     self.hist[1:] = self.hist[:-1].clone()
                     self.hist[0] = self.x
                     n_hist = min(n_hist + 1, K)
-            _lib.check(lib.ewb_set_solver_ctas(0))   # (the overlap's reduced budget)
+            _lib.check(lib.ewb_set_solver_ctas(full_ctas))   # the caller's budget back
         torch.cuda.synchronize()
         flags = flags_all.cpu().numpy()
         res_host = res_all.cpu().numpy()

@@ -227,7 +227,7 @@ def gmres_device_concurrent(As, bs, xs, tol: float, restart: int, maxiter: int, 
                              res=None if ress is None else ress[i],
                              hist=None if hists is None else hists[i])
     finally:
-        _lib.check(lib.ewb_set_solver_ctas(0))
+        _lib.check(lib.ewb_set_solver_ctas(full))   # the caller's budget back
     for st_ in streams:
         main.wait_stream(st_)
     if sync:
