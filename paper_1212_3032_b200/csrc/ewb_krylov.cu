@@ -176,6 +176,9 @@ struct Ring {
 // stay in L2 across passes.  Measured (n = 15360): 2 rows lift a standalone
 // GEMV from 6.76 to 6.88 TB/s but slow the cfg2 sweep from 4.02 to 4.09 s
 // (the pinned rows crowd the Krylov basis out of L2), so it is off.
+#ifndef EWB_X_PREFETCH
+#define EWB_X_PREFETCH 0
+#endif
 #ifndef EWB_L2_PREFETCH_TILES
 #define EWB_L2_PREFETCH_TILES 0
 #endif
@@ -1164,6 +1167,18 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
           xn[m][k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
         }
     }
+#if EWB_X_PREFETCH
+    {  // the x columns of the stage after next into L1 (no registers held)
+      const int t2 = (t + 2) % ntile;
+      const long long c2 = (long long)t2 * kTC;
+      constexpr int kLines = kTC * 16 / 128;   // 128-byte lines per vector segment
+      if (threadIdx.x < K * kLines) {
+        const int k = threadIdx.x / kLines, ln = threadIdx.x % kLines;
+        const long long cc = c2 + ln * 8;
+        if (cc < n) asm volatile("prefetch.global.L1 [%0];" ::"l"(x + k * n + cc));
+      }
+    }
+#endif
     __syncwarp();
     if ((threadIdx.x & 31) == 0 &&
         atomicAdd(&s_rel[pos % kNS], 1) == kSolveWarps - 1) {  // last reader of the slot
