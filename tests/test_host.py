@@ -178,6 +178,17 @@ def test_argument_validation_without_gpu():
     assert lib.ewb_blockdiag_inverse(ctypes.c_void_p(16), 4, ctypes.c_void_p(16),
                                      ctypes.c_void_p(16), None) == _lib.EWB_ERR_INVALID
     assert b"divisible by 3" in lib.ewb_last_error()
+    # multi-frequency entry points (ABI v3)
+    v = ctypes.c_void_p(16)
+    assert lib.ewb_assemble_system_multi(None, 4, v, v, v, v, v, v, v, v, None) == \
+        _lib.EWB_ERR_INVALID
+    assert b"null argument" in lib.ewb_last_error()
+    assert lib.ewb_assemble_system_multi_finish(None, None) == _lib.EWB_ERR_INVALID
+    assert b"no batch begun" in lib.ewb_last_error()
+    assert lib.ewb_assemble_system_multi_self(None, None) == _lib.EWB_ERR_INVALID
+    assert lib.ewb_calibrate_rows(None, 0, 2, None, None) == _lib.EWB_ERR_INVALID
+    assert b"bad argument" in lib.ewb_last_error()
+    assert lib.ewb_set_solver_ctas(-1) == _lib.EWB_ERR_INVALID
 
 
 # ----------------------------------------------------------------------
