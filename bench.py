@@ -25,6 +25,7 @@ replica sweeps (scaling "weak"); time = max over ranks of CUDA-event time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -271,6 +272,10 @@ def run_ours_sweep(args, rank, world, local_rank):
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
+    # host: move the long-lived objects out of the collector's generations so
+    # a full GC pass cannot stall the enqueueing thread inside the timed steps
+    gc.collect()
+    gc.freeze()
     if dist:
         dist.barrier()
     sampler = ClockSampler(local_rank)
@@ -283,8 +288,12 @@ def run_ours_sweep(args, rank, world, local_rank):
     matvecs = 0
     its = 0
     nfreq = 0
+    step_marks = []
     for _ in range(args.steps):
         one_step()
+        mk = torch.cuda.Event(enable_timing=True)
+        mk.record()
+        step_marks.append(mk)
         asm_ms += ds.phase["assembly_ms"]
         solve_ms += ds.phase["solve_ms"]
         matvecs += ds.phase["matvecs"]
@@ -294,6 +303,10 @@ def run_ours_sweep(args, rank, world, local_rank):
     launches = lib.ewb_launch_count() - launches0
     clocks = sampler.stop()
     elapsed_ms = start.elapsed_time(stop)
+    step_ms, prev = [], start
+    for mk in step_marks:
+        step_ms.append(round(prev.elapsed_time(mk), 2))
+        prev = mk
     if dist:
         t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -409,6 +422,7 @@ def run_ours_sweep(args, rank, world, local_rank):
                         "solve_ms_per_sweep": solve_ms / args.steps,
                         "matvec_hbm_gbs_solve_phase": solve_gbs,
                         "total_gmres_iterations": total_its, "setup_ms": setup_s * 1e3,
+                        "step_ms": step_ms,
                         "fp64_peak_tflops_measured": peak64},
         }
         print(json.dumps(line), flush=True)

@@ -429,6 +429,11 @@ class DeviceSweep:
         torch.cuda.synchronize()
         flags = flags_all.cpu().numpy()
         res_host = res_all.cpu().numpy()
+        # residual histories: one read-back of the used columns for every frequency
+        nh_max = max([min(_lib.GmresResult.from_buffer_copy(res_host[e[0], :32].tobytes()).n_hist,
+                          cap) for e in ev] + [0])
+        hist_host = hist_all[:, :nh_max].cpu().numpy()
+        self.d2h_bytes += flags_all.numel() * 4 + res_all.numel() + hist_host.nbytes
         if timing:
             for e_a, e_b in asm_ev:
                 self.phase["assembly_ms"] += e_a.elapsed_time(e_b)
@@ -443,8 +448,7 @@ class DeviceSweep:
                             init_residual=out.init_residual, final_residual=out.final_residual,
                             converged=bool(out.converged), matvecs=out.matvecs)
             nh = min(out.n_hist, cap)
-            st.residual_history = hist_all[idx, :nh].cpu().tolist() if nh else []
-            self.d2h_bytes += 16 + 32 + 8 * nh
+            st.residual_history = hist_host[idx, :nh].tolist() if nh else []
             if not st.converged:
                 log.warning("GMRES stalled at residual %.3e after %d iterations (k=%d)",
                             st.final_residual, st.iterations, k)
