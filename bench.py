@@ -166,6 +166,32 @@ def _time_dense_parts(n_full: int, n_sample: int, passes_per_freq: float, seed: 
                 gemv=gemv_s * passes_per_freq, scatter=(t5 - t4) * scale)
 
 
+def host_info() -> dict:
+    """CPU model, core count, numpy BLAS and thread settings of the host the
+    CPU baseline ran on (report them beside the number)."""
+    import numpy as np
+
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = ""
+    try:
+        b = np.show_config(mode="dicts")["Build Dependencies"]["blas"]
+        blas = f"{b.get('name', '')} {b.get('version', '')}".strip()
+    except Exception:
+        pass
+    threads = {k: os.environ[k] for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                           "MKL_NUM_THREADS") if k in os.environ}
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__,
+            "blas": blas, "thread_env": threads}
+
+
 def cpu_sweep_estimate(cfg, n_cols: int, freq_ids, seed: int, passes_per_freq: float):
     """Extrapolated CPU seconds for one full sweep of ``cfg`` (reference algorithm).
 
@@ -400,7 +426,8 @@ def run_ours_sweep(args, rank, world, local_rank):
         passes = (matvecs / max(nfreq, 1)) + cfg.sem_depth - 1   # reference: K separate matvecs
         est = cpu_sweep_estimate(cfg, 48, [1, ds.n_freq // 2, ds.n_freq - 1], 7, passes)
         cpu = {"value": round(est["value"], 1), "unit": "s/sweep", "cores": os.cpu_count(),
-               "kind": "port", "sample": est["sample"], "parts": est["parts"]}
+               "kind": "port", "sample": est["sample"], "parts": est["parts"],
+               "host": host_info()}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "s/sweep", "n_gpus": world,
@@ -451,7 +478,7 @@ def run_reference(args, rank, world):
             "data": "synthetic", "impl": "reference",
             "config": {"workload": desc, "baseline_metric": BASELINE_METRIC},
             "cpu_baseline": {"value": value, "unit": "s/sweep", "cores": os.cpu_count(),
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "sample": sample, "host": host_info()},
             "e2e": {"value": value, "unit": "s/sweep", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
