@@ -122,7 +122,7 @@ int ewb_assemble_system(ewb_ctx* ctx, double omega_re, double omega_im,
  * device arrays: prescribed (nf,N), a (nf,N,N), b (nf,N), pinv (nf,n_e,3,3),
  * flags (nf,4) int32, zeroed by the caller: [f][0] != 0 non-finite entries,
  * [f][1] singular diagonal blocks (identity fallback). */
-#define EWB_MAX_BATCH 16
+#define EWB_MAX_BATCH 32
 int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* omega_re_host,
                               const double* omega_im_host, const uint8_t* kinds_dev,
                               const void* prescribed_dev, void* a_dev, void* b_dev,

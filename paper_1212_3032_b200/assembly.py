@@ -254,12 +254,12 @@ class Assembler:
                 log.warning("%d singular 3x3 diagonal blocks; identity fallback", singular)
         return out
 
-    MAX_BATCH = 16   # EWB_MAX_BATCH
+    MAX_BATCH = 32   # EWB_MAX_BATCH
 
     def assemble_system_multi(self, omegas, bcs: BoundaryConditionSet, prescribed,
                               out: "SystemBatch | None" = None, flags=None,
                               check: bool = True) -> "SystemBatch":
-        """``assemble_system`` for nf <= 16 frequencies of one sweep in one pass
+        """``assemble_system`` for nf <= 32 frequencies of one sweep in one pass
         over the element pairs (ewb_assemble_system_multi).
 
         ``prescribed`` is (nf, N).  Member f equals ``assemble_system(omegas[f])``

@@ -117,7 +117,7 @@ __device__ __forceinline__ cplx to_c(cplx v) { return v; }
 // Multi-frequency batch: per-frequency constants plus the
 // phase step used when the batch is equispaced in Re(omega) with one
 // Im(omega) (every exponential-window sweep: omega_k = k dw - i eta).
-constexpr int kMaxBatch = 16;
+constexpr int kMaxBatch = 32;
 struct FreqBatch {
   FreqConst fc[kMaxBatch];
   int nf;

@@ -194,11 +194,11 @@ class DeviceSweep:
         nb = self.assembly_batch
         if nb is None:
             nb = int(os.environ.get("EWB_ASSEMBLY_BATCH", "16"))
-        nb = max(1, min(int(nb), 16, len(self.frequencies)))
+        nb = max(1, min(int(nb), 32, len(self.frequencies)))
         if nb > 1 and self.batch is None:
             free, _ = torch.cuda.mem_get_info()
             per = 16 * self.n * self.n + 16 * 4 * self.n
-            nb = max(1, min(nb, int(0.5 * free // per)))
+            nb = max(1, min(nb, int(0.65 * free // per)))
         return nb
 
     def run_matrix_free(self):

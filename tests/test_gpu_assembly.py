@@ -272,8 +272,8 @@ def test_multi_frequency_is_bit_deterministic_and_validates(cfg1_asm):
         cfg1_asm.assemble_system_multi([0.0, 1.0 - 0.1j], bcs, P[:2])
     with pytest.raises(ValueError, match="positive imaginary"):
         cfg1_asm.assemble_system_multi([1.0 + 0.5j], bcs, P[:1])
-    with pytest.raises(ValueError, match="batch of 17"):
-        cfg1_asm.assemble_system_multi(om[:17], bcs, np.ones((17, cfg1_asm.n), complex))
+    with pytest.raises(ValueError, match="batch of 33"):
+        cfg1_asm.assemble_system_multi(om[:33], bcs, np.ones((33, cfg1_asm.n), complex))
     with pytest.raises(ValueError, match=r"\(nf, N\)"):
         cfg1_asm.assemble_system_multi(om[1:3], bcs, P)
 

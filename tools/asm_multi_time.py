@@ -35,13 +35,16 @@ def timed(fn, reps=3):
     return e0.elapsed_time(e1) / reps
 
 
-P = torch.ones((16, n), dtype=torch.complex128, device="cuda")
+P = torch.ones((32, n), dtype=torch.complex128, device="cuda")
 single = asm.assemble_system(om[1], cfg.bcs, P[0], check=False)
 batch = None
-for k0 in (1, 60, 112):
+for k0 in (1, 60, 96):
     t1 = timed(lambda: asm.assemble_system(om[k0], cfg.bcs, P[0], out=single, check=False))
     row = [f"k0={k0} single {t1:.3f} ms"]
-    for nf in (4, 8, 16):
+    for nf in (8, 16, 24, 32):
+        if batch is not None and batch.A.shape[0] < nf:
+            batch = None
+            torch.cuda.empty_cache()
         batch = asm.assemble_system_multi(om[k0:k0 + nf], cfg.bcs, P[:nf], out=batch, check=False)
         tb = timed(lambda: asm.assemble_system_multi(om[k0:k0 + nf], cfg.bcs, P[:nf], out=batch,
                                                      check=False))
