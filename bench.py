@@ -74,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "500"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -314,9 +314,15 @@ def run_ours_sweep(args, rank, world, local_rank):
     matvecs = 0
     its = 0
     nfreq = 0
-    step_marks = []
+    step_marks, host_split = [], []
+    if os.environ.get("BENCH_GC_DISABLE") == "1":
+        gc.disable()
     for _ in range(args.steps):
+        th0 = time.perf_counter()
         one_step()
+        host_split.append([round(ds.phase.get(k, 0.0), 1) for k in
+                           ("host_enqueue_ms", "host_wait_ms", "host_post_ms")]
+                          + [round((time.perf_counter() - th0) * 1e3, 1)])
         mk = torch.cuda.Event(enable_timing=True)
         mk.record()
         step_marks.append(mk)
@@ -327,6 +333,7 @@ def run_ours_sweep(args, rank, world, local_rank):
     stop.record()
     torch.cuda.synchronize()
     launches = lib.ewb_launch_count() - launches0
+    gc.enable()
     clocks = sampler.stop()
     elapsed_ms = start.elapsed_time(stop)
     step_ms, prev = [], start
@@ -450,6 +457,7 @@ def run_ours_sweep(args, rank, world, local_rank):
                         "matvec_hbm_gbs_solve_phase": solve_gbs,
                         "total_gmres_iterations": total_its, "setup_ms": setup_s * 1e3,
                         "step_ms": step_ms,
+                        "host_enqueue_wait_post_step_ms": host_split,
                         "fp64_peak_tflops_measured": peak64},
         }
         print(json.dumps(line), flush=True)

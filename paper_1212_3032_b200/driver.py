@@ -283,6 +283,7 @@ class DeviceSweep:
         K = cfg.sem_depth
         self.hist.zero_()
         self.phase = {"assembly_ms": 0.0, "solve_ms": 0.0, "matvecs": 0, "solves": 0}
+        t_host0 = time.perf_counter()
         nf = len(self.frequencies)
         cap = gmres_hist_cap(cfg.maxiter, cfg.restart)
         res_all = torch.zeros((nf, 64), dtype=torch.uint8, device="cuda")
@@ -426,7 +427,9 @@ class DeviceSweep:
                     self.hist[0] = self.x
                     n_hist = min(n_hist + 1, K)
             _lib.check(lib.ewb_set_solver_ctas(full_ctas))   # the caller's budget back
+        t_host1 = time.perf_counter()
         torch.cuda.synchronize()
+        t_host2 = time.perf_counter()
         flags = flags_all.cpu().numpy()
         res_host = res_all.cpu().numpy()
         # residual histories: one read-back of the used columns for every frequency
@@ -460,6 +463,10 @@ class DeviceSweep:
             # passes over A: the solver's own count + SEM's Y = A X pass(es)
             self.phase["matvecs"] += st.matvecs + (n_hist_passes(sem_cols) if sem_cols else 0)
             self.phase["solves"] += 1
+        # host-side split (enqueue / wait for the device / result processing)
+        self.phase["host_enqueue_ms"] = (t_host1 - t_host0) * 1e3
+        self.phase["host_wait_ms"] = (t_host2 - t_host1) * 1e3
+        self.phase["host_post_ms"] = (time.perf_counter() - t_host2) * 1e3
         return stats
 
     def probe_half(self, probes):
