@@ -290,10 +290,18 @@ def run_ours_sweep(args, rank, world, local_rank):
     n_pairs = counts["far"] + counts["mid"] + counts["near"] + counts["n_elements"]
     flops_per_asm = 397.0 * pe + 120.0 * n_pairs        # SURVEY §8(d) algorithmic count
 
+    host_parts = []
+
     def one_step():
+        t0 = time.perf_counter()
         ds.run(timing=True)
+        t1 = time.perf_counter()
         half = ds.probe_half(cfg.probes)
+        t2 = time.perf_counter()
         windowed_inverse_device(half, cfg.window, ds.eta, cfg.period)
+        t3 = time.perf_counter()
+        host_parts.append([round((t1 - t0) * 1e3, 1), round((t2 - t1) * 1e3, 1),
+                           round((t3 - t2) * 1e3, 1)])
 
     for _ in range(args.warmup):
         one_step()
@@ -458,6 +466,7 @@ def run_ours_sweep(args, rank, world, local_rank):
                         "total_gmres_iterations": total_its, "setup_ms": setup_s * 1e3,
                         "step_ms": step_ms,
                         "host_enqueue_wait_post_step_ms": host_split,
+                        "host_run_probe_idft_ms": host_parts[-args.steps:],
                         "fp64_peak_tflops_measured": peak64},
         }
         print(json.dumps(line), flush=True)
