@@ -47,6 +47,21 @@ static int cuda_fail(cudaError_t e, const char* where) {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// The stream-ordered allocator's default pool returns freed memory to the
+// driver at every synchronisation (release threshold 0), so the next small
+// cudaMallocAsync can stall the host for tens of ms; keep it pooled.
+static void keep_pool_memory() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 extern "C" {
 
 int ewb_abi_version(void) { return EWB_ABI_VERSION; }
@@ -496,6 +511,7 @@ static int pair_prep(const double* omega_host, int32_t F, double lam, double mu,
   memcpy(h.data(), fcs.data(), sizeof(ewb::FreqConst) * F);
   memcpy(h.data() + sizeof(ewb::FreqConst) * F, b7, 21 * 8);
   memcpy(h.data() + sizeof(ewb::FreqConst) * F + 21 * 8, w7, 7 * 8);
+  keep_pool_memory();
   EWB_CUDA(cudaMallocAsync(dev_tables, bytes, s), "pair kernels");
   EWB_CUDA(cudaMemcpyAsync(*dev_tables, h.data(), bytes, cudaMemcpyHostToDevice, s), "pair kernels");
   EWB_CUDA(cudaStreamSynchronize(s), "pair kernels");
