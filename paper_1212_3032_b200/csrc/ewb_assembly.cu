@@ -747,136 +747,136 @@ __global__ void __launch_bounds__(PERSIST ? kFarPersistThreads : 128,
     warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
   }
   while (warp < nitems) {
-  const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
-  const int j = t * 32 + lane;
-  const bool jv = j < g.n_e;
-  const int jj = jv ? j : 0;
-  const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
-  const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
-  // BC kinds of column j's three DOFs (member-independent), bit c = Dirichlet
-  const unsigned kbits = (o.kinds[3 * jj] == kDirichlet ? 1u : 0u) |
-                         (o.kinds[3 * jj + 1] == kDirichlet ? 2u : 0u) |
-                         (o.kinds[3 * jj + 2] == kDirichlet ? 4u : 0u);
-  for (int r = 0; r < kFarRows; ++r) {
-    const int i = rg * kFarRows + r;
-    if (i >= g.n_e) break;
-    const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
-    const bool far = jv && j != i && exact_tier(xi, yi, zi, cxj, cyj, czj, dj) == 0;
-    if (far) {
+    const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
+    const int j = t * 32 + lane;
+    const bool jv = j < g.n_e;
+    const int jj = jv ? j : 0;
+    const double cxj = g.cx[jj], cyj = g.cy[jj], czj = g.cz[jj], dj = g.diam[jj];
+    const double nx = g.nx[jj], ny = g.ny[jj], nz = g.nz[jj], ar = g.area[jj];
+    // BC kinds of column j's three DOFs (member-independent), bit c = Dirichlet
+    const unsigned kbits = (o.kinds[3 * jj] == kDirichlet ? 1u : 0u) |
+                           (o.kinds[3 * jj + 1] == kDirichlet ? 2u : 0u) |
+                           (o.kinds[3 * jj + 2] == kDirichlet ? 4u : 0u);
+    for (int r = 0; r < kFarRows; ++r) {
+      const int i = rg * kFarRows + r;
+      if (i >= g.n_e) break;
+      const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
+      const bool far = jv && j != i && exact_tier(xi, yi, zi, cxj, cyj, czj, dj) == 0;
+      if (far) {
 #pragma unroll 1
-      for (int q = 0; q < 3; ++q) {
-        double dx = g.yfar[(size_t)(3 * q) * g.n_e + j] - xi;
-        double dy = g.yfar[(size_t)(3 * q + 1) * g.n_e + j] - yi;
-        double dz = g.yfar[(size_t)(3 * q + 2) * g.n_e + j] - zi;
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        const double ir = rsqrt(r2);
-        const double rr = r2 * ir;
-        dx *= ir; dy *= ir; dz *= ir;
-        const double w = g.wfar[q] * ar * ir;
-        SG(0, q) = rr;
-        SG(1, q) = ir;
-        SG(2, q) = dx;
-        SG(3, q) = dy;
-        SG(4, q) = dz;
-        SG(5, q) = fma(dz, nz, fma(dy, ny, dx * nx));
-        SG(6, q) = w * fc0.inv4pimu;
-        SG(7, q) = w * ir * fc0.inv4pi;
-        if (RECUR) {
-          SP(0, q) = phase_factor(fc0.ks, rr);
-          SP(1, q) = fc0.g2 * phase_factor(fc0.kp, rr);
-          SP(2, q) = unit_phase(fb.dks * rr);
-          SP(3, q) = unit_phase(fb.dkp * rr);
+        for (int q = 0; q < 3; ++q) {
+          double dx = g.yfar[(size_t)(3 * q) * g.n_e + j] - xi;
+          double dy = g.yfar[(size_t)(3 * q + 1) * g.n_e + j] - yi;
+          double dz = g.yfar[(size_t)(3 * q + 2) * g.n_e + j] - zi;
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const double ir = rsqrt(r2);
+          const double rr = r2 * ir;
+          dx *= ir; dy *= ir; dz *= ir;
+          const double w = g.wfar[q] * ar * ir;
+          SG(0, q) = rr;
+          SG(1, q) = ir;
+          SG(2, q) = dx;
+          SG(3, q) = dy;
+          SG(4, q) = dz;
+          SG(5, q) = fma(dz, nz, fma(dy, ny, dx * nx));
+          SG(6, q) = w * fc0.inv4pimu;
+          SG(7, q) = w * ir * fc0.inv4pi;
+          if (RECUR) {
+            SP(0, q) = phase_factor(fc0.ks, rr);
+            SP(1, q) = fc0.g2 * phase_factor(fc0.kp, rr);
+            SP(2, q) = unit_phase(fb.dks * rr);
+            SP(3, q) = unit_phase(fb.dkp * rr);
+          }
         }
       }
-    }
 #pragma unroll 1
-    for (int f = 0; f < nf; ++f) {
-      cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
-      if (far) {
-        // prescribed values of this member, loaded ahead of the quadrature loop
-        cplx pv[3];
+      for (int f = 0; f < nf; ++f) {
+        cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
+        if (far) {
+          // prescribed values of this member, loaded ahead of the quadrature loop
+          cplx pv[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) pv[c] = o.p[(size_t)f * N + 3 * j + c];
-        Acc<cplx> acc;
-        acc_zero(acc);
-        const double ratio = fc0.ratio;
+          for (int c = 0; c < 3; ++c) pv[c] = o.p[(size_t)f * N + 3 * j + c];
+          Acc<cplx> acc;
+          acc_zero(acc);
+          const double ratio = fc0.ratio;
 #pragma unroll kFarQUnroll
-        for (int q = 0; q < 3; ++q) {
-          const double rr = SG(0, q), ir = SG(1, q);
-          const double dx = SG(2, q), dy = SG(3, q), dz = SG(4, q);
-          const double dn = SG(5, q), wu = SG(6, q), wt = SG(7, q);
-          const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
-          const cplx iks = lds_c(&sfc[f].iks), ikp = lds_c(&sfc[f].ikp);
-          Brackets br;
-          cplx Es, Ep;
-          if (RECUR) {
-            Es = SP(0, q);
-            Ep = SP(1, q);
-            SP(0, q) = Es * SP(2, q);
-            SP(1, q) = Ep * SP(3, q);
-          } else {
-            Es = phase_factor(ks, rr);
-            Ep = lds_c(&sfc[f].g2) * phase_factor(kp, rr);
-          }
-          if (lds_d(&sfc[f].ks_abs) * rr < c_num.far_sw) {
-            FreqConst fc = fc0;
-            fc.ks = ks; fc.kp = kp; fc.g2 = lds_c(&sfc[f].g2);
-            br = brackets_series_cold(fc, rr);
-          } else {
-            br = brackets_phase_g(ks, kp, iks, ikp, rr, ir, Es, Ep);
-          }
-          // weighted scalars (kernels.py:330-333), 1/(4 pi mu), 1/(4 pi) inside
-          const cplx Phi = wu * br.f0;
-          const cplx Psi = wu * br.f1;
-          const cplx Aw = wt * (br.f2 - br.f1);
-          const cplx Bw = (c_num.two * wt * dn) * (c_num.two * br.f1 - br.f3);
-          const cplx dd = br.f2 - br.f3;
-          const cplx Cw = wt * (ratio * (dd - c_num.two * br.f1) - c_num.two * (dd - br.f1));
-          acc_point(acc, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
-        }
-        // blocks (kernels.py:336-356) entry by entry straight into A and b:
-        // U_ac = su d_ac - P_ac, T_ac = B_ac + n_a va_c + vc_a n_c + sa d_ac;
-        // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
-        // Dirichlet column A = -U, b -= T p
-        const double n[3] = {nx, ny, nz};
-        const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
-        unsigned ex = 0;
-        cplx* Af = o.A + (size_t)f * N * N;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const cplx u = a == c ? acc.su - acc.P[sym[a][c]] : -acc.P[sym[a][c]];
-            cplx tv = acc.B[sym[a][c]];
-            madd(tv, n[a], acc.va[c]);
-            madd(tv, n[c], acc.vc[a]);
-            if (a == c) tv = tv + acc.sa;
-            ex = max(ex, max(expo(u), expo(tv)));
-            if (kbits & (1u << c)) {
-              row[c] = -u;
-              bc[a] = bc[a] - tv * pv[c];
+          for (int q = 0; q < 3; ++q) {
+            const double rr = SG(0, q), ir = SG(1, q);
+            const double dx = SG(2, q), dy = SG(3, q), dz = SG(4, q);
+            const double dn = SG(5, q), wu = SG(6, q), wt = SG(7, q);
+            const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
+            const cplx iks = lds_c(&sfc[f].iks), ikp = lds_c(&sfc[f].ikp);
+            Brackets br;
+            cplx Es, Ep;
+            if (RECUR) {
+              Es = SP(0, q);
+              Ep = SP(1, q);
+              SP(0, q) = Es * SP(2, q);
+              SP(1, q) = Ep * SP(3, q);
             } else {
-              row[c] = tv;
-              bc[a] = bc[a] + u * pv[c];
+              Es = phase_factor(ks, rr);
+              Ep = lds_c(&sfc[f].g2) * phase_factor(kp, rr);
+            }
+            if (lds_d(&sfc[f].ks_abs) * rr < c_num.far_sw) {
+              FreqConst fc = fc0;
+              fc.ks = ks; fc.kp = kp; fc.g2 = lds_c(&sfc[f].g2);
+              br = brackets_series_cold(fc, rr);
+            } else {
+              br = brackets_phase_g(ks, kp, iks, ikp, rr, ir, Es, Ep);
+            }
+            // weighted scalars (kernels.py:330-333), 1/(4 pi mu), 1/(4 pi) inside
+            const cplx Phi = wu * br.f0;
+            const cplx Psi = wu * br.f1;
+            const cplx Aw = wt * (br.f2 - br.f1);
+            const cplx Bw = (c_num.two * wt * dn) * (c_num.two * br.f1 - br.f3);
+            const cplx dd = br.f2 - br.f3;
+            const cplx Cw = wt * (ratio * (dd - c_num.two * br.f1) - c_num.two * (dd - br.f1));
+            acc_point(acc, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
+          }
+          // blocks (kernels.py:336-356) entry by entry straight into A and b:
+          // U_ac = su d_ac - P_ac, T_ac = B_ac + n_a va_c + vc_a n_c + sa d_ac;
+          // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
+          // Dirichlet column A = -U, b -= T p
+          const double n[3] = {nx, ny, nz};
+          const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+          unsigned ex = 0;
+          cplx* Af = o.A + (size_t)f * N * N;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const cplx u = a == c ? acc.su - acc.P[sym[a][c]] : -acc.P[sym[a][c]];
+              cplx tv = acc.B[sym[a][c]];
+              madd(tv, n[a], acc.va[c]);
+              madd(tv, n[c], acc.vc[a]);
+              if (a == c) tv = tv + acc.sa;
+              ex = max(ex, max(expo(u), expo(tv)));
+              if (kbits & (1u << c)) {
+                row[c] = -u;
+                bc[a] = bc[a] - tv * pv[c];
+              } else {
+                row[c] = tv;
+                bc[a] = bc[a] + u * pv[c];
+              }
             }
           }
+          if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
         }
-        if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
-      }
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        warp_sum(bc[a]);
-        if (lane == 0) o.bpart[((size_t)f * ntile + t) * N + 3 * i + a] = bc[a];
+        for (int a = 0; a < 3; ++a) {
+          warp_sum(bc[a]);
+          if (lane == 0) o.bpart[((size_t)f * ntile + t) * N + 3 * i + a] = bc[a];
+        }
       }
     }
-  }
-  if (!PERSIST) break;
-  {
-    unsigned long long w0 = 0;
-    if (lane == 0) w0 = atomicAdd(counter, 1ull);
-    warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
-  }
+    if (!PERSIST) break;
+    {
+      unsigned long long w0 = 0;
+      if (lane == 0) w0 = atomicAdd(counter, 1ull);
+      warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
+    }
   }  // item loop
 }
 
