@@ -472,3 +472,27 @@ def test_overlapped_batch_assembly_sweep_equals_default(cuda, monkeypatch):
     for k in ks:
         assert abs(st[k].iterations - st_ref[k].iterations) <= 1
         assert rel_max(ds.sol[k].cpu().numpy(), ref.sol[k].cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("nb", [1, 5, 32])
+def test_cfg1_sweep_any_assembly_batch(cuda, nb):
+    """The sweep with 1, 5 or 32 frequencies per assembly pass reproduces the
+    reference's cfg1 histories (1e-6) and iteration counts (as the default-batch
+    end-to-end test)."""
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.transform import windowed_inverse_device
+    from paper_1212_3032_b200.workloads import cfg1
+
+    g = golden("cfg1_sweep")
+    cfg = cfg1()
+    ds = DeviceSweep(cfg, assembly_batch=nb)
+    assert ds.batch_size() == nb
+    st = ds.run()
+    its = np.array([st[k].iterations for k in sorted(st)])
+    d = np.abs(its - g["cfg1_its"])
+    assert d.max() <= 2 and (d <= 1).mean() >= 0.95, d
+    series, _ = windowed_inverse_device(ds.probe_half(cfg.probes), cfg.window, ds.eta, cfg.period)
+    series = series.cpu().numpy()
+    for c, p in enumerate(cfg.probes):
+        href = g[f"cfg1_h_{p.name}"]
+        assert np.linalg.norm(series[:, c] - href) / np.linalg.norm(href) <= 1e-6
