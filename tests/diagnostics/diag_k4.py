@@ -1,4 +1,7 @@
-"""Cross-check at cfg1 k=4: oracle GMRES vs GPU GMRES on oracle-/GPU-assembled A."""
+"""Cross-check at cfg1 k=4: oracle GMRES vs GPU GMRES on oracle-/GPU-assembled A.
+
+Test infrastructure (the oracle is the checker); not collected by pytest.
+Run from the repo root: python tests/diagnostics/diag_k4.py"""
 import sys, time
 sys.path.insert(0, ".")
 import numpy as np, torch
