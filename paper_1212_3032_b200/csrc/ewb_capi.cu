@@ -290,7 +290,7 @@ int ewb_reset_row_balance(void* stream) {
 int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart) {
   int64_t cpl = 16;
   int64_t G = ewb::solver_grid_max();
-  return cpl * (3 * n + (int64_t)(restart + 1) * n +
+  return cpl * (3 * n + (int64_t)(restart + 1) * n + (int64_t)(restart + 1) * n +
                 2 * (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart +
                 2 * G * (2 * ewb::kMaxRestart + 2)) +
          8 * 2 * G * 16 + 256 * 8;
@@ -320,7 +320,9 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   g.w = base + n;
   g.z = base + 2 * n;
   g.V = base + 3 * n;
-  g.H = g.V + (int64_t)(restart + 1) * n;
+  g.W = g.V + (int64_t)(restart + 1) * n;
+  g.rs = g.W + (int64_t)restart * n;
+  g.H = g.rs + n;
   g.Gram = g.H + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
   g.dpart = g.Gram + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
   g.partial = (double*)(g.dpart + 2 * (int64_t)ewb::solver_grid_max() *
@@ -328,6 +330,10 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   {
     const char* env = getenv("EWB_GMRES_ORTHO");
     g.ortho = env ? atoi(env) : 0;
+    // EWB_TRUE_RESIDUAL_PASS=1: the cycle's true residual by a fresh pass
+    // over A (as linsolve.py:200-201 literally does) instead of W y
+    const char* tr = getenv("EWB_TRUE_RESIDUAL_PASS");
+    if ((tr && atoi(tr) == 1) || g.ortho != 0) g.W = nullptr;
   }
   g.probe = nullptr;
   g.probe_cap = 0;

@@ -1440,8 +1440,10 @@ k_gmres_f(GmresArgs a) {
       gs.g[0] = {beta, 0.0};
       for (int k = 1; k <= m; ++k) gs.g[k] = {0.0, 0.0};
     }
-    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+    for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
       a.V[k] = {a.r[k].re / beta, a.r[k].im / beta};
+      if (a.W) a.rs[k] = a.r[k];   // the cycle's starting (true) residual
+    }
     grid.sync();
     double hprev = beta;
     int used = 0;
@@ -1455,6 +1457,7 @@ k_gmres_f(GmresArgs a) {
         if (threadIdx.x < nr) {
           const cplx w = sum[threadIdx.x][0] * sc;
           a.w[row0 + threadIdx.x] = w;
+          if (a.W) a.W[(size_t)j * n + row0 + threadIdx.x] = w;   // = A P^{-1} v_j
           s_wblk[threadIdx.x] = w;
         }
         __syncthreads();
@@ -1738,9 +1741,26 @@ k_gmres_f(GmresArgs a) {
       }
     }
     grid.sync();
-    rnorm = residual(dpar);  // true residual (linsolve.py:200-201)
+    if (a.W) {
+      // true residual (linsolve.py:200-201) without another pass over A:
+      // b - A x_new = r_start - sum_i y_i (A P^{-1} v_i), from the products
+      // this cycle already computed (equal to b - A x_new up
+      // to rounding of |A x|, ~1e-16 |b| against a tolerance of 1e-8 |b|)
+      double q = 0.0;
+      for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        cplx s = a.rs[k];
+        for (int i = 0; i < used; ++i) s = s - s_y[i] * a.W[(size_t)i * n + k];
+        a.r[k] = s;
+        q += abs2(s);
+      }
+      cta_norm_partial(q, dpar);
+      grid.sync();
+      rnorm = sqrt(grid_norm(dpar));
+    } else {
+      rnorm = residual(dpar);  // true residual (linsolve.py:200-201)
+      ++n_mv;
+    }
     dpar ^= 1;
-    ++n_mv;
     res = rnorm / nb;
   }
   if (tid == 0) {

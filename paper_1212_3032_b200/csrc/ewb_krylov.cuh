@@ -29,6 +29,9 @@ struct GmresArgs {
   cplx* w;              // scratch (n)
   cplx* z;              // scratch (n)
   cplx* V;              // scratch ((restart+1) n)
+  cplx* W;              // scratch (restart n): A P^{-1} v_j of the cycle, or nullptr
+                        // (then the cycle's true residual takes a pass over A)
+  cplx* rs;             // scratch (n): the cycle's starting residual (with W)
   cplx* H;              // scratch ((kMaxRestart+1) kMaxRestart)
   cplx* Gram;           // scratch ((kMaxRestart+1) kMaxRestart): <v_i, v_l>, l < i
   cplx* dpart;          // scratch (2 * grid * (2 kMaxRestart + 2)) batched-dot partials

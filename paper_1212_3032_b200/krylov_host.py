@@ -12,6 +12,7 @@ the Givens update — the only host synchronisation in the loop.
 from __future__ import annotations
 
 import logging
+import os
 
 import numpy as np
 
@@ -48,9 +49,14 @@ def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond, ax0=None):
     st.init_residual = res
     st.residual_history.append(res)
     its = 0
+    true_pass = os.environ.get("EWB_TRUE_RESIDUAL_PASS") == "1"
     while res > tol and its < maxiter:
         m = min(restart, maxiter - its)
         V = torch.empty((m + 1, n), dtype=torch.complex128, device="cuda")
+        # the cycle's operator products A P^{-1} v_j, kept so that the true
+        # residual at the end needs no further application (as ewb_gmres)
+        W = None if true_pass else torch.empty((m, n), dtype=torch.complex128, device="cuda")
+        r_start = r
         H = np.zeros((m + 1, m), dtype=complex)
         cs = np.zeros(m, dtype=complex)
         sn = np.zeros(m, dtype=complex)
@@ -61,6 +67,8 @@ def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond, ax0=None):
         used = 0
         for j in range(m):
             w = apply_a(pc(V[j])).clone()
+            if W is not None:
+                W[j] = w
             hcol = torch.empty(j + 2, dtype=torch.complex128, device="cuda")
             for i in range(j + 1):
                 h = torch.vdot(V[i], w)
@@ -99,7 +107,9 @@ def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond, ax0=None):
             y[i] = (g[i] - H[i, i + 1:used] @ y[i + 1:used]) / H[i, i]
         yd = torch.from_numpy(y).cuda()
         x = x + pc(V[:used].T @ yd)
-        r = b - apply_a(x)
+        # true residual (linsolve.py:200-201): b - A x_new equals
+        # r_start - sum_j y_j A P^{-1} v_j to rounding
+        r = b - apply_a(x) if W is None else r_start - W[:used].T @ yd
         rnorm = float(torch.linalg.vector_norm(r))
         res = rnorm / nb
     st.iterations = its
