@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EWB_ABI_VERSION 3
+#define EWB_ABI_VERSION 4
 
 enum ewb_status {
   EWB_OK = 0,
@@ -47,6 +47,17 @@ typedef struct ewb_gmres_result {
   double init_residual;
   double final_residual;
 } ewb_gmres_result;
+
+/* head of the operator-GMRES state (ewb_opgmres_*), at the start of its
+ * workspace; fields as SolveStats (linsolve.py:28-48) plus the gates */
+typedef struct ewb_op_head {
+  int32_t in_cycle;     /* gate: the next operator application is A P^{-1} v_j */
+  int32_t lit_pending;  /* gate: the next operator application is A x          */
+  int32_t done, converged;
+  int32_t iterations, j, m, used;
+  int32_t cycle_open, n_hist, applications, pad;
+  double norm_b, rnorm, residual, init_residual, final_residual;
+} ewb_op_head;
 
 typedef struct ewb_sem_result {
   int32_t kept;        /* history columns used after the rank filter */
@@ -91,6 +102,16 @@ int ewb_ctx_set_exterior(ewb_ctx* ctx, int32_t on, void* stream);
 /* counts_host[8] = n_e, far pairs, mid pairs, near pairs, near L1..L4. */
 int ewb_ctx_counts(const ewb_ctx* ctx, int64_t* counts_host);
 
+/* The context's pair tables (Assembler._prepare_geometry's buckets,
+ * assembly.py:132-161) copied to host buffers (each nullable), rows sorted:
+ * near_ptr/mid_ptr (n_e+1) CSR row pointers, near_j/near_lvl (n_near) column
+ * and subdivision level 1..4 of each near pair, mid_j (n_mid) column of each
+ * mid (gauss7) pair.  Every other off-diagonal pair is far (gauss3).
+ * Synchronises. */
+int ewb_ctx_pair_lists(const ewb_ctx* ctx, int32_t* near_ptr_host, int32_t* near_j_host,
+                       int32_t* near_lvl_host, int32_t* mid_ptr_host, int32_t* mid_j_host,
+                       void* stream);
+
 /* Static off-diagonal traction row sums, (n_e,3,3) float64
  * (Assembler.static_offdiag_rowsums, assembly.py:174-182). */
 int ewb_static_rowsums(ewb_ctx* ctx, double* out_dev, void* stream);
@@ -128,23 +149,6 @@ int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* omega_re_h
                               const void* prescribed_dev, void* a_dev, void* b_dev,
                               void* pinv_dev, int32_t* flags_dev, void* stream);
 
-/* The same batch assembled in three steps so that it can overlap the
- * previous batch's solves (the sweep):
- *   _begin   (stream A): a persistent far-pair grid of n_sms CTAs, one per SM
- *            (run it beside solver launches restricted to the other SMs with
- *            ewb_set_solver_ctas), then the mid and near pairs;
- *   _finish  (stream B): a full-GPU grid that takes the far pairs left;
- *   _self    (stream B, ordered after stream A's work by the caller):
- *            diagonal blocks, b and P^{-1}.
- * Arguments of _begin as ewb_assemble_system_multi; results identical. */
-int ewb_assemble_system_multi_begin(ewb_ctx* ctx, int32_t nf, const double* omega_re_host,
-                                    const double* omega_im_host, const uint8_t* kinds_dev,
-                                    const void* prescribed_dev, void* a_dev, void* b_dev,
-                                    void* pinv_dev, int32_t* flags_dev, int32_t n_sms,
-                                    void* stream);
-int ewb_assemble_system_multi_finish(ewb_ctx* ctx, void* stream);
-int ewb_assemble_system_multi_self(ewb_ctx* ctx, void* stream);
-
 /* Read and clear the context's fault flags (non-finite entries, singular
  * diagonal blocks) raised by the calls above.  Synchronises. */
 int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite_host, int32_t* singular_host, void* stream);
@@ -174,24 +178,16 @@ int ewb_gemv_batched(const void* a_dev, const void* x_dev, void* y_dev, int64_t 
  * Process-wide; not thread-safe. */
 int ewb_set_solver_ctas(int32_t ctas);
 int32_t ewb_solver_ctas(void);
-/* Row balance of the solver kernels (no reference counterpart: a B200
- * scheduling detail under gmres, linsolve.py:107).  Streams `a_dev` (n x n
- * complex128) iters+1 times, measuring each solver CTA's matvec speed, and
- * from then on splits rows in proportion to it (the slow SMs of a B200 under
- * full-GPU contention finish ~5 % later with equal splits).  stats_host
- * (double[4], may be NULL): per-CTA matvec time spread and mean in us, equal
- * split then calibrated split.  ewb_reset_row_balance restores equal splits. */
-int ewb_calibrate_rows(const void* a_dev, int64_t n, int32_t iters, double* stats_host,
-                       void* stream);
-int ewb_reset_row_balance(void* stream);
-
 /* Whole restarted right-preconditioned GMRES solve in one cooperative launch
  * (linsolve.py:107-210).  pinv_dev may be NULL (no preconditioner); x_dev
  * holds x0 when has_x0 != 0 and receives the solution; hist_dev receives the
  * residual history (init, then one estimate per iteration).  ax0_dev
  * (optional, used only with has_x0) holds A x0 when the caller already has
  * it (ewb_sem_guess returns it): the initial residual b - A x0
- * (linsolve.py:144) then costs no pass over A.
+ * (linsolve.py:144) then costs no pass over A unless it already meets tol.
+ * Restart residuals are formed from the cycle's stored products; every exit
+ * (converged or maxiter) is decided on, and reports, the literal
+ * ||b - A x|| / ||b|| (linsolve.py:200-205), one pass over A.
  * workspace: ewb_gmres_workspace_bytes(n, restart) bytes of device memory. */
 int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart);
 int ewb_gmres(const void* a_dev, const void* b_dev, const void* pinv_dev, void* x_dev,
@@ -201,13 +197,45 @@ int ewb_gmres(const void* a_dev, const void* b_dev, const void* pinv_dev, void* 
               ewb_gmres_result* result_dev, void* stream);
 
 /* Least-squares extrapolated initial guess (sem_initial_guess,
- * linsolve.py:213-242).  x_hist_dev: K history columns, newest first,
+ * linsolve.py:213-242), K in [1, 8].  x_hist_dev: K history columns, newest first,
  * column c at x_hist_dev + c*n; writes x0_dev (n) and, if ax0_dev is not
  * NULL, A x0 = (A X) s from the same products (for ewb_gmres). */
 int64_t ewb_sem_workspace_bytes(int64_t n, int32_t K);
 int ewb_sem_guess(const void* a_dev, const void* b_dev, const void* x_hist_dev, int32_t K,
                   int64_t n, double rank_tol, void* x0_dev, void* ax0_dev, void* workspace_dev,
                   int64_t workspace_bytes, ewb_sem_result* result_dev, void* stream);
+
+/* The same guess from caller-supplied products y_hist_dev = A X (K columns,
+ * column c at +c*n) — the matrix-free seam, where Y comes from one
+ * ewb_matfree_apply pass (linsolve.py:226-242 without the matvecs). */
+int ewb_sem_from_products(const void* b_dev, const void* x_hist_dev, const void* y_hist_dev,
+                          int32_t K, int64_t n, double rank_tol, void* x0_dev, void* ax0_dev,
+                          void* workspace_dev, int64_t workspace_bytes,
+                          ewb_sem_result* result_dev, void* stream);
+
+/* Restarted right-preconditioned GMRES around an operator applied by the
+ * caller (the matrix-free seam gmres(apply_a=callable), linsolve.py:73-77,
+ * 107-210).  All solver state stays on the device (ewb_op_head at the start
+ * of the workspace).  Phases (cooperative launches): 0 begin, 1 Arnoldi step
+ * on w = A z, 2 cycle end (back substitution, x update), 3 settle (literal
+ * residual b - A x).  The host enqueues
+ *   begin; apply(lit); settle;  { apply(cycle); step } x chunk; cycle_end; apply(lit); settle
+ * and reads `done` once per chunk; apply(cycle) / apply(lit) are operator
+ * applications z -> w (or vt/vu -> w for ewb_matfree_apply) gated on the
+ * gate words (ewb_opgmres_buffers): with the gate at 0 they must do no work,
+ * which ewb_matfree_apply's gate_dev does.  Every exit is decided on, and
+ * reports, the literal ||b - A x|| / ||b||.  pinv_dev (n/3,3,3) or NULL;
+ * kinds_dev (n) NEUMANN/DIRICHLET or NULL (vt = z), split_u: also write
+ * vu = -mask_D z. */
+int64_t ewb_opgmres_workspace_bytes(int64_t n, int32_t restart);
+int ewb_opgmres_buffers(void* workspace_dev, int64_t n, int32_t restart, void** z_dev,
+                        void** vt_dev, void** vu_dev, void** w_dev, int32_t** gate_cycle_dev,
+                        int32_t** gate_literal_dev);
+int ewb_opgmres_phase(int32_t phase, void* workspace_dev, int64_t workspace_bytes,
+                      const void* b_dev, void* x_dev, int32_t has_x0, const void* ax0_dev,
+                      const void* pinv_dev, const uint8_t* kinds_dev, int32_t split_u, int64_t n,
+                      double tol, int32_t restart, int32_t maxiter, double* hist_dev,
+                      int32_t hist_cap, void* stream);
 
 /* conjugate_fill + window_weights + inverse_mft (transform.py:137-203) for D
  * columns at once.  half_dev: (n_half, D) complex (row k = frequency k);
@@ -224,11 +252,14 @@ int ewb_window_idft(const void* half_dev, int64_t n_half, int64_t D, int32_t win
  * vu = -mask_D v; b uses vt = -mask_D p, vu = mask_N p (assembly.py:293-296).
  * vu_dev may be NULL (all-Neumann: U not applied).  If pinv_dev is non-NULL
  * the inverse 3x3 diagonal blocks of A (kinds_dev mixes the columns) are
- * written too (block_diag_precond, linsolve.py:80-104). */
+ * written too (block_diag_precond, linsolve.py:80-104).  gate_dev (device
+ * int32, nullable): when *gate_dev == 0 at execution time the application
+ * does no work (ewb_opgmres_*). */
 int64_t ewb_matfree_workspace_bytes(const ewb_ctx* ctx, int32_t K);
 int ewb_matfree_apply(ewb_ctx* ctx, double omega_re, double omega_im, const void* vt_dev,
                       const void* vu_dev, int32_t K, void* y_dev, const uint8_t* kinds_dev,
-                      void* pinv_dev, void* workspace_dev, int64_t workspace_bytes, void* stream);
+                      void* pinv_dev, void* workspace_dev, int64_t workspace_bytes,
+                      const int32_t* gate_dev, void* stream);
 
 /* Pair-kernel microbenchmark (BASELINE cfg3): P points x M triangles x F
  * frequencies with gauss7 on every pair (pair_geometry + integrated_blocks,

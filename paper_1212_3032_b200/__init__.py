@@ -16,15 +16,15 @@ from .assembly import (  # noqa: F401
     DIRICHLET, NEUMANN, Assembler, BoundaryConditionError, BoundaryConditionSet, DenseSystem,
     apply_bcs, assemble_tu, scatter_solution,
 )
-from .config import ConfigError, Probe, SweepConfig, parse_config  # noqa: F401
 from .driver import SweepError, SweepResult, emit_outputs, run_sweep  # noqa: F401
 from .linsolve import (  # noqa: F401
     SolutionHistory, SolveStats, block_diag_precond, gmres, sem_initial_guess,
 )
 from .material import Material, wave_speeds, wavenumbers  # noqa: F401
 from .matfree import MatrixFreeOperator  # noqa: F401
-from .mesh import TriangleMesh, generate_box_mesh, generate_icosphere, merge_meshes  # noqa: F401
 from .quadrature import QuadratureSet  # noqa: F401
+from .spec import Probe, SweepSpec  # noqa: F401
+from .surface import SurfaceMesh  # noqa: F401
 from .transform import (  # noqa: F401
     Spectrum, SpectrumSymmetryError, TimeSignal, conjugate_fill, eta_from_kappa,
     forward_mft, frequency_grid, inverse_mft, window_weights,

@@ -16,23 +16,23 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_NAME = "libewbem_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 
-# Every symbol include/ewbem_b200.h declares (checked by tests/test_capi.py).
+# Every symbol include/ewbem_b200.h declares (checked by tests/test_host.py).
 EXPORTS = (
     "ewb_abi_version", "ewb_last_error", "ewb_launch_count", "ewb_ctx_create", "ewb_ctx_destroy",
-    "ewb_ctx_set_exterior", "ewb_ctx_counts", "ewb_static_rowsums", "ewb_static_tu",
+    "ewb_ctx_set_exterior", "ewb_ctx_counts", "ewb_ctx_pair_lists", "ewb_static_rowsums", "ewb_static_tu",
     "ewb_assemble_tu",
-    "ewb_assemble_system", "ewb_assemble_system_multi", "ewb_assemble_system_multi_begin",
-    "ewb_assemble_system_multi_finish", "ewb_assemble_system_multi_self", "ewb_calibrate_rows",
-    "ewb_reset_row_balance", "ewb_ctx_flags", "ewb_ctx_flags_async", "ewb_apply_bcs", "ewb_blockdiag_inverse",
+    "ewb_assemble_system", "ewb_assemble_system_multi", "ewb_ctx_flags", "ewb_ctx_flags_async", "ewb_apply_bcs", "ewb_blockdiag_inverse",
     "ewb_gemv_batched", "ewb_set_solver_ctas", "ewb_solver_ctas",
     "ewb_gmres_workspace_bytes", "ewb_gmres",
-    "ewb_sem_workspace_bytes", "ewb_sem_guess", "ewb_window_idft",
+    "ewb_sem_workspace_bytes", "ewb_sem_guess", "ewb_sem_from_products",
+    "ewb_opgmres_workspace_bytes", "ewb_opgmres_buffers", "ewb_opgmres_phase", "ewb_window_idft",
     "ewb_matfree_workspace_bytes", "ewb_matfree_apply",
     "ewb_pair_kernels_blocks", "ewb_pair_kernels_workspace_bytes",
     "ewb_pair_kernels_reduce", "ewb_fp64_peak_probe",
 )
 
 EWB_OK, EWB_ERR_INVALID, EWB_ERR_CUDA, EWB_ERR_NONFINITE = 0, 1, 2, 3
+ABI_VERSION = 4
 
 
 class NativeUnavailable(RuntimeError):
@@ -64,16 +64,12 @@ _SIGS = {
     "ewb_ctx_destroy": (I32, [P]),
     "ewb_ctx_counts": (I32, [P, P]),
     "ewb_ctx_set_exterior": (I32, [P, I32, P]),
+    "ewb_ctx_pair_lists": (I32, [P, P, P, P, P, P, P]),
     "ewb_static_rowsums": (I32, [P, P, P]),
     "ewb_static_tu": (I32, [P, P, P, P]),
     "ewb_assemble_tu": (I32, [P, D, D, P, P, P]),
     "ewb_assemble_system": (I32, [P, D, D, P, P, P, P, P, P]),
     "ewb_assemble_system_multi": (I32, [P, I32, P, P, P, P, P, P, P, P, P]),
-    "ewb_assemble_system_multi_begin": (I32, [P, I32, P, P, P, P, P, P, P, P, I32, P]),
-    "ewb_assemble_system_multi_finish": (I32, [P, P]),
-    "ewb_assemble_system_multi_self": (I32, [P, P]),
-    "ewb_calibrate_rows": (I32, [P, I64, I32, P, P]),
-    "ewb_reset_row_balance": (I32, [P]),
     "ewb_ctx_flags": (I32, [P, P, P, P]),
     "ewb_ctx_flags_async": (I32, [P, P, P]),
     "ewb_apply_bcs": (I32, [P, P, P, P, I64, P, P, P]),
@@ -85,9 +81,14 @@ _SIGS = {
     "ewb_gmres": (I32, [P, P, P, P, I32, P, I64, D, I32, I32, P, I64, P, I32, P, P]),
     "ewb_sem_workspace_bytes": (I64, [I64, I32]),
     "ewb_sem_guess": (I32, [P, P, P, I32, I64, D, P, P, P, I64, P, P]),
+    "ewb_sem_from_products": (I32, [P, P, P, I32, I64, D, P, P, P, I64, P, P]),
+    "ewb_opgmres_workspace_bytes": (I64, [I64, I32]),
+    "ewb_opgmres_buffers": (I32, [P, I64, I32, P, P, P, P, P, P]),
+    "ewb_opgmres_phase": (I32, [I32, P, I64, P, P, I32, P, P, P, I32, I64, D, I32, I32, P, I32,
+                                P]),
     "ewb_window_idft": (I32, [P, I64, I64, I32, D, D, P, P, P]),
     "ewb_matfree_workspace_bytes": (I64, [P, I32]),
-    "ewb_matfree_apply": (I32, [P, D, D, P, P, I32, P, P, P, P, I64, P]),
+    "ewb_matfree_apply": (I32, [P, D, D, P, P, I32, P, P, P, P, I64, P, P]),
     "ewb_pair_kernels_blocks": (I32, [P, I64, P, I64, P, I32, D, D, D, P, P, P]),
     "ewb_pair_kernels_workspace_bytes": (I64, [I64, I64, I32]),
     "ewb_pair_kernels_reduce": (I32, [P, I64, P, I64, P, P, I32, D, D, D, P, P, P, I64, P]),
@@ -100,8 +101,7 @@ def load(path: os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    # EWB_LIB: an A/B build variant (tools/build_variant.py) instead of the default
-    p = Path(path) if path else Path(os.environ.get("EWB_LIB", LIB_PATH))
+    p = Path(path) if path else LIB_PATH
     if not p.exists():
         raise NativeUnavailable(
             f"{p} is not built; run `python -m paper_1212_3032_b200.build` "
@@ -111,7 +111,7 @@ def load(path: os.PathLike | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.ewb_abi_version() != 3:
+    if lib.ewb_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libewbem_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _lib
 from .material import Material
-from .mesh import TriangleMesh
+from .surface import corner_arrays
 from .quadrature import QuadratureSet, device_rule_tables, gauss_legendre_tables
 
 log = logging.getLogger(__name__)
@@ -52,7 +52,7 @@ class BoundaryConditionSet:
         return cls(kind=np.zeros((n_elements, 3), dtype=np.uint8),
                    signal_index=np.zeros((n_elements, 3), dtype=np.int32))
 
-    def set_region(self, mesh: TriangleMesh, region_tag: int, components, kind: int,
+    def set_region(self, mesh, region_tag: int, components, kind: int,
                    signal_index: int) -> None:
         elements = np.flatnonzero(mesh.region_tag == region_tag)
         if elements.size == 0:
@@ -108,7 +108,7 @@ def _as_device(a, dtype):
 class Assembler:
     """Device-resident per-mesh context + per-frequency assembly (assembly.py:103-254)."""
 
-    def __init__(self, mesh: TriangleMesh, material: Material,
+    def __init__(self, mesh, material: Material,
                  quadrature: QuadratureSet | None = None, exterior: bool = False):
         """``exterior=True`` (not a reference mode; parity unpinned) puts +I on
         every dynamic T diagonal block: c + PV int T = I for an unbounded
@@ -119,7 +119,7 @@ class Assembler:
         self.quad = quadrature or QuadratureSet.default()
         if self.quad != QuadratureSet.default():
             raise NotImplementedError("only the default quadrature ladder is compiled in")
-        v0, v1, v2 = mesh.corner_arrays()
+        v0, v1, v2 = corner_arrays(mesh)
         corners = np.ascontiguousarray(np.stack([v0, v1, v2], axis=1))  # (n_e, 3, 3)
         rules, off, q = device_rule_tables()
         gl8, gl16 = gauss_legendre_tables(self.quad.duffy_radial, self.quad.duffy_angular)
@@ -165,6 +165,20 @@ class Assembler:
         _lib.check(self._lib.ewb_ctx_counts(self._ctx, c))
         return dict(n_elements=c[0], far=c[1], mid=c[2], near=c[3],
                     near_levels={1: c[4], 2: c[5], 3: c[6], 4: c[7]})
+
+    def pair_lists(self) -> dict:
+        """The near / mid pair tables as host CSR arrays (rows sorted): near_ptr,
+        near_j, near_lvl, mid_ptr, mid_j (assembly.py:132-161's buckets)."""
+        pc = self.pair_counts()
+        n = pc["n_elements"]
+        out = dict(near_ptr=np.empty(n + 1, np.int32), near_j=np.empty(pc["near"], np.int32),
+                   near_lvl=np.empty(pc["near"], np.int32), mid_ptr=np.empty(n + 1, np.int32),
+                   mid_j=np.empty(pc["mid"], np.int32))
+        _lib.check(self._lib.ewb_ctx_pair_lists(
+            self._ctx, *[out[k].ctypes.data for k in ("near_ptr", "near_j", "near_lvl",
+                                                      "mid_ptr", "mid_j")],
+            _lib.stream_handle()), "ewb_ctx_pair_lists")
+        return out
 
     def point_evals(self) -> int:
         """Quadrature-point evaluations per dense assembly."""
@@ -307,48 +321,6 @@ class Assembler:
                     log.warning("%d singular 3x3 diagonal blocks; identity fallback", fl[f, 1])
         return out
 
-    # The batch assembly in three steps so that it can overlap the previous
-    # batch's solves (DeviceSweep.run): begin on a side stream beside a solver
-    # restricted to the other SMs, finish + self on the solver's stream.
-    def assemble_system_multi_begin(self, omegas, bcs, prescribed, out, flags, n_sms: int, stream):
-        """Persistent far-pair grid on ``n_sms`` SMs + mid/near pairs, on ``stream``."""
-        torch = _torch()
-        om = np.asarray([complex(w) for w in omegas], dtype=complex)
-        nf = len(om)
-        if not 1 <= nf <= self.MAX_BATCH:
-            raise ValueError(f"batch of {nf} frequencies (1..{self.MAX_BATCH})")
-        if np.any(om == 0):
-            raise ValueError("omega == 0 takes the static path (assemble_system)")
-        kinds = np.ascontiguousarray(bcs.flat_kind(), dtype=np.uint8)
-        n = self.n
-        p = _as_device(prescribed, torch.complex128)
-        if tuple(p.shape) != (nf, n):
-            raise ValueError("prescribed spectra must be (nf, N)")
-        kd = getattr(out, "_kinds_dev", None)
-        if kd is None or not np.array_equal(getattr(out, "_kinds_host", None), kinds):
-            kd = torch.from_numpy(kinds).cuda()
-            out._kinds_dev, out._kinds_host = kd, kinds
-        out._keep_p = p   # alive until the kernels that read it have run
-        ore = np.ascontiguousarray(om.real)
-        oim = np.ascontiguousarray(om.imag)
-        _lib.check(self._lib.ewb_assemble_system_multi_begin(
-            self._ctx, nf, ore.ctypes.data, oim.ctypes.data, _lib.ptr(kd), _lib.ptr(p),
-            _lib.ptr(out.A), _lib.ptr(out.b), _lib.ptr(out.pinv), _lib.ptr(flags), int(n_sms),
-            _lib.stream_handle(stream)), "ewb_assemble_system_multi_begin")
-        out.nf = nf
-        out.unknown_kind = kinds.copy()
-        return out
-
-
-    def assemble_system_multi_finish(self, stream=None):
-        _lib.check(self._lib.ewb_assemble_system_multi_finish(self._ctx, _lib.stream_handle(stream)),
-                   "ewb_assemble_system_multi_finish")
-
-
-    def assemble_system_multi_self(self, stream=None):
-        _lib.check(self._lib.ewb_assemble_system_multi_self(self._ctx, _lib.stream_handle(stream)),
-                   "ewb_assemble_system_multi_self")
-
 
 @dataclass
 class SystemBatch:
@@ -374,7 +346,7 @@ class SystemBatch:
                            pinv=self.pinv[f])
 
 
-def assemble_tu(mesh: TriangleMesh, material: Material, omega: complex,
+def assemble_tu(mesh, material: Material, omega: complex,
                 quadrature: QuadratureSet | None = None):
     return Assembler(mesh, material, quadrature).assemble_tu(omega)
 

@@ -711,17 +711,9 @@ __device__ __forceinline__ unsigned expo(double v) {
 }
 __device__ __forceinline__ unsigned expo(cplx v) { return max(expo(v.re), expo(v.im)); }
 
-// PERSIST: warps pull items (row group x column tile) from a global counter
-// until none is left, so a small resident grid (a few SMs next to the
-// solver) and a later full-GPU grid can share one batch's far pairs
-// (ewb_assemble_system_multi_begin / _finish).  Every item writes the same
-// values whichever warp takes it: results stay deterministic.
-constexpr int kFarPersistThreads = 384;   // one block per SM (smem-limited)
-template <bool RECUR, bool PERSIST>
-__global__ void __launch_bounds__(PERSIST ? kFarPersistThreads : 128,
-                                  PERSIST ? 1 : EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
-                                                                    SysBatch o,
-                                                                    unsigned long long* counter) {
+template <bool RECUR>
+__global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
+                                                                      SysBatch o) {
   extern __shared__ double sm_far[];
   const int BD = blockDim.x;
   const int tid = threadIdx.x;
@@ -740,13 +732,8 @@ __global__ void __launch_bounds__(PERSIST ? kFarPersistThreads : 128,
   const long long N = 3LL * g.n_e;
   const FreqConst& fc0 = fb.fc[0];   // material constants (member-independent)
   const int nf = fb.nf;
-  long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (PERSIST) {
-    unsigned long long w0 = 0;
-    if (lane == 0) w0 = atomicAdd(counter, 1ull);
-    warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
-  }
-  while (warp < nitems) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp < nitems) {
     const int rg = (int)(warp / ntile), t = (int)(warp % ntile);
     const int j = t * 32 + lane;
     const bool jv = j < g.n_e;
@@ -871,13 +858,7 @@ __global__ void __launch_bounds__(PERSIST ? kFarPersistThreads : 128,
         }
       }
     }
-    if (!PERSIST) break;
-    {
-      unsigned long long w0 = 0;
-      if (lane == 0) w0 = atomicAdd(counter, 1ull);
-      warp = (long long)__shfl_sync(0xffffffffu, w0, 0);
-    }
-  }  // item loop
+  }
 }
 
 // Mid pairs (tier 1, gauss7) from the CSR list: thread = (pair, member).
@@ -1426,7 +1407,6 @@ static cudaError_t ensure_multi_scratch(Context& c, int nf) {
   c.nf_cap = 0;
   cudaError_t err = cudaSuccess;
   const size_t n3 = 3 * (size_t)c.n_e;
-  if (!c.far_counter) c.far_counter = dalloc<unsigned long long>(c, 1, err);
   c.bpart_m = dalloc<cplx>(c, (size_t)nf * c.n_tiles * n3, err);
   c.bmid_m = dalloc<cplx>(c, (size_t)nf * 3 * c.n_mid + 1, err);
   c.bnear_m = dalloc<cplx>(c, (size_t)nf * 3 * c.n_near + 1, err);
@@ -1437,20 +1417,16 @@ static cudaError_t ensure_multi_scratch(Context& c, int nf) {
 static void far_attrs() {
   static bool attr = false;
   if (attr) return;
-  cudaFuncSetAttribute(k_far_multi<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_far_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kFarMultiSmem);
-  cudaFuncSetAttribute(k_far_multi<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_far_multi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kFarMultiSmem);
-  cudaFuncSetAttribute(k_far_multi<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)far_smem(kFarPersistThreads));
-  cudaFuncSetAttribute(k_far_multi<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)far_smem(kFarPersistThreads));
   attr = true;
 }
 
 static FreqBatch make_batch(Context& c, int nf, const double* ore, const double* oim);
 static cudaError_t launch_multi_rest(Context& c, const FreqBatch& fb, const SysBatch& o,
-                                     bool midnear, bool self, cudaStream_t s);
+                                     cudaStream_t s);
 
 cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
                                          const double* oim, const uint8_t* kinds,
@@ -1467,10 +1443,10 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
   const unsigned fb_blocks = blocks_for(warps * 32, 128);
   far_attrs();
   if (recur)
-    EWB_NOTE k_far_multi<true, false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o, nullptr);
+    EWB_NOTE k_far_multi<true><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
   else
-    EWB_NOTE k_far_multi<false, false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o, nullptr);
-  return launch_multi_rest(c, fb, o, true, true, s);
+    EWB_NOTE k_far_multi<false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
+  return launch_multi_rest(c, fb, o, s);
 }
 
 static FreqBatch make_batch(Context& c, int nf, const double* ore, const double* oim) {
@@ -1496,66 +1472,19 @@ static FreqBatch make_batch(Context& c, int nf, const double* ore, const double*
   return fb;
 }
 
-// mid / near (and self) kernels of a batch
+// mid, near and self kernels of a batch
 static cudaError_t launch_multi_rest(Context& c, const FreqBatch& fb, const SysBatch& o,
-                                     bool midnear, bool self, cudaStream_t s) {
+                                     cudaStream_t s) {
   const int n = c.n_e, nf = fb.nf;
-  if (midnear && c.n_mid)
+  if (c.n_mid)
     EWB_NOTE k_mid_multi<<<blocks_for((long long)c.n_mid * nf, 128), 128, 0, s>>>(c.g, fb, o,
                                                                                 (int)c.n_mid);
-  if (midnear && c.n_near)
+  if (c.n_near)
     EWB_NOTE k_near_multi<<<blocks_for((long long)c.n_near * 32, 128), 128, 0, s>>>(c.g, fb, o,
                                                                                   c.n_near);
-  if (self)
-    EWB_NOTE k_self_multi<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(
+  EWB_NOTE k_self_multi<<<blocks_for((long long)n * 32, 128), 128, 0, s>>>(
         c.g, fb, o, c.diag_base, c.n_tiles, (int)c.n_mid, c.n_near);
   return cudaGetLastError();
-}
-
-static cudaError_t launch_far_persistent(Context& c, int blocks, cudaStream_t s) {
-  far_attrs();
-  const size_t sm = far_smem(kFarPersistThreads);
-  if (c.pend_fb.recur)
-    EWB_NOTE k_far_multi<true, true><<<blocks, kFarPersistThreads, sm, s>>>(c.g, c.pend_fb,
-                                                                           c.pend_o, c.far_counter);
-  else
-    EWB_NOTE k_far_multi<false, true><<<blocks, kFarPersistThreads, sm, s>>>(c.g, c.pend_fb,
-                                                                            c.pend_o, c.far_counter);
-  return cudaGetLastError();
-}
-
-// Overlapped batch assembly (the sweep assembles batch b+1 while it solves
-// batch b): begin() puts a persistent far-pair grid of `n_sms` one-block-per-
-// SM CTAs on stream `s` (next to a solver restricted to the other SMs, see
-// ewb_set_solver_ctas), followed by the mid and near kernels; finish() runs
-// a full-GPU grid on the same work counter (it takes whatever far items are
-// left); self() builds the diagonal blocks, b and P^{-1} once both streams'
-// work is done (the caller orders it after begin's stream).
-cudaError_t launch_assemble_multi_begin(Context& c, int nf, const double* ore, const double* oim,
-                                        const uint8_t* kinds, const cplx* prescribed, cplx* A,
-                                        cplx* b, cplx* pinv, int* flags, int n_sms,
-                                        cudaStream_t s) {
-  if (nf < 1 || nf > kMaxBatch || n_sms < 1) return cudaErrorInvalidValue;
-  cudaError_t err = ensure_multi_scratch(c, nf);
-  if (err) return err;
-  c.pend_fb = make_batch(c, nf, ore, oim);
-  c.pend_o = SysBatch{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
-  err = cudaMemsetAsync(c.far_counter, 0, sizeof(unsigned long long), s);
-  if (err) return err;
-  err = launch_far_persistent(c, n_sms, s);
-  if (err) return err;
-  return launch_multi_rest(c, c.pend_fb, c.pend_o, true, false, s);
-}
-
-cudaError_t launch_assemble_multi_finish(Context& c, cudaStream_t s) {
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return launch_far_persistent(c, sms, s);
-}
-
-cudaError_t launch_assemble_multi_self(Context& c, cudaStream_t s) {
-  return launch_multi_rest(c, c.pend_fb, c.pend_o, false, true, s);
 }
 
 }  // namespace ewb

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -125,6 +126,23 @@ int ewb_ctx_counts(const ewb_ctx* ctx, int64_t* counts) {
   return EWB_OK;
 }
 
+int ewb_ctx_pair_lists(const ewb_ctx* ctx, int32_t* near_ptr, int32_t* near_j, int32_t* near_lvl,
+                       int32_t* mid_ptr, int32_t* mid_j, void* stream) {
+  if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_pair_lists: null context");
+  const ewb::Geo& g = ctx->c.g;
+  const size_t n1 = sizeof(int32_t) * (ctx->c.n_e + 1);
+  const size_t nn = sizeof(int32_t) * ctx->c.n_near, nm = sizeof(int32_t) * ctx->c.n_mid;
+  struct { void* dst; const void* src; size_t bytes; } cp[] = {
+      {near_ptr, g.near_ptr, n1}, {near_j, g.near_j, nn}, {near_lvl, g.near_lvl, nn},
+      {mid_ptr, g.mid_ptr, n1}, {mid_j, g.mid_j, nm}};
+  for (auto& c : cp)
+    if (c.dst && c.bytes)
+      EWB_CUDA(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, S(stream)),
+               "ewb_ctx_pair_lists");
+  EWB_CUDA(cudaStreamSynchronize(S(stream)), "ewb_ctx_pair_lists");
+  return EWB_OK;
+}
+
 int ewb_static_rowsums(ewb_ctx* ctx, double* out, void* stream) {
   if (!ctx || !out) return fail(EWB_ERR_INVALID, "ewb_static_rowsums: null argument");
   EWB_CUDA(cudaMemcpyAsync(out, ctx->c.rowsums, sizeof(double) * 9 * ctx->c.n_e,
@@ -186,37 +204,6 @@ int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* ore, const
   return EWB_OK;
 }
 
-int ewb_assemble_system_multi_begin(ewb_ctx* ctx, int32_t nf, const double* ore,
-                                    const double* oim, const uint8_t* kinds, const void* p,
-                                    void* a, void* b, void* pinv, int32_t* flags, int32_t n_sms,
-                                    void* stream) {
-  if (!ctx || !ore || !oim || !kinds || !p || !a || !b || !pinv || !flags)
-    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_begin: null argument");
-  if (nf < 1 || nf > EWB_MAX_BATCH || n_sms < 1)
-    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_begin: bad nf or n_sms");
-  for (int f = 0; f < nf; ++f)
-    if (int rc = check_omega(ore[f], oim[f], "ewb_assemble_system_multi_begin")) return rc;
-  EWB_CUDA(ewb::launch_assemble_multi_begin(ctx->c, nf, ore, oim, kinds, (const ewb::cplx*)p,
-                                            (ewb::cplx*)a, (ewb::cplx*)b, (ewb::cplx*)pinv, flags,
-                                            n_sms, S(stream)),
-           "ewb_assemble_system_multi_begin");
-  return EWB_OK;
-}
-
-int ewb_assemble_system_multi_finish(ewb_ctx* ctx, void* stream) {
-  if (!ctx || ctx->c.pend_fb.nf < 1)
-    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_finish: no batch begun");
-  EWB_CUDA(ewb::launch_assemble_multi_finish(ctx->c, S(stream)), "ewb_assemble_system_multi_finish");
-  return EWB_OK;
-}
-
-int ewb_assemble_system_multi_self(ewb_ctx* ctx, void* stream) {
-  if (!ctx || ctx->c.pend_fb.nf < 1)
-    return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi_self: no batch begun");
-  EWB_CUDA(ewb::launch_assemble_multi_self(ctx->c, S(stream)), "ewb_assemble_system_multi_self");
-  return EWB_OK;
-}
-
 int ewb_ctx_flags(ewb_ctx* ctx, int32_t* nonfinite, int32_t* singular, void* stream) {
   if (!ctx) return fail(EWB_ERR_INVALID, "ewb_ctx_flags: null argument");
   int h[4] = {0, 0, 0, 0};
@@ -274,18 +261,6 @@ int ewb_set_solver_ctas(int32_t ctas) {
 
 int32_t ewb_solver_ctas(void) { return ewb::solver_grid_blocks(); }
 
-int ewb_calibrate_rows(const void* a, int64_t n, int32_t iters, double* stats, void* stream) {
-  if (!a || n < 1 || iters < 0) return fail(EWB_ERR_INVALID, "ewb_calibrate_rows: bad argument");
-  EWB_CUDA(ewb::calibrate_rows((const ewb::cplx*)a, n, iters, stats, S(stream)),
-           "ewb_calibrate_rows");
-  return EWB_OK;
-}
-
-int ewb_reset_row_balance(void* stream) {
-  EWB_CUDA(ewb::reset_row_balance(S(stream)), "ewb_reset_row_balance");
-  return EWB_OK;
-}
-
 // workspace layout: r, w, z (3n), V ((restart+1) n), H, partial
 int64_t ewb_gmres_workspace_bytes(int64_t n, int32_t restart) {
   int64_t cpl = 16;
@@ -327,24 +302,6 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   g.dpart = g.Gram + (int64_t)(ewb::kMaxRestart + 1) * ewb::kMaxRestart;
   g.partial = (double*)(g.dpart + 2 * (int64_t)ewb::solver_grid_max() *
                                       (2 * ewb::kMaxRestart + 2));
-  {
-    const char* env = getenv("EWB_GMRES_ORTHO");
-    g.ortho = env ? atoi(env) : 0;
-    // EWB_TRUE_RESIDUAL_PASS=1: the cycle's true residual by a fresh pass
-    // over A (as linsolve.py:200-201 literally does) instead of W y
-    const char* tr = getenv("EWB_TRUE_RESIDUAL_PASS");
-    if ((tr && atoi(tr) == 1) || g.ortho != 0) g.W = nullptr;
-  }
-  g.probe = nullptr;
-  g.probe_cap = 0;
-  {
-    // diagnostics: EWB_GMRES_PROBE=<device address> enables the phase trace
-    const char* env = getenv("EWB_GMRES_PROBE");
-    if (env) {
-      g.probe = (unsigned long long*)strtoull(env, nullptr, 0);
-      g.probe_cap = 1 << 16;
-    }
-  }
   g.hist = hist;
   g.out = (ewb::GmresOut*)result;
   g.n = n;
@@ -367,7 +324,7 @@ int ewb_sem_guess(const void* a, const void* b, const void* xh, int32_t K, int64
                   ewb_sem_result* result, void* stream) {
   if (!a || !b || !xh || !x0 || !ws || !result || n < 1)
     return fail(EWB_ERR_INVALID, "ewb_sem_guess: bad argument");
-  if (K < 1 || K > ewb::kMaxSem) return fail(EWB_ERR_INVALID, "ewb_sem_guess: K must be in [1, 4]");
+  if (K < 1 || K > ewb::kMaxSem) return fail(EWB_ERR_INVALID, "ewb_sem_guess: K must be in [1, 8]");
   if (ws_bytes < ewb_sem_workspace_bytes(n, K))
     return fail(EWB_ERR_INVALID, "ewb_sem_guess: workspace too small");
   ewb::SemArgs s{};
@@ -385,6 +342,102 @@ int ewb_sem_guess(const void* a, const void* b, const void* xh, int32_t K, int64
   s.K = K;
   s.rank_tol = rank_tol;
   EWB_CUDA(ewb::launch_sem(s, S(stream)), "ewb_sem_guess");
+  return EWB_OK;
+}
+
+int ewb_sem_from_products(const void* b, const void* xh, const void* yh, int32_t K, int64_t n,
+                          double rank_tol, void* x0, void* ax0, void* ws, int64_t ws_bytes,
+                          ewb_sem_result* result, void* stream) {
+  if (!b || !xh || !yh || !x0 || !ws || !result || n < 1)
+    return fail(EWB_ERR_INVALID, "ewb_sem_from_products: bad argument");
+  if (K < 1 || K > ewb::kMaxSem)
+    return fail(EWB_ERR_INVALID, "ewb_sem_from_products: K must be in [1, 8]");
+  if (ws_bytes < ewb_sem_workspace_bytes(n, K))
+    return fail(EWB_ERR_INVALID, "ewb_sem_from_products: workspace too small");
+  ewb::SemArgs s{};
+  auto* base = (ewb::cplx*)ws;
+  s.b = (const ewb::cplx*)b;
+  s.X = (const ewb::cplx*)xh;
+  s.Y = (ewb::cplx*)yh;
+  s.Q = base;
+  s.partial = (double*)(base + (int64_t)K * n);
+  s.x0 = (ewb::cplx*)x0;
+  s.ax0 = (ewb::cplx*)ax0;
+  s.out = (ewb::SemOut*)result;
+  s.n = n;
+  s.K = K;
+  s.rank_tol = rank_tol;
+  EWB_CUDA(ewb::launch_sem_products(s, S(stream)), "ewb_sem_from_products");
+  return EWB_OK;
+}
+
+// operator-GMRES workspace: state | z vt vu w r rs (6n) | V ((restart+1) n) |
+// W (restart n) | partials
+static_assert(sizeof(ewb_op_head) == sizeof(ewb::OpHead), "ewb_op_head mirrors OpHead");
+static_assert(offsetof(ewb_op_head, final_residual) == offsetof(ewb::OpHead, final_res),
+              "ewb_op_head mirrors OpHead");
+static int64_t op_state_bytes() { return ((int64_t)sizeof(ewb::OpState) + 255) / 256 * 256; }
+
+int64_t ewb_opgmres_workspace_bytes(int64_t n, int32_t restart) {
+  if (n < 1 || restart < 1 || restart > ewb::kMaxRestart) return -1;
+  const int64_t G = ewb::solver_grid_max();
+  return op_state_bytes() + 16 * (6 * n + (int64_t)(2 * restart + 1) * n) + 8 * 2 * G * 16;
+}
+
+int ewb_opgmres_buffers(void* ws, int64_t n, int32_t restart, void** z, void** vt, void** vu,
+                        void** w, int32_t** gate_cycle, int32_t** gate_literal) {
+  if (!ws || n < 1 || restart < 1 || restart > ewb::kMaxRestart)
+    return fail(EWB_ERR_INVALID, "ewb_opgmres_buffers: bad argument");
+  auto* st = (ewb::OpState*)ws;
+  auto* v = (ewb::cplx*)((unsigned char*)ws + op_state_bytes());
+  if (z) *z = v;
+  if (vt) *vt = v + n;
+  if (vu) *vu = v + 2 * n;
+  if (w) *w = v + 3 * n;
+  if (gate_cycle) *gate_cycle = &st->h.in_cycle;
+  if (gate_literal) *gate_literal = &st->h.lit_pending;
+  return EWB_OK;
+}
+
+int ewb_opgmres_phase(int32_t phase, void* ws, int64_t ws_bytes, const void* b, void* x,
+                      int32_t has_x0, const void* ax0, const void* pinv, const uint8_t* kinds,
+                      int32_t split_u, int64_t n, double tol, int32_t restart, int32_t maxiter,
+                      double* hist, int32_t hist_cap, void* stream) {
+  if (phase < 0 || phase > 3 || !ws || !b || !x || !hist || n < 1)
+    return fail(EWB_ERR_INVALID, "ewb_opgmres_phase: bad argument");
+  if (!(tol > 0.0 && tol < 1.0)) return fail(EWB_ERR_INVALID, "tol must be in (0, 1)");
+  if (restart < 1 || restart > ewb::kMaxRestart)
+    return fail(EWB_ERR_INVALID, "ewb_opgmres_phase: restart must be in [1, 128]");
+  if (maxiter < 0) return fail(EWB_ERR_INVALID, "ewb_opgmres_phase: maxiter must be >= 0");
+  if ((pinv || kinds) && n % 3)
+    return fail(EWB_ERR_INVALID, "ewb_opgmres_phase: preconditioner/kinds need n % 3 == 0");
+  if (ws_bytes < ewb_opgmres_workspace_bytes(n, restart))
+    return fail(EWB_ERR_INVALID, "ewb_opgmres_phase: workspace too small");
+  ewb::OpArgs a{};
+  a.st = (ewb::OpState*)ws;
+  auto* v = (ewb::cplx*)((unsigned char*)ws + op_state_bytes());
+  a.z = v;
+  a.vt = v + n;
+  a.vu = split_u ? v + 2 * n : nullptr;
+  a.w = v + 3 * n;
+  a.r = v + 4 * n;
+  a.rs = v + 5 * n;
+  a.V = v + 6 * n;
+  a.W = a.V + (int64_t)(restart + 1) * n;
+  a.partial = (double*)(a.W + (int64_t)restart * n);
+  a.b = (const ewb::cplx*)b;
+  a.x = (ewb::cplx*)x;
+  a.ax0 = has_x0 ? (const ewb::cplx*)ax0 : nullptr;
+  a.pinv = (const ewb::cplx*)pinv;
+  a.kinds = kinds;
+  a.hist = hist;
+  a.hist_cap = hist_cap;
+  a.n = n;
+  a.restart = restart;
+  a.maxiter = maxiter;
+  a.has_x0 = has_x0;
+  a.tol = tol;
+  EWB_CUDA(ewb::launch_op_gmres(phase, a, S(stream)), "ewb_opgmres_phase");
   return EWB_OK;
 }
 
@@ -443,7 +496,7 @@ namespace ewb {
 size_t mf_workspace_bytes(const Context& c, int K);
 cudaError_t launch_matfree(Context& c, double ore, double oim, const cplx* vt, const cplx* vu,
                            int K, cplx* y, const uint8_t* kinds, cplx* pinv, void* ws,
-                           cudaStream_t s);
+                           const int* gate, cudaStream_t s);
 cudaError_t launch_pair_blocks(const double* x, long long P, const double* tri, long long M,
                                const FreqConst* fcs_dev, int F, const double* b7, const double* w7,
                                cplx* u, cplx* t, cudaStream_t s);
@@ -491,14 +544,14 @@ int64_t ewb_matfree_workspace_bytes(const ewb_ctx* ctx, int32_t K) {
 
 int ewb_matfree_apply(ewb_ctx* ctx, double ore, double oim, const void* vt, const void* vu,
                       int32_t K, void* y, const uint8_t* kinds, void* pinv, void* ws,
-                      int64_t ws_bytes, void* stream) {
+                      int64_t ws_bytes, const int32_t* gate, void* stream) {
   if (!ctx || !vt || !y || !ws) return fail(EWB_ERR_INVALID, "ewb_matfree_apply: null argument");
   if (K < 1 || K > 5) return fail(EWB_ERR_INVALID, "ewb_matfree_apply: K must be in [1, 5]");
   if (int rc = check_omega(ore, oim, "ewb_matfree_apply")) return rc;
   if (ws_bytes < (int64_t)ewb::mf_workspace_bytes(ctx->c, K))
     return fail(EWB_ERR_INVALID, "ewb_matfree_apply: workspace too small");
   EWB_CUDA(ewb::launch_matfree(ctx->c, ore, oim, (const ewb::cplx*)vt, (const ewb::cplx*)vu, K,
-                               (ewb::cplx*)y, kinds, (ewb::cplx*)pinv, ws, S(stream)),
+                               (ewb::cplx*)y, kinds, (ewb::cplx*)pinv, ws, gate, S(stream)),
            "ewb_matfree_apply");
   return EWB_OK;
 }

@@ -164,10 +164,6 @@ struct Context {
   cplx* bpart_m = nullptr;
   cplx* bmid_m = nullptr;
   cplx* bnear_m = nullptr;
-  // overlapped batch assembly (launch_assemble_multi_begin/finish/self)
-  unsigned long long* far_counter = nullptr;
-  FreqBatch pend_fb{};
-  SysBatch pend_o{};
   cudaStream_t stream = nullptr;
 };
 
@@ -196,11 +192,5 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
                                          const double* oim, const uint8_t* kinds,
                                          const cplx* prescribed, cplx* A, cplx* b, cplx* pinv,
                                          int* flags, cudaStream_t s);
-cudaError_t launch_assemble_multi_begin(Context& c, int nf, const double* ore, const double* oim,
-                                        const uint8_t* kinds, const cplx* prescribed, cplx* A,
-                                        cplx* b, cplx* pinv, int* flags, int n_sms,
-                                        cudaStream_t s);
-cudaError_t launch_assemble_multi_finish(Context& c, cudaStream_t s);
-cudaError_t launch_assemble_multi_self(Context& c, cudaStream_t s);
 
 }  // namespace ewb

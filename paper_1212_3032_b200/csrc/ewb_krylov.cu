@@ -26,13 +26,10 @@ namespace cg = cooperative_groups;
 
 namespace ewb {
 
-#ifndef EWB_SOLVE_THREADS
-#define EWB_SOLVE_THREADS 512
-#endif
-constexpr int kSolveThreads = EWB_SOLVE_THREADS;
-// register cap 65536 / (kSolveThreads * kSolveMinBlocks) = 128: with 256 threads a
-// solver CTA leaves half of the register file to co-resident assembly CTAs
-constexpr int kSolveMinBlocks = 512 / kSolveThreads;
+// one 512-thread CTA per SM: register cap 65536 / 512 = 128 per thread
+// (a 256-thread CTA streamed a pass in 749 us instead of 525 us)
+constexpr int kSolveThreads = 512;
+constexpr int kSolveMinBlocks = 1;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kMaxRed = 16;  // doubles per grid reduction
 
@@ -87,56 +84,6 @@ __device__ void grid_sum(cg::grid_group& grid, GridRed& R, double (&v)[C]) {
   R.parity ^= 1;
 }
 
-// y[:, k] = A x[:, k] for K right-hand sides (x, y stored column after
-// column, leading dimension n).  Rows are dealt to warps R at a time.
-template <int RR, int K>
-__device__ void matvec_grid(const cplx* __restrict__ A, long long n, const cplx* x, cplx* y) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long r0 = gw * RR; r0 < n; r0 += nw * RR) {
-    cplx acc[RR][K];
-#pragma unroll
-    for (int a = 0; a < RR; ++a)
-#pragma unroll
-      for (int k = 0; k < K; ++k) acc[a][k] = {0.0, 0.0};
-    const int nr = (int)min((long long)RR, n - r0);
-    if (nr == RR) {
-      const cplx* rowp = A + r0 * n;
-#pragma unroll 2
-      for (long long c = lane; c < n; c += 32) {
-        cplx xv[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) xv[k] = ldg(x + k * n + c);
-#pragma unroll
-        for (int a = 0; a < RR; ++a) {
-          cplx av = ldc(rowp + a * n + c);
-#pragma unroll
-          for (int k = 0; k < K; ++k) cfma(acc[a][k], av, xv[k]);
-        }
-      }
-    } else {
-      for (long long c = lane; c < n; c += 32) {
-        cplx xv[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) xv[k] = ldg(x + k * n + c);
-        for (int a = 0; a < nr; ++a) {
-          cplx av = ldc(A + (r0 + a) * n + c);
-#pragma unroll
-          for (int k = 0; k < K; ++k) cfma(acc[a][k], av, xv[k]);
-        }
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < RR; ++a)
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        warp_sum(acc[a][k]);
-        if (lane == 0 && a < nr) y[k * n + r0 + a] = acc[a][k];
-      }
-  }
-}
-
 // ---------------------------------------------------------------------
 // TMA (cp.async.bulk) matvec.  Row groups of kRR rows are dealt to CTAs
 // round-robin; each CTA streams its groups through a kNS-stage ring of
@@ -171,22 +118,6 @@ struct Ring {
   unsigned evict_first; // L2 policy for A: evict_first (A larger than L2) or evict_last
 };
 
-// Optional L2 residency of part of A: the first kPinRows rows of every CTA's
-// slice are loaded evict_last, the rest evict_first, so ~kPinRows x 148 rows
-// stay in L2 across passes.  Measured (n = 15360): 2 rows lift a standalone
-// GEMV from 6.76 to 6.88 TB/s but slow the cfg2 sweep from 4.02 to 4.09 s
-// (the pinned rows crowd the Krylov basis out of L2), so it is off.
-#ifndef EWB_X_PREFETCH
-#define EWB_X_PREFETCH 0
-#endif
-#ifndef EWB_L2_PREFETCH_TILES
-#define EWB_L2_PREFETCH_TILES 0
-#endif
-#ifndef EWB_PIN_ROWS
-#define EWB_PIN_ROWS 0
-#endif
-constexpr int kPinRows = EWB_PIN_ROWS;
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -203,29 +134,26 @@ __device__ __forceinline__ void ring_init(Ring& R, bool evict_first) {
 }
 
 __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cplx* A, long long n,
-                                           long long row0, int nrows, long long c0, int tc,
-                                           int npin = 0) {
+                                           long long row0, int nrows, long long c0, int tc) {
   const int b = pos % kNS;
   const uint32_t bar = smem_u32(&R.bar[b]);
   const uint32_t bytes = (uint32_t)(nrows * tc * 16);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
-  // policies are made here (issuing thread only) instead of living in
+  // the policy is made here (issuing thread only) instead of living in
   // registers of every thread across the whole solve
-  uint64_t stream_pol, pin_pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pin_pol));
+  uint64_t pol;
   if (R.evict_first)
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(stream_pol));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   else
-    stream_pol = pin_pol;
-  if (kPinRows == 0) npin = 0;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   for (int r = 0; r < nrows; ++r) {
     const uint32_t dst = smem_u32(R.buf + (size_t)b * kStageElems + r * kTC);
     const cplx* src = A + (row0 + r) * n + c0;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-        "l"(src), "r"(tc * 16), "r"(bar), "l"(r < npin ? pin_pol : stream_pol)
+        "l"(src), "r"(tc * 16), "r"(bar), "l"(pol)
         : "memory");
   }
 }
@@ -233,19 +161,6 @@ __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cp
 __device__ __forceinline__ void ring_wait(const Ring& R, unsigned pos) {
   const uint32_t bar = smem_u32(&R.bar[pos % kNS]);
   const uint32_t parity = (pos / kNS) & 1u;
-#ifdef EWB_WAIT_HINT   // experiment: suspend-time hint (ns) for the waiting warps
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity), "n"(EWB_WAIT_HINT)
-      : "memory");
-#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -257,140 +172,6 @@ __device__ __forceinline__ void ring_wait(const Ring& R, unsigned pos) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
-#endif
-}
-
-// y[k] = A x[k] for K vectors (x, y: vector k at +k n), all CTAs cooperate;
-// the caller separates phases with grid.sync().
-template <int K>
-__device__ void matvec_tma(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
-                           cplx* y) {
-  __shared__ cplx s_red[kSolveWarps][kRpt][K];
-  const long long ngroups = (n + kRR - 1) / kRR;
-  const int ntile = (int)((n + kTC - 1) / kTC);
-  const long long mine = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const long long S = mine * ntile;
-  auto coords = [&](long long s, long long& row0, int& nrows, long long& c0, int& tc) {
-    const long long gi = s / ntile;
-    const int t = (int)(s % ntile);
-    row0 = (blockIdx.x + gi * gridDim.x) * kRR;
-    nrows = (int)min((long long)kRR, n - row0);
-    c0 = (long long)t * kTC;
-    tc = (int)min((long long)kTC, n - c0);
-  };
-  if (threadIdx.x == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (long long s = 0; s < S && s < kNS; ++s) {
-      long long row0, c0;
-      int nrows, tc;
-      coords(s, row0, nrows, c0, tc);
-      ring_issue(R, R.pos + (unsigned)s, A, n, row0, nrows, c0, tc);
-    }
-  }
-  const int col = threadIdx.x % kTC, slice = threadIdx.x / kTC;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  cplx acc[kRpt][K];
-#pragma unroll
-  for (int r = 0; r < kRpt; ++r)
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
-  for (long long s = 0; s < S; ++s) {
-    long long row0, c0;
-    int nrows, tc;
-    coords(s, row0, nrows, c0, tc);
-    const unsigned pos = R.pos + (unsigned)s;
-    ring_wait(R, pos);
-    if (col < tc) {
-      cplx xv[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) xv[k] = ldg(x + k * n + c0 + col);
-      const cplx* tile = R.buf + (size_t)(pos % kNS) * kStageElems;
-#pragma unroll
-      for (int r = 0; r < kRpt; ++r) {
-        const int row = slice * kRpt + r;
-        if (row < nrows) {
-          double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + col);
-          cplx av = {a2.x, a2.y};
-#pragma unroll
-          for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[k]);
-        }
-      }
-    }
-    __syncthreads();  // every consumer is done with this stage's buffer
-    if (threadIdx.x == 0 && s + kNS < S) {
-      long long r2, c2;
-      int n2, t2;
-      coords(s + kNS, r2, n2, c2, t2);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      ring_issue(R, pos + kNS, A, n, r2, n2, c2, t2);
-    }
-    if (c0 + tc >= n) {  // last tile of the row group: reduce and store
-#pragma unroll
-      for (int r = 0; r < kRpt; ++r)
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          warp_sum(acc[r][k]);
-          if (lane == 0) s_red[wid][r][k] = acc[r][k];
-          acc[r][k] = {0.0, 0.0};
-        }
-      __syncthreads();
-      if (threadIdx.x < kRR * K) {
-        const int row = threadIdx.x / K, k = threadIdx.x % K;
-        const int h = row / kRpt, r = row % kRpt;
-        constexpr int wps = kSolveWarps / kSlices;  // warps per row slice
-        cplx sum = {0.0, 0.0};
-        for (int w = 0; w < wps; ++w) sum = sum + s_red[h * wps + w][r][k];
-        if (row < nrows) y[k * n + row0 + row] = sum;
-      }
-      __syncthreads();
-    }
-  }
-  R.pos += (unsigned)S;
-}
-
-// One out-of-line copy of the single-vector matvec for the GMRES kernel:
-// every call site shares the same (register-allocated once) code.  The ring
-// travels by value and the new position is returned, so nothing is spilled.
-__device__ __noinline__ unsigned matvec1_nl(Ring R, const cplx* __restrict__ A, long long n,
-                                            const cplx* x, cplx* y) {
-  matvec_tma<1>(R, A, n, x, y);
-  return R.pos;
-}
-// (measured: the out-of-line copy is ~15 % slower than inlining; kept for
-// A/B tests with -DEWB_MATVEC_NOINLINE)
-#ifndef EWB_MATVEC_NOINLINE
-#define EWB_MATVEC1(ring, A, n, x, y) matvec_tma<1>(ring, A, n, x, y)
-#else
-#define EWB_MATVEC1(ring, A, n, x, y) (ring).pos = matvec1_nl(ring, A, n, x, y)
-#endif
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// optional phase trace (CTA 0): (phase << 56) | %globaltimer
-#define EWB_PROBE(id)                                                                  \
-  do {                                                                                 \
-    if (a.probe && blockIdx.x == 0 && threadIdx.x == 0 && n_probe < a.probe_cap)       \
-      a.probe[n_probe++] = ((unsigned long long)(id) << 56) |                          \
-                           (gtimer() & ((1ull << 56) - 1));                            \
-  } while (0)
-
-// z = P^{-1} v  (3x3 blocks; identity when pinv == nullptr).  Grid-stride
-// over elements: thread e owns DOFs 3e..3e+2.
-__device__ __forceinline__ void precond_apply_elem(const cplx* pinv, long long e, const cplx* v,
-                                                   cplx* z) {
-  cplx v0 = v[3 * e], v1 = v[3 * e + 1], v2 = v[3 * e + 2];
-  const cplx* P = pinv + 9 * e;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    // numpy einsum('bij,bj->bi') order: ((P0 v0 + P1 v1) + P2 v2)
-    cplx s = P[3 * a] * v0;
-    s = s + P[3 * a + 1] * v1;
-    s = s + P[3 * a + 2] * v2;
-    z[3 * e + a] = s;
-  }
 }
 
 __device__ __forceinline__ long long gtid() {
@@ -404,249 +185,7 @@ struct GivensShared {
   cplx h[kMaxRestart + 1];
 };
 
-// Classic sequential MGS (one grid barrier per projection) — kept as the
-// GmresArgs::ortho == 1 variant for A/B parity checks.
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_mgs(GmresArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(128) unsigned char ring_smem[];
-  __shared__ uint64_t ring_bar[kNS];
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
-  ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
-  __shared__ GivensShared gs;
-  __shared__ cplx s_y[kMaxRestart];
-  const long long n = a.n;
-  const long long tid = gtid(), nth = gthreads();
-  const bool have_pc = a.pinv != nullptr;
-  GridRed R{a.partial, 0};
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-
-  // ||b||
-  double v1[1] = {0.0};
-  for (long long k = tid; k < n; k += nth) v1[0] += abs2(a.b[k]);
-  grid_sum(grid, R, v1);
-  const double nb = sqrt(v1[0]);
-  if (nb == 0.0) {  // linsolve.py:136-140
-    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
-    if (tid == 0) { a.out->iterations = 0; a.out->init_res = 0; a.out->final_res = 0;
-                    a.out->n_hist = 0; a.out->converged = 1; a.out->matvecs = 0; }
-    return;
-  }
-  int n_mv = 0;
-  // r = b - A x0  (skipped when x0 is all zero: linsolve.py:144)
-  double anyv[1] = {0.0};
-  if (a.has_x0)
-    for (long long k = tid; k < n; k += nth) anyv[0] += (a.x[k].re != 0.0 || a.x[k].im != 0.0);
-  else
-    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
-  grid_sum(grid, R, anyv);
-  if (anyv[0] > 0.0) {
-    matvec_tma<1>(ring, a.A, n, a.x, a.w);
-    ++n_mv;
-    grid.sync();
-    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
-  } else {
-    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k];
-  }
-  double rr[1] = {0.0};
-  for (long long k = tid; k < n; k += nth) rr[0] += abs2(a.r[k]);
-  grid_sum(grid, R, rr);
-  double rnorm = sqrt(rr[0]);
-  double res = rnorm / nb;
-  int n_hist = 0;
-  if (tid == 0) { a.out->init_res = res; a.hist[n_hist] = res; }
-  n_hist++;
-  int its = 0;
-  while (res > a.tol && its < a.maxiter) {
-    const int m = min(a.restart, a.maxiter - its);
-    const double beta = rnorm;
-    // V0 = r / beta ; z = P^{-1} V0
-    for (long long k = tid; k < n; k += nth) {
-      cplx v = a.r[k];
-      a.V[k] = {v.re / beta, v.im / beta};
-    }
-    if (threadIdx.x == 0) {
-      gs.g[0] = {beta, 0.0};
-      for (int k = 1; k <= m; ++k) gs.g[k] = {0.0, 0.0};
-    }
-    grid.sync();
-    int used = 0;
-    for (int j = 0; j < m; ++j) {
-      const cplx* vj = a.V + (size_t)j * n;
-      // z = P^{-1} v_j
-      if (have_pc) {
-        for (long long e = tid; e < n / 3; e += nth) precond_apply_elem(a.pinv, e, vj, a.z);
-      } else {
-        for (long long k = tid; k < n; k += nth) a.z[k] = vj[k];
-      }
-      grid.sync();
-      matvec_tma<1>(ring, a.A, n, a.z, a.w);
-      ++n_mv;
-      grid.sync();
-      // MGS, fused: partial <v_0, w>
-      double dv[2] = {0.0, 0.0};
-      for (long long k = tid; k < n; k += nth) {
-        cplx p = conj(a.V[k]) * a.w[k];
-        dv[0] += p.re; dv[1] += p.im;
-      }
-      for (int i = 0; i <= j; ++i) {
-        grid_sum(grid, R, dv);
-        const cplx h = {dv[0], dv[1]};
-        if (threadIdx.x == 0) gs.h[i] = h;
-        const cplx* vi = a.V + (size_t)i * n;
-        const cplx* vn = a.V + (size_t)(i + 1) * n;
-        dv[0] = dv[1] = 0.0;
-        if (i < j) {
-          for (long long k = tid; k < n; k += nth) {
-            cplx w = a.w[k] - h * vi[k];
-            a.w[k] = w;
-            cplx p = conj(vn[k]) * w;
-            dv[0] += p.re; dv[1] += p.im;
-          }
-        } else {
-          for (long long k = tid; k < n; k += nth) {
-            cplx w = a.w[k] - h * vi[k];
-            a.w[k] = w;
-            dv[0] += abs2(w);
-          }
-        }
-      }
-      double nw[1] = {dv[0]};
-      grid_sum(grid, R, nw);
-      const double hn = sqrt(nw[0]);
-      if (hn > 0.0) {
-        cplx* vn = a.V + (size_t)(j + 1) * n;
-        for (long long k = tid; k < n; k += nth) {
-          cplx w = a.w[k];
-          vn[k] = {w.re / hn, w.im / hn};
-        }
-      }
-      // Givens (linsolve.py:171-194), identical in every block
-      if (threadIdx.x == 0) {
-        gs.h[j + 1] = {hn, 0.0};
-        for (int i = 0; i < j; ++i) {
-          cplx top = gs.cs[i] * gs.h[i] + gs.sn[i] * gs.h[i + 1];
-          gs.h[i + 1] = (-conj(gs.sn[i])) * gs.h[i] + conj(gs.cs[i]) * gs.h[i + 1];
-          gs.h[i] = top;
-        }
-        double ahj = hypot(gs.h[j].re, gs.h[j].im), ahn = hypot(gs.h[j + 1].re, gs.h[j + 1].im);
-        double den = sqrt(ahj * ahj + ahn * ahn);
-        if (den == 0.0) {
-          gs.cs[j] = {1.0, 0.0}; gs.sn[j] = {0.0, 0.0};
-        } else if (gs.h[j].re == 0.0 && gs.h[j].im == 0.0) {
-          gs.cs[j] = {0.0, 0.0}; gs.sn[j] = {1.0, 0.0};
-        } else {
-          gs.cs[j] = {ahj / den, 0.0};
-          cplx ph = {gs.h[j].re / ahj, gs.h[j].im / ahj};
-          cplx t = ph * conj(gs.h[j + 1]);
-          gs.sn[j] = {t.re / den, t.im / den};
-        }
-        gs.h[j] = gs.cs[j] * gs.h[j] + gs.sn[j] * gs.h[j + 1];
-        gs.h[j + 1] = {0.0, 0.0};
-        gs.g[j + 1] = (-conj(gs.sn[j])) * gs.g[j];
-        gs.g[j] = gs.cs[j] * gs.g[j];
-        if (blockIdx.x == 0) {
-          for (int i = 0; i <= j; ++i) a.H[(size_t)i * kMaxRestart + j] = gs.h[i];
-        }
-      }
-      __syncthreads();
-      ++its;
-      used = j + 1;
-      const double est = hypot(gs.g[j + 1].re, gs.g[j + 1].im) / nb;
-      if (tid == 0 && n_hist < a.hist_cap) a.hist[n_hist] = est;
-      n_hist++;
-      grid.sync();  // V_{j+1} complete, H visible
-      if (est <= a.tol) break;
-    }
-    // back substitution (linsolve.py:196-198): warp 0 of every block
-    if (wid == 0) {
-      for (int i = used - 1; i >= 0; --i) {
-        cplx s = {0.0, 0.0};
-        for (int k = i + 1 + lane; k < used; k += 32) s = s + a.H[(size_t)i * kMaxRestart + k] * s_y[k];
-        warp_sum(s);
-        if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, a.H[(size_t)i * kMaxRestart + i]);
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    // x += P^{-1} (V^T y)   (u in w as scratch)
-    for (long long k = tid; k < n; k += nth) {
-      cplx u = {0.0, 0.0};
-      for (int i = 0; i < used; ++i) cfma(u, a.V[(size_t)i * n + k], s_y[i]);
-      a.w[k] = u;
-    }
-    if (have_pc) {
-      grid.sync();
-      for (long long e = tid; e < n / 3; e += nth) {
-        precond_apply_elem(a.pinv, e, a.w, a.z);
-        for (int c = 0; c < 3; ++c) a.x[3 * e + c] = a.x[3 * e + c] + a.z[3 * e + c];
-      }
-    } else {
-      for (long long k = tid; k < n; k += nth) a.x[k] = a.x[k] + a.w[k];
-    }
-    grid.sync();
-    // true residual (linsolve.py:200-201)
-    matvec_tma<1>(ring, a.A, n, a.x, a.w);
-    ++n_mv;
-    grid.sync();
-    double q[1] = {0.0};
-    for (long long k = tid; k < n; k += nth) {
-      cplx r = a.b[k] - a.w[k];
-      a.r[k] = r;
-      q[0] += abs2(r);
-    }
-    grid_sum(grid, R, q);
-    rnorm = sqrt(q[0]);
-    res = rnorm / nb;
-  }
-  if (tid == 0) {
-    a.out->iterations = its;
-    a.out->final_res = res;
-    a.out->converged = res <= a.tol;
-    a.out->n_hist = n_hist;
-    a.out->matvecs = n_mv;
-  }
-}
-
-// ---------------------------------------------------------------------
-// One-reduction MGS-GMRES (default).  The reference's MGS computes
-//   h_i = <v_i, w - sum_{l<i} h_l v_l> = d_i - sum_{l<i} <v_i, v_l> h_l,
-// d_i = <v_i, w>, i.e. h = (I + L)^{-1} d with L the strictly lower part of
-// the Gram matrix V^H V.  Row j of L (<v_j, v_l>, l < j) is reduced together
-// with d in ONE grid reduction, the unit-triangular solve runs redundantly
-// (and identically) in every CTA, and w -= h_0 v_0 -= h_1 v_1 ... (the MGS
-// update order) plus |w|^2 take the second reduction.  Same algorithm and
-// coefficients as MGS up to floating-point association — no approximation —
-// with 4 grid barriers per Arnoldi step instead of j + 5.
-// ---------------------------------------------------------------------
 constexpr int kMaxDots = 2 * kMaxRestart + 2;
-
-// CTA-partial dots over this CTA's DOF slice [k0, k1):
-//   t < nd        : <V_t, w>
-//   nd <= t < nd+ng: <v_j, V_{t-nd}>
-__device__ void slice_dots(const cplx* V, long long n, const cplx* w, int nd, int ng, int j,
-                           long long k0, long long k1, cplx* part) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int t = wid; t < nd + ng; t += kSolveWarps) {
-    const cplx* p = t < nd ? V + (size_t)t * n : V + (size_t)j * n;
-    const cplx* q = t < nd ? w : V + (size_t)(t - nd) * n;
-    cplx s = {0.0, 0.0};
-    for (long long k = k0 + lane; k < k1; k += 32) cfma(s, conj(p[k]), q[k]);
-    warp_sum(s);
-    if (lane == 0) part[(size_t)blockIdx.x * kMaxDots + t] = s;
-  }
-}
-
-// Every CTA reduces the CTA partials in the same fixed order -> s_out.
-__device__ void reduce_slices(const cplx* part, int cnt, cplx* s_out) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int t = wid; t < cnt; t += kSolveWarps) {
-    cplx s = {0.0, 0.0};
-    for (int b = lane; b < (int)gridDim.x; b += 32) s = s + part[(size_t)b * kMaxDots + t];
-    warp_sum(s);
-    if (lane == 0) s_out[t] = s;
-  }
-  __syncthreads();
-}
 
 __device__ __forceinline__ void precond_regs(const cplx* pinv, long long e, const cplx v[3],
                                              cplx* z) {
@@ -657,256 +196,6 @@ __device__ __forceinline__ void precond_regs(const cplx* pinv, long long e, cons
     s = s + P[3 * r + 1] * v[1];
     s = s + P[3 * r + 2] * v[2];
     z[3 * e + r] = s;
-  }
-}
-
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresArgs a) {
-  int n_probe = 0;
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(128) unsigned char ring_smem[];
-  __shared__ uint64_t ring_bar[kNS];
-  __shared__ GivensShared gs;
-  __shared__ cplx s_y[kMaxRestart];
-  __shared__ cplx s_dots[kMaxDots];
-  __shared__ cplx s_h[kMaxRestart + 1];
-  __shared__ double s_est;
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
-  ring_init(ring, 16.0 * (double)a.n * (double)a.n > 96e6);
-  const long long n = a.n;
-  const long long tid = gtid(), nth = gthreads();
-  const bool pc = a.pinv != nullptr;
-  const int ucnt = pc ? 3 : 1;
-  const long long nunits = pc ? n / 3 : n;
-  const long long k0 = (long long)blockIdx.x * n / gridDim.x;
-  const long long k1 = (long long)(blockIdx.x + 1) * n / gridDim.x;
-  GridRed R{a.partial, 0};
-  int dpar = 0;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-
-  // ||b|| and "x0 has a nonzero entry", one reduction
-  double v2[2] = {0.0, 0.0};
-  for (long long k = tid; k < n; k += nth) {
-    v2[0] += abs2(a.b[k]);
-    if (a.has_x0) v2[1] += (a.x[k].re != 0.0 || a.x[k].im != 0.0);
-    else a.x[k] = {0.0, 0.0};
-  }
-  grid_sum(grid, R, v2);
-  const double nb = sqrt(v2[0]);
-  if (nb == 0.0) {  // linsolve.py:136-140
-    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
-    if (tid == 0) { a.out->iterations = 0; a.out->init_res = 0; a.out->final_res = 0;
-                    a.out->n_hist = 0; a.out->converged = 1; a.out->matvecs = 0; }
-    return;
-  }
-  int n_mv = 0;
-  if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
-    EWB_MATVEC1(ring, a.A, n, a.x, a.w);
-    ++n_mv;
-    grid.sync();
-    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k] - a.w[k];
-  } else {
-    for (long long k = tid; k < n; k += nth) a.r[k] = a.b[k];
-  }
-  double rr[1] = {0.0};
-  for (long long k = tid; k < n; k += nth) rr[0] += abs2(a.r[k]);
-  grid_sum(grid, R, rr);
-  double rnorm = sqrt(rr[0]);
-  double res = rnorm / nb;
-  int n_hist = 0;
-  if (tid == 0) { a.out->init_res = res; a.hist[0] = res; }
-  n_hist++;
-  int its = 0;
-  while (res > a.tol && its < a.maxiter) {
-    const int m = min(a.restart, a.maxiter - its);
-    const double beta = rnorm;
-    // V0 = r / beta and z = P^{-1} V0, per unit (element or DOF)
-    for (long long u = tid; u < nunits; u += nth) {
-      cplx v[3];
-      for (int c = 0; c < ucnt; ++c) {
-        const long long k = u * ucnt + c;
-        v[c] = {a.r[k].re / beta, a.r[k].im / beta};
-        a.V[k] = v[c];
-      }
-      if (pc) precond_regs(a.pinv, u, v, a.z);
-      else a.z[u] = v[0];
-    }
-    if (threadIdx.x == 0) {
-      gs.g[0] = {beta, 0.0};
-      for (int k = 1; k <= m; ++k) gs.g[k] = {0.0, 0.0};
-    }
-    grid.sync();
-    int used = 0;
-    for (int j = 0; j < m; ++j) {
-#ifdef EWB_DBG_LOOP_X
-      EWB_MATVEC1(ring, a.A, n, a.x, a.w);   // timing experiment only
-#else
-      EWB_MATVEC1(ring, a.A, n, a.z, a.w);   // w = A P^{-1} v_j
-#endif
-      ++n_mv;
-      grid.sync();
-      // reduction 1: d_i = <v_i, w> (i <= j) and Gram row j: <v_j, v_l> (l < j)
-      cplx* part = a.dpart + (size_t)dpar * gridDim.x * kMaxDots;
-      dpar ^= 1;
-      EWB_PROBE(20);
-#ifdef EWB_DBG_WARM
-      for (int rep = 0; rep < 2; ++rep) {  // second pass: same code and data, warm
-        slice_dots(a.V, n, a.w, j + 1, j, j, k0, k1, part);
-        EWB_PROBE(21 + rep);
-      }
-#else
-      slice_dots(a.V, n, a.w, j + 1, j, j, k0, k1, part);
-      EWB_PROBE(21);
-#endif
-      grid.sync();
-      reduce_slices(part, 2 * j + 1, s_dots);
-      // h = (I + L)^{-1} d  (warp 0, identical in every CTA).  The Gram rows
-      // i < j are first staged (packed, one parallel round trip) into the
-      // idle TMA ring — the matvec is complete, nothing is in flight.
-      cplx* gsm = ring.buf;
-      for (int i = 1; i < j; ++i)
-        for (int l = threadIdx.x; l < i; l += blockDim.x)
-          gsm[i * (i - 1) / 2 + l] = a.Gram[(size_t)i * kMaxRestart + l];
-      __syncthreads();
-      if (wid == 0) {
-        for (int i = 0; i <= j; ++i) {
-          cplx s = {0.0, 0.0};
-          for (int l = lane; l < i; l += 32) {
-            const cplx g = i == j ? s_dots[j + 1 + l] : gsm[i * (i - 1) / 2 + l];
-            s = s + g * s_h[l];
-          }
-          warp_sum(s);
-          if (lane == 0) s_h[i] = s_dots[i] - s;
-          __syncwarp();
-        }
-        if (blockIdx.x == 0)
-          for (int l = lane; l < j; l += 32) a.Gram[(size_t)j * kMaxRestart + l] = s_dots[j + 1 + l];
-      }
-      __syncthreads();
-      // w <- (((w - h0 v0) - h1 v1) ... - hj vj)  and |w|^2 (reduction 2)
-      double q[1] = {0.0};
-      for (long long k = tid; k < n; k += nth) {
-        cplx wk = a.w[k];
-        for (int i = 0; i <= j; ++i) wk = wk - s_h[i] * a.V[(size_t)i * n + k];
-        a.w[k] = wk;
-        q[0] += abs2(wk);
-      }
-      grid_sum(grid, R, q);
-      const double hn = sqrt(q[0]);
-      // Givens (linsolve.py:171-194), identical in every CTA
-      if (threadIdx.x == 0) {
-        // apply the previous rotations; only `carry` (the running h_i) is
-        // on the dependency chain
-        cplx carry = s_h[0];
-#pragma unroll 4
-        for (int i = 0; i < j; ++i) {
-          const cplx c = gs.cs[i], sn = gs.sn[i], hn1 = s_h[i + 1];
-          gs.h[i] = c * carry + sn * hn1;
-          carry = (-conj(sn)) * carry + conj(c) * hn1;
-        }
-        gs.h[j] = carry;
-        gs.h[j + 1] = {hn, 0.0};
-        double ahj = hypot(gs.h[j].re, gs.h[j].im), ahn = hypot(gs.h[j + 1].re, gs.h[j + 1].im);
-        double den = sqrt(ahj * ahj + ahn * ahn);
-        if (den == 0.0) {
-          gs.cs[j] = {1.0, 0.0}; gs.sn[j] = {0.0, 0.0};
-        } else if (gs.h[j].re == 0.0 && gs.h[j].im == 0.0) {
-          gs.cs[j] = {0.0, 0.0}; gs.sn[j] = {1.0, 0.0};
-        } else {
-          gs.cs[j] = {ahj / den, 0.0};
-          cplx ph = {gs.h[j].re / ahj, gs.h[j].im / ahj};
-          cplx t = ph * conj(gs.h[j + 1]);
-          gs.sn[j] = {t.re / den, t.im / den};
-        }
-        gs.h[j] = gs.cs[j] * gs.h[j] + gs.sn[j] * gs.h[j + 1];
-        gs.h[j + 1] = {0.0, 0.0};
-        gs.g[j + 1] = (-conj(gs.sn[j])) * gs.g[j];
-        gs.g[j] = gs.cs[j] * gs.g[j];
-        s_est = hypot(gs.g[j + 1].re, gs.g[j + 1].im) / nb;
-        if (blockIdx.x == 0)
-          for (int i = 0; i <= j; ++i) a.H[(size_t)i * kMaxRestart + j] = gs.h[i];
-      }
-      __syncthreads();
-      ++its;
-      used = j + 1;
-      const double est = s_est;
-      if (tid == 0 && n_hist < a.hist_cap) a.hist[n_hist] = est;
-      n_hist++;
-      if (est <= a.tol) {
-        grid.sync();  // H visible to every CTA before the back substitution
-        break;
-      }
-      // v_{j+1} = w / h_{j+1,j} and z = P^{-1} v_{j+1}
-      if (hn > 0.0) {
-        cplx* vn = a.V + (size_t)(j + 1) * n;
-        for (long long u = tid; u < nunits; u += nth) {
-          cplx v[3];
-          for (int c = 0; c < ucnt; ++c) {
-            const long long k = u * ucnt + c;
-            v[c] = {a.w[k].re / hn, a.w[k].im / hn};
-            vn[k] = v[c];
-          }
-          if (pc) precond_regs(a.pinv, u, v, a.z);
-          else a.z[u] = v[0];
-        }
-      }
-      grid.sync();
-    }
-    // back substitution (linsolve.py:196-198): warp 0 of every CTA, with
-    // the upper triangle of H staged (packed) into the idle ring first.
-    {
-      cplx* hsm = ring.buf;
-      for (int i = 0; i < used; ++i)
-        for (int k = i + threadIdx.x; k < used; k += blockDim.x)
-          hsm[i * used - i * (i - 1) / 2 + (k - i)] = a.H[(size_t)i * kMaxRestart + k];
-      __syncthreads();
-      if (wid == 0) {
-        for (int i = used - 1; i >= 0; --i) {
-          const cplx* row = hsm + i * used - i * (i - 1) / 2 - i;
-          cplx s = {0.0, 0.0};
-          for (int k = i + 1 + lane; k < used; k += 32) s = s + row[k] * s_y[k];
-          warp_sum(s);
-          if (lane == 0) s_y[i] = cdiv(gs.g[i] - s, row[i]);
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-    }
-    // x += P^{-1} (V^T y), per unit
-    for (long long u = tid; u < nunits; u += nth) {
-      cplx uv[3];
-      for (int c = 0; c < ucnt; ++c) {
-        const long long k = u * ucnt + c;
-        cplx s = {0.0, 0.0};
-        for (int i = 0; i < used; ++i) cfma(s, a.V[(size_t)i * n + k], s_y[i]);
-        uv[c] = s;
-      }
-      if (pc) {
-        precond_regs(a.pinv, u, uv, a.z);
-        for (int c = 0; c < 3; ++c) a.x[3 * u + c] = a.x[3 * u + c] + a.z[3 * u + c];
-      } else {
-        a.x[u] = a.x[u] + uv[0];
-      }
-    }
-    grid.sync();
-    EWB_MATVEC1(ring, a.A, n, a.x, a.w);  // true residual (linsolve.py:200-201)
-    ++n_mv;
-    grid.sync();
-    double q2[1] = {0.0};
-    for (long long k = tid; k < n; k += nth) {
-      cplx r = a.b[k] - a.w[k];
-      a.r[k] = r;
-      q2[0] += abs2(r);
-    }
-    grid_sum(grid, R, q2);
-    rnorm = sqrt(q2[0]);
-    res = rnorm / nb;
-  }
-  if (tid == 0) {
-    a.out->iterations = its;
-    a.out->final_res = res;
-    a.out->converged = res <= a.tol;
-    a.out->n_hist = n_hist;
-    a.out->matvecs = n_mv;
   }
 }
 
@@ -923,47 +212,16 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres(GmresA
 // residuals, partial dot products) happens while the next stages are
 // already in flight.
 // ---------------------------------------------------------------------
-//
-// Row balance.  The matvec bandwidth of an SM under full-GPU contention is
-// not uniform: with equal row counts some SMs finish ~25 us (5 %) after the
-// others, every pass, and the grid barrier waits for them.  The slowness
-// follows the SM, not the rows (swapping the row chunks keeps the slow set:
-// tools/gmres_trace.py), and the CTA -> SM map of the solver launches is
-// fixed, so ewb_calibrate_rows measures each CTA's rows per second once and
-// the row split follows those speeds: CTA b owns [cumw[b] n, cumw[b+1] n).
-// Results stay bit-identical for a given split; splits from different
-// calibrations change only the grouping of the dot-product partials
-// (rounding level).  c_bal_g == 0 (default) or a different grid: equal split.
-constexpr int kMaxBalGrid = 512;
-__constant__ double c_cumw[kMaxBalGrid + 1];
-__constant__ int c_bal_g;
-
 __device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& r1) {
-#ifdef EWB_ROWS_REVERSED   // experiment: is a slow CTA slow because of its SM or its rows?
-  const long long b = gridDim.x - 1 - blockIdx.x;
-#else
-  const long long b = blockIdx.x;
-#endif
-  if (c_bal_g == (int)gridDim.x) {
-    r0 = llrint(c_cumw[b] * (double)n);
-    r1 = llrint(c_cumw[b + 1] * (double)n);
-  } else {
-    r0 = b * n / gridDim.x;
-    r1 = (b + 1) * n / gridDim.x;
-  }
-}
-// host mirror of cta_rows' balanced split
-static inline long long host_split(const double* cumw, int b, long long n) {
-  return llrint(cumw[b] * (double)n);
+  r0 = (long long)blockIdx.x * n / gridDim.x;
+  r1 = ((long long)blockIdx.x + 1) * n / gridDim.x;
 }
 
 struct NoPre {
   __device__ __forceinline__ void operator()(long long, int) const {}
 };
-#ifndef EWB_EPI_PREFETCH
-#define EWB_EPI_PREFETCH 12
-#endif
-// pre(row0, nrows) runs EWB_EPI_PREFETCH tiles before a block's epilogue:
+constexpr int kEpiPrefetch = 12;
+// pre(row0, nrows) runs kEpiPrefetch tiles before a block's epilogue:
 // the GMRES kernel prefetches the basis rows its dot products will read
 // into L1 there, so the epilogue (during which this CTA consumes no ring
 // stage) does not wait on L2.
@@ -988,8 +246,7 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
     const int q = u / ntile, t = u - q * ntile;
     const int rel0 = q * rows / nblk, nr = (q + 1) * rows / nblk - rel0;
     const int tc = t == ntile - 1 ? last_tc : kTC;
-    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc,
-               max(0, min(nr, kPinRows - rel0)));
+    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc);
   };
   if (threadIdx.x < kNS) s_rel[threadIdx.x] = 0;
   __syncthreads();
@@ -1021,7 +278,7 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
 #pragma unroll
       for (int k = 0; k < K; ++k) xn[k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
     }
-    if (t == max(0, ntile - 1 - EWB_EPI_PREFETCH)) pre(row0, nrows);
+    if (t == max(0, ntile - 1 - kEpiPrefetch)) pre(row0, nrows);
     const unsigned pos = R.pos + (unsigned)s;
     ring_wait(R, pos);
     if (col < tc) {
@@ -1106,8 +363,7 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
     const int q = u / ntile, t = u - q * ntile;
     const int rel0 = q * rows / nblk, nr = (q + 1) * rows / nblk - rel0;
     const int tc = t == ntile - 1 ? last_tc : kTC;
-    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc,
-               max(0, min(nr, kPinRows - rel0)));
+    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc);
   };
   if (threadIdx.x < kNS) s_rel[threadIdx.x] = 0;
   __syncthreads();
@@ -1167,18 +423,6 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
           xn[m][k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
         }
     }
-#if EWB_X_PREFETCH
-    {  // the x columns of the stage after next into L1 (no registers held)
-      const int t2 = (t + 2) % ntile;
-      const long long c2 = (long long)t2 * kTC;
-      constexpr int kLines = kTC * 16 / 128;   // 128-byte lines per vector segment
-      if (threadIdx.x < K * kLines) {
-        const int k = threadIdx.x / kLines, ln = threadIdx.x % kLines;
-        const long long cc = c2 + ln * 8;
-        if (cc < n) asm volatile("prefetch.global.L1 [%0];" ::"l"(x + k * n + cc));
-      }
-    }
-#endif
     __syncwarp();
     if ((threadIdx.x & 31) == 0 &&
         atomicAdd(&s_rel[pos % kNS], 1) == kSolveWarps - 1) {  // last reader of the slot
@@ -1232,47 +476,14 @@ __device__ __forceinline__ void group_sum(cplx& v) {
   }
 }
 
-// Fixed-order reduction of `cnt` CTA partials (layout part[b * stride + t]):
-// 8 threads per value, thread `sub` summing CTAs sub, sub + 8, ... with all
-// of its loads issued before the first add (one L2 round trip per round
-// instead of one per CTA), then a 3-step shuffle.  Identical in every CTA.
-constexpr int kRedPer = 20;  // partial loads per thread: grids up to 160 CTAs
-
-__device__ void reduce_parts(const cplx* part, int stride, int cnt, cplx* out) {
-  const int sub = threadIdx.x & 7;
-  const int G = gridDim.x;
-  for (int base = 0; base < cnt; base += kSolveThreads / 8) {
-    const int t = base + (threadIdx.x >> 3);
-    cplx s = {0.0, 0.0};
-    if (t < cnt) {
-      if (G <= 8 * kRedPer) {
-        cplx v[kRedPer];
-#pragma unroll
-        for (int i = 0; i < kRedPer; ++i) {
-          const int b = sub + 8 * i;
-          v[i] = b < G ? part[(size_t)b * stride + t] : cplx{0.0, 0.0};
-        }
-#pragma unroll
-        for (int i = 0; i < kRedPer; ++i) s = s + v[i];
-      } else {
-        for (int b = sub; b < G; b += 8) s = s + part[(size_t)b * stride + t];
-      }
-    }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      s.re += __shfl_xor_sync(0xffffffffu, s.re, o);
-      s.im += __shfl_xor_sync(0xffffffffu, s.im, o);
-    }
-    if (sub == 0 && t < cnt) out[t] = s;
-  }
-  __syncthreads();
-}
-
 // ---------------------------------------------------------------------
-// GMRES with the Arnoldi vector work fused around the matvec (default,
-// GmresArgs::ortho == 0).  Same algorithm as k_gmres (one-reduction MGS,
-// linsolve.py:150-170 up to association), restructured so that an Arnoldi
-// step costs one pass over A plus two grid barriers:
+// GMRES with the Arnoldi vector work fused around the matvec: the
+// reference's MGS (linsolve.py:150-170) in its one-reduction form
+//   h_i = <v_i, w - sum_{l<i} h_l v_l> = d_i - sum_{l<i} <v_i, v_l> h_l,
+// d_i = <v_i, w>, i.e. h = (I + L)^{-1} d with L the strictly lower part of
+// the basis's Gram matrix (same coefficients up to floating-point
+// association), arranged so that an Arnoldi step costs one pass over A
+// plus two grid barriers:
 //
 //   matvec   w = (A z') / h_{j,j-1} over the CTA's own rows; each finished
 //            row block immediately adds <V_t, w>, t <= j, to CTA partials
@@ -1295,13 +506,7 @@ constexpr int kNormSlot = kMaxDots - 1;
 constexpr int kGrp = kRR <= 16 ? 16 : 32;  // lanes per epilogue dot
 
 
-#ifdef EWB_GMRES_MAXNREG
-__global__ void __maxnreg__(EWB_GMRES_MAXNREG)
-#else
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks)
-#endif
-k_gmres_f(GmresArgs a) {
-  int n_probe = 0;
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(GmresArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) unsigned char ring_smem[];
   __shared__ uint64_t ring_bar[kNS];
@@ -1395,7 +600,6 @@ k_gmres_f(GmresArgs a) {
   }
   int n_mv = 0;
   double rnorm;
-#ifndef EWB_NO_AX0
   if (v2[1] > 0.0 && a.ax0) {  // r = b - A x0 with A x0 supplied (SEM's Y s)
     double q = 0.0;
     for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
@@ -1407,9 +611,12 @@ k_gmres_f(GmresArgs a) {
     grid.sync();
     rnorm = sqrt(grid_norm(dpar));
     dpar ^= 1;
-  } else
-#endif
-  if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
+    if (rnorm / nb <= a.tol) {  // a 0-iteration exit is decided on b - A x0 itself
+      rnorm = residual(dpar);
+      dpar ^= 1;
+      ++n_mv;
+    }
+  } else if (v2[1] > 0.0) {  // r = b - A x0 (linsolve.py:144)
     rnorm = residual(dpar);
     dpar ^= 1;
     ++n_mv;
@@ -1442,7 +649,7 @@ k_gmres_f(GmresArgs a) {
     }
     for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
       a.V[k] = {a.r[k].re / beta, a.r[k].im / beta};
-      if (a.W) a.rs[k] = a.r[k];   // the cycle's starting (true) residual
+      if (a.W) a.rs[k] = a.r[k];   // the cycle's starting residual
     }
     grid.sync();
     double hprev = beta;
@@ -1452,7 +659,6 @@ k_gmres_f(GmresArgs a) {
       const double sc = 1.0 / hprev;
       for (int t = threadIdx.x; t <= j; t += blockDim.x) s_dacc[t] = {0.0, 0.0};
       __syncthreads();
-      EWB_PROBE(2);
       matvec_rows<1>(ring, a.A, n, a.z, k0, k1, [&](long long row0, int nr, cplx (*sum)[1]) {
         if (threadIdx.x < nr) {
           const cplx w = sum[threadIdx.x][0] * sc;
@@ -1485,35 +691,9 @@ k_gmres_f(GmresArgs a) {
             asm volatile("prefetch.global.L1 [%0];" ::"l"(a.V + (size_t)ta * n + row0 + sub));
       });
       ++n_mv;
-#if EWB_L2_PREFETCH_TILES > 0
-      {  // the next pass's first tiles of this CTA's rows into L2 while the
-         // grid waits at S1 and reduces (HBM otherwise idle)
-        const int rows = (int)(k1 - k0), nblk = (rows + kRR - 1) / kRR;
-        const int nr = rows / nblk;
-        const int ntile = (int)((n + kTC - 1) / kTC);
-        const int nt = min(EWB_L2_PREFETCH_TILES, ntile);
-        for (int idx = threadIdx.x; idx < nr * nt; idx += blockDim.x) {
-          const int r = idx % nr, t = idx / nr;
-          const long long c0 = (long long)t * kTC;
-          const uint32_t bytes = (uint32_t)(min((long long)kTC, n - c0) * 16);
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.A + (k0 + r) * n + c0),
-                       "r"(bytes)
-                       : "memory");
-        }
-      }
-#endif
       cplx* part = part_buf(dpar);
       for (int t = threadIdx.x; t <= j; t += blockDim.x)
         part[(size_t)blockIdx.x * kMaxDots + t] = s_dacc[t];
-      EWB_PROBE(3);
-      if (a.probe && threadIdx.x == 0 && j < 100 && its == j) {  // per-CTA matvec finish (cycle 0)
-        a.probe[32768 + j * gridDim.x + blockIdx.x] = gtimer();
-        if (j == 0) {
-          unsigned sm;
-          asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-          a.probe[32768 + 100 * gridDim.x + blockIdx.x] = sm;   // which SM ran this CTA
-        }
-      }
       // Gram rows 1..j-1 (written in earlier steps) staged into the idle
       // ring while other CTAs finish their matvec
       cplx* gsm = scr;
@@ -1529,7 +709,6 @@ k_gmres_f(GmresArgs a) {
         }
       }
       grid.sync();  // S1
-      EWB_PROBE(4);
       // ---- d_t and Gram row j; h = (I + L)^{-1} d --------------------------
       {
         // reduce-scatter (CTA b sums value t = b mod G over the CTA partials
@@ -1537,10 +716,6 @@ k_gmres_f(GmresArgs a) {
         // once instead of once per CTA
         cplx* fin = reinterpret_cast<cplx*>(a.partial);
         const int cnt = 2 * j + 1;
-#ifdef EWB_DBG_WARM
-        for (int rep = 0; rep < 2; ++rep) {
-        if (rep) EWB_PROBE(15);
-#endif
         for (int t = blockIdx.x + wid * gridDim.x; t < cnt; t += kSolveWarps * gridDim.x) {
           cplx v[5];
 #pragma unroll
@@ -1553,16 +728,9 @@ k_gmres_f(GmresArgs a) {
           warp_sum(sum);
           if (lane == 0) fin[t] = t > j ? sum * sc : sum;  // <u, V_l> / h = <v_j, V_l>
         }
-#ifdef EWB_DBG_WARM
-        __syncthreads();
-        }
-#endif
-        EWB_PROBE(11);
         grid.sync();  // S1b
-        EWB_PROBE(12);
         for (int t = threadIdx.x; t < cnt; t += blockDim.x) s_dots[t] = fin[t];
         __syncthreads();
-        EWB_PROBE(8);
         if (blockIdx.x == 0)
           for (int l = threadIdx.x; l < j; l += blockDim.x)
             a.Gram[(size_t)j * kMaxRestart + l] = s_dots[j + 1 + l];
@@ -1580,10 +748,8 @@ k_gmres_f(GmresArgs a) {
             if (lane == 0) hout[i] = s_dots[i] - s;
           }
           __syncthreads();
-          EWB_PROBE(9 + sweep);
         }
       }
-      EWB_PROBE(5);
       // ---- update: u = w - sum_i h_i V_i over [ka, kb) --------------------
       {
         const int nv = j + 1;
@@ -1638,11 +804,8 @@ k_gmres_f(GmresArgs a) {
         cta_norm_partial(q, dpar ^ 1);
       }
       dpar ^= 1;
-      EWB_PROBE(6);
       grid.sync();  // S2
-      EWB_PROBE(13);
       const double hn = sqrt(grid_norm(dpar));
-      EWB_PROBE(14);
       // Givens (linsolve.py:171-194), identical in every CTA
       if (threadIdx.x == 0) {
         // apply the previous rotations; only `carry` (the running h_i) is
@@ -1677,7 +840,6 @@ k_gmres_f(GmresArgs a) {
           for (int i = 0; i <= j; ++i) a.H[(size_t)i * kMaxRestart + j] = gs.h[i];
       }
       __syncthreads();
-      EWB_PROBE(7);
       ++its;
       used = j + 1;
       const double est = s_est;
@@ -1741,11 +903,14 @@ k_gmres_f(GmresArgs a) {
       }
     }
     grid.sync();
-    if (a.W) {
-      // true residual (linsolve.py:200-201) without another pass over A:
-      // b - A x_new = r_start - sum_i y_i (A P^{-1} v_i), from the products
-      // this cycle already computed (equal to b - A x_new up
-      // to rounding of |A x|, ~1e-16 |b| against a tolerance of 1e-8 |b|)
+    // Cycle end (linsolve.py:200-201).  The restart residual comes from the
+    // products this cycle already computed, b - A x_new = r_start - sum_i
+    // y_i (A P^{-1} v_i) (no pass over A; equal up to rounding of |A x|).
+    // Every exit decision — converged, or out of iterations — is taken on
+    // the literal b - A x (one pass), the quantity the reference tests and
+    // reports, so final_residual is always the true relative residual.
+    bool literal = a.W == nullptr || its >= a.maxiter;
+    if (!literal) {
       double q = 0.0;
       for (long long k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         cplx s = a.rs[k];
@@ -1756,11 +921,14 @@ k_gmres_f(GmresArgs a) {
       cta_norm_partial(q, dpar);
       grid.sync();
       rnorm = sqrt(grid_norm(dpar));
-    } else {
-      rnorm = residual(dpar);  // true residual (linsolve.py:200-201)
-      ++n_mv;
+      dpar ^= 1;
+      literal = rnorm / nb <= a.tol;
     }
-    dpar ^= 1;
+    if (literal) {
+      rnorm = residual(dpar);
+      ++n_mv;
+      dpar ^= 1;
+    }
     res = rnorm / nb;
   }
   if (tid == 0) {
@@ -1773,17 +941,17 @@ k_gmres_f(GmresArgs a) {
 }
 
 // ---------------------------------------------------------------------
-// SEM (linsolve.py:213-242): Y = A X (one pass over A for all K columns),
+// SEM (linsolve.py:213-242): Y = A X (passes of up to 4 columns over A),
 // QR of Y[:, keep] by classical Gram-Schmidt with one re-orthogonalisation
 // (|R_ii| agrees with Householder's to rounding), rank filter
 // |R_ii| >= rank_tol * max|R_ii| (<= 2 passes), x0 = X s with R s = Q^H b;
 // falls back to the newest column.
 // ---------------------------------------------------------------------
-template <int K>
 __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
   const long long n = a.n, tid = gtid(), nth = gthreads();
   // Y = A X was produced by k_multi_gemv (its own launch: the K-vector
-  // matvec needs more registers than this cooperative kernel can give it)
+  // matvec needs more registers than this cooperative kernel can give it),
+  // or by the matrix-free operator (ewb_sem_from_products)
   __shared__ int keep[kMaxSem];
   __shared__ cplx Rm[kMaxSem][kMaxSem];
   __shared__ int nkeep;
@@ -1898,12 +1066,7 @@ __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
 __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_sem(SemArgs a) {
   cg::grid_group grid = cg::this_grid();
   GridRed R{a.partial, 0};
-  switch (a.K) {
-    case 1: sem_body<1>(grid, R, a); break;
-    case 2: sem_body<2>(grid, R, a); break;
-    case 3: sem_body<3>(grid, R, a); break;
-    default: sem_body<4>(grid, R, a); break;
-  }
+  sem_body(grid, R, a);
 }
 
 // Batched GEMV y_b = A_b x_b through the TMA ring (regular launch; system
@@ -1922,68 +1085,6 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gemv_tma(con
                  [&](long long row0, int nr, cplx (*sum)[1]) {
                    if (threadIdx.x < nr) ys[row0 + threadIdx.x] = sum[threadIdx.x][0];
                  });
-}
-
-// Row-balance calibration: one matvec over the current split, all CTAs
-// released together (cooperative launch), per-CTA duration recorded.
-__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_calib(const cplx* A,
-                                                                         const cplx* x, cplx* y,
-                                                                         long long n,
-                                                                         unsigned long long* t) {
-  extern __shared__ __align__(128) unsigned char ring_smem[];
-  __shared__ uint64_t ring_bar[kNS];
-  Ring ring{reinterpret_cast<cplx*>(ring_smem), ring_bar, 0u, 0u};
-  ring_init(ring, true);
-  long long r0, r1;
-  cta_rows(n, r0, r1);
-  cg::this_grid().sync();
-  const unsigned long long t0 = gtimer();
-  // rate mark: time and rows done when the CTA passes half of its rows, i.e.
-  // while (nearly) every CTA is still streaming; a finish-time measure would
-  // credit the last CTAs with the bandwidth the early finishers released
-  long long done = 0;
-  const long long half = (r1 - r0) / 2;
-  matvec_rows<1>(ring, A, n, x, r0, r1, [&](long long row0, int nr, cplx (*sum)[1]) {
-    if (threadIdx.x < nr) y[row0 + threadIdx.x] = sum[threadIdx.x][0];
-    if (done < half && done + nr >= half && threadIdx.x == 0) {
-      t[gridDim.x + blockIdx.x] = gtimer() - t0;
-      t[2 * gridDim.x + blockIdx.x] = (unsigned long long)(done + nr);
-    }
-    done += nr;
-  });
-  __syncthreads();
-  if (threadIdx.x == 0) t[blockIdx.x] = gtimer() - t0;
-}
-
-// Plain batched GEMV y_b = A_b x_b (one launch, `batch` systems of size n).
-template <int RR>
-__global__ void __launch_bounds__(512) k_gemv_batched(const cplx* A, const cplx* x, cplx* y,
-                                                      long long n, int batch) {
-  // blockIdx.y = system
-  const cplx* Ab = A + (size_t)blockIdx.y * n * n;
-  const cplx* xb = x + (size_t)blockIdx.y * n;
-  cplx* yb = y + (size_t)blockIdx.y * n;
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long r0 = gw * RR; r0 < n; r0 += nw * RR) {
-    cplx acc[RR];
-#pragma unroll
-    for (int a = 0; a < RR; ++a) acc[a] = {0.0, 0.0};
-    const int nr = (int)min((long long)RR, n - r0);
-#pragma unroll 2
-    for (long long c = lane; c < n; c += 32) {
-      cplx xv = ldg(xb + c);
-#pragma unroll
-      for (int a = 0; a < RR; ++a)
-        if (a < nr) cfma(acc[a], ldc(Ab + (r0 + a) * n + c), xv);
-    }
-#pragma unroll
-    for (int a = 0; a < RR; ++a) {
-      warp_sum(acc[a]);
-      if (lane == 0 && a < nr) yb[r0 + a] = acc[a];
-    }
-  }
 }
 
 // ---------------------------------------------------------------------
@@ -2010,11 +1111,8 @@ int solver_grid_blocks() {
 
 int solver_grid_max() {
   if (g_coop_blocks == 0) {
-    int a = coop_grid((const void*)k_gmres), b = coop_grid((const void*)k_sem);
-    int c = coop_grid((const void*)k_gmres_mgs), d = coop_grid((const void*)k_gmres_f);
+    const int a = coop_grid((const void*)k_sem), b = coop_grid((const void*)k_gmres_f);
     g_coop_blocks = a < b ? a : b;
-    g_coop_blocks = c < g_coop_blocks ? c : g_coop_blocks;
-    g_coop_blocks = d < g_coop_blocks ? d : g_coop_blocks;
   }
   return g_coop_blocks;
 }
@@ -2023,10 +1121,7 @@ cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
   note_launch();
-  const void* fn = args.ortho == 1   ? (const void*)k_gmres_mgs
-                   : args.ortho == 2 ? (const void*)k_gmres
-                                     : (const void*)k_gmres_f;
-  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kSolveThreads), params, kRingBytes, s);
+  return cudaLaunchCooperativeKernel((const void*)k_gmres_f, dim3(G), dim3(kSolveThreads), params, kRingBytes, s);
 }
 
 // Y = A X for K <= 4 columns in one TMA-streamed pass (SEM's products,
@@ -2066,15 +1161,23 @@ static cudaError_t launch_multi_gemv(const cplx* A, const cplx* X, cplx* Y, long
 }
 
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
-  // Y = A X in one pass over A (K = 3, 4 with the 4-slice layout)
-  cudaError_t e;
-  switch (args.K) {
-    case 1: e = launch_multi_gemv<1>(args.A, args.X, args.Y, args.n, s); break;
-    case 2: e = launch_multi_gemv<2>(args.A, args.X, args.Y, args.n, s); break;
-    case 3: e = launch_multi_gemv<3>(args.A, args.X, args.Y, args.n, s); break;
-    default: e = launch_multi_gemv<4>(args.A, args.X, args.Y, args.n, s); break;
+  // Y = A X in passes of up to 4 columns (K = 3, 4 with the 4-slice layout)
+  for (int c0 = 0; c0 < args.K; c0 += 4) {
+    const cplx* X = args.X + (size_t)c0 * args.n;
+    cplx* Y = args.Y + (size_t)c0 * args.n;
+    cudaError_t e;
+    switch (args.K - c0 < 4 ? args.K - c0 : 4) {
+      case 1: e = launch_multi_gemv<1>(args.A, X, Y, args.n, s); break;
+      case 2: e = launch_multi_gemv<2>(args.A, X, Y, args.n, s); break;
+      case 3: e = launch_multi_gemv<3>(args.A, X, Y, args.n, s); break;
+      default: e = launch_multi_gemv<4>(args.A, X, Y, args.n, s); break;
+    }
+    if (e != cudaSuccess) return e;
   }
-  if (e != cudaSuccess) return e;
+  return launch_sem_products(args, s);
+}
+
+cudaError_t launch_sem_products(SemArgs& args, cudaStream_t s) {
   int G = solver_grid_blocks();
   void* params[] = {&args};
   note_launch();
@@ -2082,86 +1185,355 @@ cudaError_t launch_sem(SemArgs& args, cudaStream_t s) {
                                      kRingBytes, s);
 }
 
-#ifndef EWB_BAL_DAMP
-#define EWB_BAL_DAMP 0.7
-#endif
-constexpr double kBalDamp = EWB_BAL_DAMP;
-
-cudaError_t calibrate_rows(const cplx* A, long long n, int iters, double* stats,
-                           cudaStream_t s) {
-  const int G = solver_grid_blocks();
-  if (G > kMaxBalGrid || n < 2LL * G) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute((const void*)k_calib, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kRingBytes);
-  cplx *x = nullptr, *y = nullptr;
-  unsigned long long* t = nullptr;
-  cudaError_t e = cudaMalloc(&x, sizeof(cplx) * n);
-  if (!e) e = cudaMalloc(&y, sizeof(cplx) * n);
-  if (!e) e = cudaMalloc(&t, sizeof(unsigned long long) * 3 * G);
-  if (!e) e = cudaMemsetAsync(x, 0, sizeof(cplx) * n, s);
-  std::vector<double> cumw(G + 1), speed(G, 0.0);
-  std::vector<unsigned long long> th(3 * G);
-  for (int b = 0; b <= G; ++b) cumw[b] = (double)b / G;
-  int zero = 0;
-  if (!e) e = cudaMemcpyToSymbolAsync(c_bal_g, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-  void* params[] = {(void*)&A, (void*)&x, (void*)&y, (void*)&n, (void*)&t};
-  double spread0 = 0.0, spread1 = 0.0, mean0 = 0.0, mean1 = 0.0;
-  for (int it = 0; !e && it <= iters; ++it) {
-    // two launches per split: the first warms up, the second is measured
-    for (int rep = 0; !e && rep < 2; ++rep) {
-      note_launch();
-      e = cudaLaunchCooperativeKernel((const void*)k_calib, dim3(G), dim3(kSolveThreads), params,
-                                      kRingBytes, s);
+// ---------------------------------------------------------------------
+// Operator GMRES (matrix-free seam): the reference's algorithm
+// (linsolve.py:107-210) with the operator applied by separate launches and
+// every vector, coefficient and decision on the device (OpState).  MGS is
+// the reference's sequential form (one grid reduction per projection, the
+// update of projection i fused with the dot of projection i+1).
+// ---------------------------------------------------------------------
+// operator input for vector v: z = P^{-1} v, vt = mask_N z, vu = -mask_D z
+__device__ void op_stage_input(const OpArgs& a, const cplx* v, bool precond) {
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  const bool pc = precond && a.pinv != nullptr;
+  if (!pc && !a.kinds) {   // plain copy (any n)
+    for (long long k = tid; k < n; k += nth) {
+      a.z[k] = v[k];
+      a.vt[k] = v[k];
     }
-    if (!e) e = cudaMemcpyAsync(th.data(), t, sizeof(unsigned long long) * 3 * G,
-                                cudaMemcpyDeviceToHost, s);
-    if (!e) e = cudaStreamSynchronize(s);
-    if (e) break;
-    double tmax = 0.0, tmin = 1e30, tsum = 0.0;
-    for (int b = 0; b < G; ++b) {
-      const double tb = (double)th[b];
-      tmax = tb > tmax ? tb : tmax;
-      tmin = tb < tmin ? tb : tmin;
-      tsum += tb;
-    }
-    if (it == 0) { spread0 = tmax - tmin; mean0 = tsum / G; }
-    spread1 = tmax - tmin;
-    mean1 = tsum / G;
-    if (it == iters) break;   // last pass only measures the final split
-    // damped fixed-point step on the finish times: a CTA that finishes
-    // later than the mean gives rows away in proportion (the rates depend
-    // on the split through the contention pattern, so no one-shot solve)
-    const double tmean = tsum / G;
-    double fsum = 0.0;
-    for (int b = 0; b < G; ++b) {
-      const double f = cumw[b + 1] - cumw[b];
-      speed[b] = f * (1.0 + kBalDamp * (tmean - (double)th[b]) / tmean);
-      fsum += speed[b];
-    }
-    double acc = 0.0;
-    for (int b = 0; b < G; ++b) {
-      cumw[b] = acc;
-      acc += speed[b] / fsum;
-    }
-    cumw[G] = 1.0;
-    e = cudaMemcpyToSymbolAsync(c_cumw, cumw.data(), sizeof(double) * (G + 1), 0,
-                                cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemcpyToSymbolAsync(c_bal_g, &G, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+    return;
   }
-  if (stats) {
-    stats[0] = spread0 * 1e-3; stats[1] = mean0 * 1e-3;   // us, equal split
-    stats[2] = spread1 * 1e-3; stats[3] = mean1 * 1e-3;   // us, calibrated split
+  for (long long e = tid; e < n / 3; e += nth) {
+    cplx z[3] = {v[3 * e], v[3 * e + 1], v[3 * e + 2]};
+    if (pc) {
+      const cplx* P = a.pinv + 9 * e;
+      cplx o[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {   // einsum('bij,bj->bi') order
+        cplx s = P[3 * r] * z[0];
+        s = s + P[3 * r + 1] * z[1];
+        s = s + P[3 * r + 2] * z[2];
+        o[r] = s;
+      }
+      z[0] = o[0]; z[1] = o[1]; z[2] = o[2];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long k = 3 * e + c;
+      a.z[k] = z[c];
+      const bool dir = a.kinds && a.kinds[k] == kDirichlet;
+      a.vt[k] = dir ? cplx{0.0, 0.0} : z[c];
+      if (a.vu) a.vu[k] = dir ? cplx{-z[c].re, -z[c].im} : cplx{0.0, 0.0};
+    }
   }
-  cudaStreamSynchronize(s);
-  cudaFree(x);
-  cudaFree(y);
-  cudaFree(t);
-  return e;
 }
 
-cudaError_t reset_row_balance(cudaStream_t s) {
-  int zero = 0;
-  return cudaMemcpyToSymbolAsync(c_bal_g, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+// Scalar state: every CTA keeps an identical copy of the head (OpHead) in
+// shared memory, modified by its thread 0 only, and block 0 writes it back
+// after a grid barrier that follows every CTA's read.
+
+// cycle start from the residual in a.r, |r| = s.rnorm (linsolve.py:153-163)
+__device__ void op_start_cycle(cg::grid_group& grid, const OpArgs& a, OpHead& s) {
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  const double beta = s.rnorm;
+  for (long long k = tid; k < n; k += nth) {
+    a.V[k] = {a.r[k].re / beta, a.r[k].im / beta};
+    a.rs[k] = a.r[k];
+  }
+  grid.sync();
+  op_stage_input(a, a.V, true);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s.m = min(a.restart, a.maxiter - s.its);
+    s.j = 0;
+    s.used = 0;
+    s.in_cycle = 1;
+    s.cycle_open = 1;
+    if (blockIdx.x == 0) {
+      a.st->g[0] = {beta, 0.0};
+      for (int k = 1; k <= s.m; ++k) a.st->g[k] = {0.0, 0.0};
+    }
+  }
+  __syncthreads();
+}
+
+// exit on the literal residual (linsolve.py:200-205): next apply is A x
+__device__ void op_request_literal(const OpArgs& a, OpHead& s) {
+  op_stage_input(a, a.x, false);
+  __syncthreads();
+  if (threadIdx.x == 0) s.lit_pending = 1;
+  __syncthreads();
+}
+
+__device__ void op_exit(const OpArgs& a, OpHead& s) {
+  if (threadIdx.x == 0) {
+    s.done = 1;
+    s.final_res = s.res;
+    s.converged = s.res <= a.tol;
+  }
+  __syncthreads();
+}
+
+__device__ void op_writeback(cg::grid_group& grid, const OpArgs& a, const OpHead& s) {
+  grid.sync();   // every CTA has read the old head
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.st->h = s;
+}
+
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_op_begin(OpArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  GridRed R{a.partial, 0};
+  __shared__ OpHead s;
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  if (threadIdx.x == 0) memset(&s, 0, sizeof(OpHead));
+  __syncthreads();
+  double v2[2] = {0.0, 0.0};
+  for (long long k = tid; k < n; k += nth) {
+    v2[0] += abs2(a.b[k]);
+    if (a.has_x0) v2[1] += (a.x[k].re != 0.0 || a.x[k].im != 0.0);
+    else a.x[k] = {0.0, 0.0};
+  }
+  grid_sum(grid, R, v2);
+  const double nb = sqrt(v2[0]);
+  if (threadIdx.x == 0) s.nb = nb;
+  __syncthreads();
+  if (nb == 0.0) {   // linsolve.py:136-140
+    for (long long k = tid; k < n; k += nth) a.x[k] = {0.0, 0.0};
+    if (threadIdx.x == 0) { s.done = 1; s.converged = 1; }
+    __syncthreads();
+  } else if (v2[1] > 0.0 && !a.ax0) {   // r0 = b - A x0 needs an application
+    op_request_literal(a, s);
+  } else {
+    double q[1] = {0.0};
+    for (long long k = tid; k < n; k += nth) {
+      const cplx r = v2[1] > 0.0 ? a.b[k] - a.ax0[k] : a.b[k];
+      a.r[k] = r;
+      q[0] += abs2(r);
+    }
+    grid_sum(grid, R, q);
+    const double rn = sqrt(q[0]), res = rn / nb;
+    if (v2[1] > 0.0 && res <= a.tol) {
+      op_request_literal(a, s);   // a 0-iteration exit is decided on b - A x0
+    } else {
+      if (threadIdx.x == 0) {
+        s.rnorm = rn; s.res = res; s.init_res = res; s.n_hist = 1;
+        if (tid == 0) a.hist[0] = res;
+      }
+      __syncthreads();
+      if (res <= a.tol || a.maxiter <= 0) op_exit(a, s);
+      else op_start_cycle(grid, a, s);
+    }
+  }
+  op_writeback(grid, a, s);
+}
+
+// r = b - A x from the literal application; exit or restart
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_op_settle(OpArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  GridRed R{a.partial, 0};
+  __shared__ OpHead s;
+  if (threadIdx.x == 0) s = a.st->h;
+  __syncthreads();
+  if (!s.lit_pending) return;   // uniform over the grid
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  double q[1] = {0.0};
+  for (long long k = tid; k < n; k += nth) {
+    const cplx r = a.b[k] - a.w[k];
+    a.r[k] = r;
+    q[0] += abs2(r);
+  }
+  grid_sum(grid, R, q);
+  const double rn = sqrt(q[0]), res = rn / s.nb;
+  if (threadIdx.x == 0) {
+    s.rnorm = rn;
+    s.res = res;
+    s.lit_pending = 0;
+    s.applies += 1;
+    if (s.n_hist == 0) {   // the initial residual (linsolve.py:144-147)
+      s.init_res = res;
+      s.n_hist = 1;
+      if (tid == 0) a.hist[0] = res;
+    }
+  }
+  __syncthreads();
+  if (res <= a.tol || s.its >= a.maxiter) op_exit(a, s);
+  else op_start_cycle(grid, a, s);
+  op_writeback(grid, a, s);
+}
+
+// one Arnoldi step on w = A P^{-1} v_j (linsolve.py:164-194)
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_op_step(OpArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  GridRed R{a.partial, 0};
+  __shared__ OpHead s;
+  __shared__ cplx hc[kMaxRestart + 1];            // new Hessenberg column
+  __shared__ cplx cs_new, sn_new, gj_new, gj1_new;
+  if (threadIdx.x == 0) s = a.st->h;
+  __syncthreads();
+  if (!s.in_cycle) return;   // uniform over the grid
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  const int j = s.j;
+  cplx* w = a.r;   // working vector (the cycle's start residual is in a.rs)
+  // MGS: h_i = <v_i, w>, w -= h_i v_i; the update of projection i-1 and the
+  // dot of projection i share one sweep; the last sweep gives |w|^2
+  cplx h = {0.0, 0.0};
+  for (int i = 0; i <= j + 1; ++i) {
+    double d[2] = {0.0, 0.0};
+    const cplx* vi = a.V + (size_t)i * n;
+    const cplx* vp = a.V + (size_t)(i > 0 ? i - 1 : 0) * n;
+    for (long long k = tid; k < n; k += nth) {
+      cplx wk;
+      if (i == 0) {
+        wk = a.w[k];
+        a.W[(size_t)j * n + k] = wk;
+      } else {
+        wk = w[k] - h * vp[k];
+      }
+      w[k] = wk;
+      if (i <= j) {
+        const cplx p = conj(vi[k]) * wk;
+        d[0] += p.re; d[1] += p.im;
+      } else {
+        d[0] += abs2(wk);
+      }
+    }
+    grid_sum(grid, R, d);
+    h = i <= j ? cplx{d[0], d[1]} : cplx{sqrt(d[0]), 0.0};
+    if (threadIdx.x == 0) hc[i] = h;
+  }
+  __syncthreads();
+  const double hn = hc[j + 1].re;
+  if (threadIdx.x == 0) {   // Givens, identical in every CTA
+    const OpState* S = a.st;
+    for (int i = 0; i < j; ++i) {   // previous rotations on the new column
+      const cplx hi = hc[i], hi1 = hc[i + 1];
+      hc[i] = S->cs[i] * hi + S->sn[i] * hi1;
+      hc[i + 1] = (-conj(S->sn[i])) * hi + conj(S->cs[i]) * hi1;
+    }
+    const cplx hjj = hc[j], hj1 = hc[j + 1];
+    const double ahj = hypot(hjj.re, hjj.im), ahn = hypot(hj1.re, hj1.im);
+    const double den = sqrt(ahj * ahj + ahn * ahn);
+    cplx c, sn;
+    if (den == 0.0) {
+      c = {1.0, 0.0}; sn = {0.0, 0.0};
+    } else if (hjj.re == 0.0 && hjj.im == 0.0) {
+      c = {0.0, 0.0}; sn = {1.0, 0.0};
+    } else {
+      c = {ahj / den, 0.0};
+      const cplx ph = {hjj.re / ahj, hjj.im / ahj};
+      const cplx t = ph * conj(hj1);
+      sn = {t.re / den, t.im / den};
+    }
+    hc[j] = c * hjj + sn * hj1;
+    hc[j + 1] = {0.0, 0.0};
+    const cplx gj = S->g[j];
+    cs_new = c;
+    sn_new = sn;
+    gj1_new = (-conj(sn)) * gj;
+    gj_new = c * gj;
+    const double est = hypot(gj1_new.re, gj1_new.im) / s.nb;
+    if (tid == 0 && s.n_hist < a.hist_cap) a.hist[s.n_hist] = est;
+    s.n_hist += 1;
+    s.its += 1;
+    s.applies += 1;
+    s.used = j + 1;
+    s.j = j + 1;
+    if (est <= a.tol || j + 1 == s.m) s.in_cycle = 0;
+  }
+  __syncthreads();
+  grid.sync();   // every CTA has read cs, sn, g before block 0 updates them
+  if (blockIdx.x == 0) {
+    OpState* S = a.st;
+    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) S->H[i * kMaxRestart + j] = hc[i];
+    if (threadIdx.x == 0) {
+      S->cs[j] = cs_new;
+      S->sn[j] = sn_new;
+      S->g[j] = gj_new;
+      S->g[j + 1] = gj1_new;
+      S->h = s;
+    }
+  }
+  if (s.in_cycle) {
+    cplx* vn = a.V + (size_t)(j + 1) * n;
+    if (hn > 0.0)
+      for (long long k = tid; k < n; k += nth) vn[k] = {w[k].re / hn, w[k].im / hn};
+    grid.sync();
+    op_stage_input(a, vn, true);
+  }
+}
+
+// back substitution, x update, restart residual (linsolve.py:195-201)
+__global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_op_cycle_end(OpArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  GridRed R{a.partial, 0};
+  __shared__ OpHead s;
+  __shared__ cplx y[kMaxRestart];
+  if (threadIdx.x == 0) s = a.st->h;
+  __syncthreads();
+  if (!s.cycle_open || s.in_cycle) return;   // uniform over the grid
+  const long long n = a.n, tid = gtid(), nth = gthreads();
+  const int used = s.used;
+  if (threadIdx.x == 0) {
+    const OpState* S = a.st;
+    for (int i = used - 1; i >= 0; --i) {
+      cplx t = S->g[i];
+      for (int k = i + 1; k < used; ++k) t = t - S->H[i * kMaxRestart + k] * y[k];
+      y[i] = cdiv(t, S->H[i * kMaxRestart + i]);
+    }
+  }
+  __syncthreads();
+  // x += P^{-1} (V y) and r = r_start - W y (= b - A x_new up to rounding);
+  // unit u = element (3 DOFs, preconditioned) or a single DOF
+  const bool pc = a.pinv != nullptr;
+  const int per = pc ? 3 : 1;
+  double q[1] = {0.0};
+  for (long long e = tid; e < n / per; e += nth) {
+    cplx u[3];
+    for (int c = 0; c < per; ++c) {
+      const long long k = per * e + c;
+      cplx sv = {0.0, 0.0}, sr = a.rs[k];
+      for (int i = 0; i < used; ++i) {
+        cfma(sv, a.V[(size_t)i * n + k], y[i]);
+        sr = sr - y[i] * a.W[(size_t)i * n + k];
+      }
+      u[c] = sv;
+      a.r[k] = sr;
+      q[0] += abs2(sr);
+    }
+    if (pc) {
+      const cplx* P = a.pinv + 9 * e;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {   // einsum order, as block_diag_precond
+        cplx t = P[3 * r] * u[0];
+        t = t + P[3 * r + 1] * u[1];
+        t = t + P[3 * r + 2] * u[2];
+        a.x[3 * e + r] = a.x[3 * e + r] + t;
+      }
+    } else {
+      a.x[e] = a.x[e] + u[0];
+    }
+  }
+  grid_sum(grid, R, q);   // also orders the x update before the staging below
+  const double rn = sqrt(q[0]), res = rn / s.nb;
+  if (threadIdx.x == 0) {
+    s.cycle_open = 0;
+    s.rnorm = rn;
+    s.res = res;
+  }
+  __syncthreads();
+  if (res <= a.tol || s.its >= a.maxiter) op_request_literal(a, s);
+  else op_start_cycle(grid, a, s);
+  op_writeback(grid, a, s);
+}
+
+cudaError_t launch_op_gmres(int phase, OpArgs& args, cudaStream_t s) {
+  const void* fn = phase == 0 ? (const void*)k_op_begin
+                   : phase == 1 ? (const void*)k_op_step
+                   : phase == 2 ? (const void*)k_op_cycle_end
+                                : (const void*)k_op_settle;
+  int G = solver_grid_blocks();
+  void* params[] = {&args};
+  note_launch();
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kSolveThreads), params, 0, s);
 }
 
 cudaError_t launch_gemv_batched(const cplx* A, const cplx* x, cplx* y, long long n, int batch,

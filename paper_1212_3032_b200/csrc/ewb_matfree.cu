@@ -74,8 +74,11 @@ struct MfArgs {
   cplx* pinv;           // (n_e,3,3) or nullptr
   const double* diag_base;
   int* flags;
+  const int* gate;      // nullable: the application is skipped when *gate == 0
   int K, nchunk, chunk_cols;
 };
+#define EWB_MF_GATE \
+  if (m.gate && *m.gate == 0) return;
 
 #ifndef EWB_MF_MINB
 #define EWB_MF_MINB 3
@@ -91,6 +94,7 @@ constexpr int kMfQUnroll = EWB_MF_QUNROLL;
 template <int K, bool USE_U>
 __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_MF_MINB)
     k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
+  EWB_MF_GATE
   __shared__ double s_geo[kMfTile][8];        // cx cy cz diam nx ny nz area
   __shared__ double s_y[kMfTile][30];         // 3 far + 7 mid points
   __shared__ cplx s_vt[kMfTile][K][3];
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
 
 template <int K, bool USE_U>
 __global__ void __launch_bounds__(128) k_mf_near(Geo g, Phys<true> ph, MfArgs m, int n_near) {
+  EWB_MF_GATE
   const int lane = threadIdx.x & 31;
   const int wp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wp >= n_near) return;
@@ -278,6 +283,7 @@ __device__ bool inv3_mf(const cplx Ain[3][3], cplx Inv[3][3]) {
 // Self term + fixed-order final sum:  y_i = sum_chunks + sum_near + D_i v_i.
 template <int K, bool USE_U>
 __global__ void __launch_bounds__(128) k_mf_self(Geo g, Phys<true> ph, MfArgs m) {
+  EWB_MF_GATE
   const int lane = threadIdx.x & 31;
   const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= g.n_e) return;
@@ -376,13 +382,13 @@ size_t mf_workspace_bytes(const Context& c, int K) {
 
 cudaError_t launch_matfree(Context& c, double ore, double oim, const cplx* vt, const cplx* vu,
                            int K, cplx* y, const uint8_t* kinds, cplx* pinv, void* ws,
-                           cudaStream_t s) {
+                           const int* gate, cudaStream_t s) {
   cudaError_t e = upload_series(s);
   if (e) return e;
   Phys<true> ph{freq_const(c, ore, oim)};
   MfArgs m{};
   m.vt = vt; m.vu = vu; m.y = y; m.kinds = kinds; m.pinv = pinv;
-  m.diag_base = c.diag_base; m.flags = c.flags; m.K = K;
+  m.diag_base = c.diag_base; m.flags = c.flags; m.K = K; m.gate = gate;
   m.nchunk = mf_chunks(c);
   m.chunk_cols = (c.n_e + m.nchunk - 1) / m.nchunk;
   size_t N = 3 * (size_t)c.n_e;

@@ -35,7 +35,6 @@ import numpy as np
 
 from . import _lib
 from .assembly import DIRICHLET, NEUMANN, Assembler
-from .config import SweepConfig
 from .linsolve import SolveStats, block_diag_precond, gmres_device, sem_device
 from .transform import (check_residue, eta_from_kappa, forward_mft_batch, frequency_grid,
                         windowed_inverse_device)
@@ -111,9 +110,12 @@ def gather_frequency_results(local: dict, n_freq: int, width: int, dist=None):
     return vals, meta
 
 
+MAX_SEM_DEPTH = 8   # SEM history columns the device QR holds (kMaxSem)
+
+
 def n_hist_passes(K: int) -> int:
-    """Passes over A of one SEM product Y = A X (all K <= 4 columns in one pass)."""
-    return 1 if K > 0 else 0
+    """Passes over A of one SEM product Y = A X (up to 4 columns per pass)."""
+    return (K + 3) // 4 if K > 0 else 0
 
 
 class DeviceSweep:
@@ -126,11 +128,16 @@ class DeviceSweep:
     roofline report).
     """
 
-    def __init__(self, cfg: SweepConfig, assembler: Assembler | None = None,
+    def __init__(self, cfg, assembler: Assembler | None = None,
                  frequencies: list | None = None, assembly_batch: int | None = None):
         import torch
 
         _lib.require_cuda()
+        if cfg.sem_enabled and cfg.sem_depth > MAX_SEM_DEPTH:
+            # rejected before any assembly or solve (the reference accepts any
+            # depth; the device SEM keeps up to 8 history columns)
+            raise ValueError(f"sem_depth {cfg.sem_depth} > {MAX_SEM_DEPTH} is not supported "
+                             "on the device path")
         self.cfg = cfg
         self.eta = eta_from_kappa(cfg.kappa, cfg.period)
         self.omegas = frequency_grid(cfg.period, cfg.n_omega, self.eta)
@@ -164,24 +171,6 @@ class DeviceSweep:
         """Prescribed spectra of frequencies ks as an (nf, N) device view/copy."""
         return (self.P[ks[0]:ks[-1] + 1] if ks == list(range(ks[0], ks[-1] + 1))
                 else self.P[ks].contiguous())
-
-    def _overlap_buffers(self, nb: int) -> bool:
-        """Two batch buffers for the overlapped assembly, if HBM allows."""
-        import torch
-
-        from .assembly import SystemBatch
-
-        if getattr(self, "_bufs", None) is not None and self._bufs[0].A.shape[0] >= nb:
-            return True
-        self._bufs = None
-        self.batch = None
-        torch.cuda.empty_cache()
-        free, _ = torch.cuda.mem_get_info()
-        need = 2 * nb * (16 * self.n * self.n + 16 * 4 * self.n)
-        if need > 0.8 * free:
-            return False
-        self._bufs = [SystemBatch.allocate(nb, self.n), SystemBatch.allocate(nb, self.n)]
-        return True
 
     def batch_size(self) -> int:
         """Frequencies assembled per pass over the element pairs.
@@ -246,9 +235,9 @@ class DeviceSweep:
             torch.cuda.synchronize()
             st.k, st.omega = k, omega
             st.seconds = time.perf_counter() - t0
-            st.matvecs = op.applications
+            st.matvecs += op.applications   # GMRES's applications + the b / SEM passes
             stats[k] = st
-            self.phase["applications"] += op.applications
+            self.phase["applications"] += st.matvecs
             self.phase["solves"] += 1
             self.phase["seconds"] += st.seconds
             self.sol[k] = x
@@ -256,7 +245,7 @@ class DeviceSweep:
                 self.hist[1:] = self.hist[:-1].clone()
                 self.hist[0] = x
                 n_hist = min(n_hist + 1, K)
-            log.info("k=%d its=%d applications=%d %.2fs", k, st.iterations, op.applications,
+            log.info("k=%d its=%d applications=%d %.2fs", k, st.iterations, st.matvecs,
                      st.seconds)
         return stats
 
@@ -307,17 +296,7 @@ class DeviceSweep:
         conc_env = os.environ.get("EWB_CONCURRENT_SOLVES", "auto")
         concurrent = (not cfg.sem_enabled
                       and (conc_env == "1" or (conc_env == "auto" and self.n < 12000)))
-        # overlap (opt-in, EWB_OVERLAP_ASSEMBLY=1): batch g+1's far pairs are
-        # assembled on a few SMs while batch g is solved on the others; needs
-        # two batch buffers.  Measured on cfg2: it hides half
-        # the assembly but the concurrent FP64 work slows every GMRES pass by
-        # 2.6-3.9 %, a net loss, so it is off by default.
-        n_ovl = int(os.environ.get("EWB_OVERLAP_SMS", "8"))
-        overlap = (os.environ.get("EWB_OVERLAP_ASSEMBLY", "0") == "1" and not concurrent
-                   and len(groups) > 1 and n_ovl > 0 and self._overlap_buffers(nb))
-        stream_a = torch.cuda.Stream() if overlap else None
         full_ctas = int(lib.ewb_solver_ctas())
-        pending = None   # index of the group whose assembly was begun on stream_a
         for gi, group in enumerate(groups):
             ks = [self.frequencies[i] for i in group]
             idx = group[0]
@@ -325,22 +304,11 @@ class DeviceSweep:
                 e_a = torch.cuda.Event(enable_timing=True)
                 e_b = torch.cuda.Event(enable_timing=True)
                 e_a.record()
-                if pending == gi:
-                    buf = self._bufs[gi % 2]
-                    asm.assemble_system_multi_finish()
-                    torch.cuda.current_stream().wait_stream(stream_a)
-                    asm.assemble_system_multi_self()
-                    members = [buf.member(f) for f in range(len(group))]
-                    pending = None
-                elif complex(self.omegas[ks[0]]) != 0:
-                    out = self._bufs[gi % 2] if overlap else self.batch
-                    out = asm.assemble_system_multi(
-                        [self.omegas[k] for k in ks], cfg.bcs, self._p_rows(ks), out=out,
+                if complex(self.omegas[ks[0]]) != 0:
+                    self.batch = asm.assemble_system_multi(
+                        [self.omegas[k] for k in ks], cfg.bcs, self._p_rows(ks), out=self.batch,
                         flags=flags_all[group[0]:group[-1] + 1], check=False)
-                    if overlap:
-                        self._bufs[gi % 2] = out
-                    else:
-                        self.batch = out
+                    out = self.batch
                     members = [out.member(f) for f in range(len(group))]
                 else:
                     omega = complex(self.omegas[ks[0]])
@@ -352,34 +320,12 @@ class DeviceSweep:
                     members = [sysm]
                 e_b.record()
                 asm_ev.append((e_a, e_b))
-                nxt = groups[gi + 1] if gi + 1 < len(groups) else None
-                if (overlap and nxt is not None
-                        and complex(self.omegas[self.frequencies[nxt[0]]]) != 0):
-                    # batch gi+1 starts on n_ovl SMs once batch gi's diagonal
-                    # kernel (shared scratch) and batch gi-1's solves (its buffer)
-                    # are done; batch gi's solves use the other SMs
-                    kn = [self.frequencies[i] for i in nxt]
-                    stream_a.wait_stream(torch.cuda.current_stream())
-                    self._bufs[(gi + 1) % 2] = asm.assemble_system_multi_begin(
-                        [self.omegas[k] for k in kn], cfg.bcs, self._p_rows(kn),
-                        self._bufs[(gi + 1) % 2], flags_all[nxt[0]:nxt[-1] + 1], n_ovl,
-                        stream_a)
-                    pending = gi + 1
-                    _lib.check(lib.ewb_set_solver_ctas(max(1, full_ctas - n_ovl)))
             except SweepError:
                 raise
             except Exception as exc:
                 _lib.check(lib.ewb_set_solver_ctas(full_ctas))
                 omega = complex(self.omegas[ks[0]])
                 raise SweepError(f"frequency index {ks[0]} (omega={omega:.6g}): {exc}") from exc
-            if (os.environ.get("EWB_ROW_BALANCE") == "1" and self.n >= 4096
-                    and not getattr(self, "_balanced", False)):
-                # opt-in: split the solver rows by measured per-SM speed
-                # (measured slower on cfg2; kept as an experiment)
-                from .linsolve import calibrate_row_balance
-
-                calibrate_row_balance(members[0].A)
-                self._balanced = True
             if concurrent and len(group) > 1:
                 # independent members (no SEM chain): solved side by side
                 # (measured: 1.4-1.8x faster at N = 3840-4096, 1.06-1.1x at
@@ -489,7 +435,7 @@ class DeviceSweep:
         return torch.where(neu[None, :], self.sol, self.P)
 
 
-def run_sweep(cfg: SweepConfig, full_field: bool = False, assembler: Assembler | None = None,
+def run_sweep(cfg, full_field: bool = False, assembler: Assembler | None = None,
               distributed: bool = True, _sweep_out: list | None = None,
               matrix_free: bool | None = None) -> SweepResult:
     """Run the transient analysis described by ``cfg`` on the GPU.
@@ -562,7 +508,7 @@ def run_sweep(cfg: SweepConfig, full_field: bool = False, assembler: Assembler |
                        full_field=field_hist)
 
 
-def build_manifest(cfg: SweepConfig, eta: float, seconds: float, failed: list) -> dict:
+def build_manifest(cfg, eta: float, seconds: float, failed: list) -> dict:
     """driver.py:179-201."""
     dw = 2.0 * math.pi / cfg.period
     return {
@@ -575,7 +521,7 @@ def build_manifest(cfg: SweepConfig, eta: float, seconds: float, failed: list) -
     }
 
 
-def emit_outputs(result: SweepResult, cfg: SweepConfig) -> dict:
+def emit_outputs(result: SweepResult, cfg) -> dict:
     """history_<probe>.csv, solve_stats.csv, manifest.txt (driver.py:248-283)."""
     out = Path(cfg.output_dir)
     out.mkdir(parents=True, exist_ok=True)

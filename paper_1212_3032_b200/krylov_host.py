@@ -1,20 +1,31 @@
 """GMRES / SEM for operator callables (the matrix-free seam, linsolve.py:73-77).
 
-Same algorithm as the reference (right preconditioning, MGS Arnoldi,
-complex Givens with real cosine, true-residual restart test;
-linsolve.py:107-210) with every vector on the device: the operator is
-one expensive launch per iteration (ewb_matfree_apply), the Arnoldi
-dot/axpy run on device tensors with the coefficients kept on the device,
-and the (j+2)-entry Hessenberg column is read back once per iteration for
-the Givens update — the only host synchronisation in the loop.
+The reference's algorithm (right preconditioning, MGS Arnoldi, complex
+Givens with real cosine, exit decided on the literal residual b - A x;
+linsolve.py:107-210) with every vector, coefficient and decision on the
+device: ``ewb_opgmres_phase`` kernels hold the whole solver state in HBM
+(``ewb_op_head`` + Hessenberg/Givens arrays), the operator is applied by
+its own launches between them, and the host only enqueues.  Operator
+applications carry a device gate word, so a chunk of iterations is queued
+ahead and the ones past convergence do no work; the host reads the
+4-byte ``done`` word once per chunk (one synchronisation per solve at the
+sizes of cfg5, not one per iteration).
+
+A generic Python callable cannot be gated: it is called once per
+iteration after reading the gate word (the seam accepts any callable; the
+B200 hot path is ``MatrixFreeOperator``).
+
+SEM (linsolve.py:213-242) for an operator: Y = A X from one multi-vector
+application, then the device CGS2 QR / rank filter / solve of
+``ewb_sem_from_products`` (the dense path's ``k_sem``).
 """
 
 from __future__ import annotations
 
+import ctypes
 import logging
-import os
 
-import numpy as np
+from . import _lib
 
 log = logging.getLogger(__name__)
 
@@ -25,122 +36,164 @@ def _torch():
     return torch
 
 
+class OpHead(ctypes.Structure):
+    """``ewb_op_head`` (include/ewbem_b200.h)."""
+
+    _fields_ = [(nm, ctypes.c_int32) for nm in
+                ("in_cycle", "lit_pending", "done", "converged", "iterations", "j", "m", "used",
+                 "cycle_open", "n_hist", "applications", "pad")] + \
+               [(nm, ctypes.c_double) for nm in
+                ("norm_b", "rnorm", "residual", "init_residual", "final_residual")]
+
+
+class OpSolver:
+    """Device workspace + enqueue logic of one operator GMRES (reusable)."""
+
+    CHUNK = 8   # Arnoldi steps queued between two reads of the `done` word
+
+    def __init__(self, n: int, restart: int, maxiter: int):
+        torch = _torch()
+        lib = _lib.require_cuda()
+        self.lib = lib
+        self.n, self.restart, self.maxiter = n, restart, maxiter
+        nbytes = int(lib.ewb_opgmres_workspace_bytes(n, restart))
+        if nbytes < 0:
+            raise ValueError("restart must be in [1, 128]")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        from .linsolve import gmres_hist_cap
+
+        self.hist_cap = gmres_hist_cap(maxiter, restart)
+        self.hist = torch.zeros(self.hist_cap, dtype=torch.float64, device="cuda")
+        ptrs = [ctypes.c_void_p() for _ in range(4)]
+        gates = [ctypes.POINTER(ctypes.c_int32)() for _ in range(2)]
+        _lib.check(lib.ewb_opgmres_buffers(_lib.ptr(self.ws), n, restart,
+                                           *[ctypes.byref(p) for p in ptrs],
+                                           *[ctypes.byref(g) for g in gates]),
+                   "ewb_opgmres_buffers")
+        self.z_ptr, self.vt_ptr, self.vu_ptr, self.w_ptr = (p.value for p in ptrs)
+        self.gate_cycle = ctypes.cast(gates[0], ctypes.c_void_p).value
+        self.gate_lit = ctypes.cast(gates[1], ctypes.c_void_p).value
+        self.head_host = torch.empty(ctypes.sizeof(OpHead), dtype=torch.uint8, pin_memory=True)
+        self.done_host = torch.empty(4, dtype=torch.uint8, pin_memory=True)
+        base = _lib.ptr(self.ws)
+        off = OpHead.done.offset
+        self.ws_done = self.ws[off:off + 4]
+        self.ws_head = self.ws[:ctypes.sizeof(OpHead)]
+        self.z = self._view(self.z_ptr - base)
+        self.w = self._view(self.w_ptr - base)
+
+    def _view(self, off):
+        return self.ws[off:off + 16 * self.n].view(_torch().complex128)
+
+    def _phase(self, ph, b, x, has_x0, ax0, pinv, kinds, split_u, tol):
+        _lib.check(self.lib.ewb_opgmres_phase(
+            ph, _lib.ptr(self.ws), self.ws.numel(), _lib.ptr(b), _lib.ptr(x), int(has_x0),
+            _lib.ptr(ax0) if ax0 is not None else None,
+            _lib.ptr(pinv) if pinv is not None else None,
+            _lib.ptr(kinds) if kinds is not None else None, int(split_u), self.n, float(tol),
+            self.restart, self.maxiter, _lib.ptr(self.hist), self.hist_cap,
+            _lib.stream_handle()), "ewb_opgmres_phase")
+
+    def head(self) -> OpHead:
+        self.head_host.copy_(self.ws_head)
+        return OpHead.from_buffer_copy(self.head_host.numpy().tobytes())
+
+    def solve(self, op, b, x, has_x0, tol, pinv, ax0=None):
+        """x <- GMRES solution of op x = b; returns the final ewb_op_head."""
+        gated = hasattr(op, "apply_gated")
+        kinds = op.kinds_dev if gated and not op.all_neumann else None
+        split_u = kinds is not None
+        args = (b, x, has_x0, ax0, pinv, kinds, split_u, tol)
+
+        def apply(gate):
+            if gated:
+                op.apply_gated(self.vt_ptr, self.vu_ptr if split_u else None, self.w_ptr, gate)
+            else:   # a plain callable: decide on the host
+                self.done_host.copy_(self.ws[OpHead.in_cycle.offset if gate == self.gate_cycle
+                                             else OpHead.lit_pending.offset:][:4])
+                if int(self.done_host.view(_torch().int32)[0]):
+                    self.w.copy_(op(self.z))
+
+        self._phase(0, *args)
+        apply(self.gate_lit)
+        self._phase(3, *args)
+        chunk = self.CHUNK if gated else 1
+        while True:
+            self.done_host.copy_(self.ws_done)
+            if int(self.done_host.view(_torch().int32)[0]):
+                break
+            for _ in range(chunk):
+                apply(self.gate_cycle)
+                self._phase(1, *args)
+            self._phase(2, *args)
+            apply(self.gate_lit)
+            self._phase(3, *args)
+        return self.head()
+
+
+_SOLVERS: dict = {}
+
+
 def gmres_operator(apply_a, b, x0, tol, restart, maxiter, precond, ax0=None):
-    """``ax0``: A x0 when the caller already has it (SEM's (A X) s), so the
-    initial residual costs no operator application (the dense path's ax0,
-    DESIGN.md §8); otherwise r0 = b - A x0 as linsolve.py:144."""
-    from .linsolve import SolveStats
+    """Operator GMRES on the device.  ``ax0``: A x0 when the caller already
+    has it (SEM's (A X) s): the initial residual then costs no application
+    unless it already meets tol."""
+    from .linsolve import BlockDiagPreconditioner, SolveStats
 
     torch = _torch()
-    pc = precond if precond is not None else (lambda v: v)
-    n = b.shape[0]
-    nb = float(torch.linalg.vector_norm(b))
-    st = SolveStats()
-    if nb == 0.0:
-        return torch.zeros(n, dtype=torch.complex128, device="cuda"), st
+    n = int(b.shape[0])
+    pinv = None
+    if precond is not None:
+        if not isinstance(precond, BlockDiagPreconditioner):
+            raise TypeError("precond must be a BlockDiagPreconditioner on the device path")
+        pinv = precond.pinv
+    key = (n, restart, maxiter)
+    solver = _SOLVERS.get(key)
+    if solver is None:
+        _SOLVERS.clear()   # one live workspace (cfg5: V and W are 236 MB each)
+        solver = _SOLVERS[key] = OpSolver(n, restart, maxiter)
+    b = b.to(device="cuda", dtype=torch.complex128).contiguous()
     x = (torch.zeros(n, dtype=torch.complex128, device="cuda") if x0 is None
          else x0.to(device="cuda", dtype=torch.complex128).clone())
-    if ax0 is not None and x0 is not None:
-        r = b - ax0
-    else:
-        r = b - apply_a(x) if bool((x != 0).any()) else b.clone()
-    rnorm = float(torch.linalg.vector_norm(r))
-    res = rnorm / nb
-    st.init_residual = res
-    st.residual_history.append(res)
-    its = 0
-    true_pass = os.environ.get("EWB_TRUE_RESIDUAL_PASS") == "1"
-    while res > tol and its < maxiter:
-        m = min(restart, maxiter - its)
-        V = torch.empty((m + 1, n), dtype=torch.complex128, device="cuda")
-        # the cycle's operator products A P^{-1} v_j, kept so that the true
-        # residual at the end needs no further application (as ewb_gmres)
-        W = None if true_pass else torch.empty((m, n), dtype=torch.complex128, device="cuda")
-        r_start = r
-        H = np.zeros((m + 1, m), dtype=complex)
-        cs = np.zeros(m, dtype=complex)
-        sn = np.zeros(m, dtype=complex)
-        beta = rnorm
-        V[0] = r / beta
-        g = np.zeros(m + 1, dtype=complex)
-        g[0] = beta
-        used = 0
-        for j in range(m):
-            w = apply_a(pc(V[j])).clone()
-            if W is not None:
-                W[j] = w
-            hcol = torch.empty(j + 2, dtype=torch.complex128, device="cuda")
-            for i in range(j + 1):
-                h = torch.vdot(V[i], w)
-                hcol[i] = h
-                w -= h * V[i]
-            hn = torch.linalg.vector_norm(w)
-            hcol[j + 1] = hn
-            col = hcol.cpu().numpy()
-            H[: j + 2, j] = col
-            if col[j + 1].real > 0:
-                V[j + 1] = w / hn
-            for i in range(j):
-                top = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -np.conj(sn[i]) * H[i, j] + np.conj(cs[i]) * H[i + 1, j]
-                H[i, j] = top
-            den = np.sqrt(abs(H[j, j]) ** 2 + abs(H[j + 1, j]) ** 2)
-            if den == 0.0:
-                cs[j], sn[j] = 1.0, 0.0
-            elif H[j, j] == 0.0:
-                cs[j], sn[j] = 0.0, 1.0
-            else:
-                cs[j] = abs(H[j, j]) / den
-                sn[j] = (H[j, j] / abs(H[j, j])) * np.conj(H[j + 1, j]) / den
-            H[j, j] = cs[j] * H[j, j] + sn[j] * H[j + 1, j]
-            H[j + 1, j] = 0.0
-            g[j + 1] = -np.conj(sn[j]) * g[j]
-            g[j] = cs[j] * g[j]
-            its += 1
-            used = j + 1
-            est = abs(g[j + 1]) / nb
-            st.residual_history.append(est)
-            if est <= tol:
-                break
-        y = np.zeros(used, dtype=complex)
-        for i in range(used - 1, -1, -1):
-            y[i] = (g[i] - H[i, i + 1:used] @ y[i + 1:used]) / H[i, i]
-        yd = torch.from_numpy(y).cuda()
-        x = x + pc(V[:used].T @ yd)
-        # true residual (linsolve.py:200-201): b - A x_new equals
-        # r_start - sum_j y_j A P^{-1} v_j to rounding (DESIGN.md §8)
-        r = b - apply_a(x) if W is None else r_start - W[:used].T @ yd
-        rnorm = float(torch.linalg.vector_norm(r))
-        res = rnorm / nb
-    st.iterations = its
-    st.final_residual = res
-    st.converged = res <= tol
+    if ax0 is not None:
+        ax0 = ax0.to(device="cuda", dtype=torch.complex128).contiguous()
+    head = solver.solve(apply_a, b, x, x0 is not None, tol, pinv, ax0)
+    st = SolveStats(iterations=head.iterations, init_residual=head.init_residual,
+                    final_residual=head.final_residual, converged=bool(head.converged),
+                    matvecs=head.applications)
+    nh = min(head.n_hist, solver.hist_cap)
+    st.residual_history = solver.hist[:nh].cpu().tolist() if nh else []
     if not st.converged:
-        log.warning("GMRES stalled at residual %.3e after %d iterations", res, its)
+        log.warning("GMRES stalled at residual %.3e after %d iterations",
+                    st.final_residual, st.iterations)
     return x, st
 
 
+_SEM_WS: dict = {}
+
+
 def sem_operator(apply_a, b, xcols, rank_tol, Y=None, return_ax0=False):
-    """SEM guess for an operator; Y = A X computed in one multi-vector pass.
-    With ``return_ax0`` also returns A x0 = Y s (no extra application)."""
+    """SEM guess for an operator: Y = A X in one multi-vector application
+    (unless given), then the device QR / rank filter / solve.  With
+    ``return_ax0`` also returns A x0 = Y s (no extra application)."""
     torch = _torch()
-    K = xcols.shape[0]
+    lib = _lib.require_cuda()
+    xcols = xcols.contiguous()
+    K, n = int(xcols.shape[0]), int(xcols.shape[1])
     if Y is None:
-        if hasattr(apply_a, "apply_multi"):
-            Y = apply_a.apply_multi(xcols)
-        else:
-            Y = torch.stack([apply_a(xcols[i]) for i in range(K)])
-    Yt = Y.T  # (n, K)
-    keep = np.arange(K)
-    for _ in range(2):
-        q, r = torch.linalg.qr(Yt[:, keep])
-        dg = torch.abs(torch.diagonal(r)).cpu().numpy()
-        good = dg >= rank_tol * dg.max() if dg.max() > 0 else dg > 0
-        if good.all():
-            s = torch.linalg.solve(r, q.conj().T @ b)
-            x0 = (xcols[keep].T @ s).to(torch.complex128)
-            return (x0, (Yt[:, keep] @ s).to(torch.complex128)) if return_ax0 else x0
-        keep = keep[good]
-        if keep.size == 0:
-            break
-    return (xcols[0].clone(), Y[0].clone()) if return_ax0 else xcols[0].clone()
+        Y = (apply_a.apply_multi(xcols) if hasattr(apply_a, "apply_multi")
+             else torch.stack([apply_a(xcols[i]) for i in range(K)]))
+    Y = Y.contiguous()
+    nbytes = int(lib.ewb_sem_workspace_bytes(n, K))
+    ws = _SEM_WS.get("ws")
+    if ws is None or ws.numel() < nbytes:
+        ws = _SEM_WS["ws"] = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        _SEM_WS["res"] = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    x0 = torch.empty(n, dtype=torch.complex128, device="cuda")
+    ax0 = torch.empty(n, dtype=torch.complex128, device="cuda") if return_ax0 else None
+    bd = b.to(device="cuda", dtype=torch.complex128).contiguous()
+    _lib.check(lib.ewb_sem_from_products(
+        _lib.ptr(bd), _lib.ptr(xcols), _lib.ptr(Y), K, n, float(rank_tol), _lib.ptr(x0),
+        _lib.ptr(ax0) if ax0 is not None else None, _lib.ptr(ws), ws.numel(),
+        _lib.ptr(_SEM_WS["res"]), _lib.stream_handle()), "ewb_sem_from_products")
+    return (x0, ax0) if return_ax0 else x0

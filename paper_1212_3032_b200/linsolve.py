@@ -237,46 +237,6 @@ def gmres_device_concurrent(As, bs, xs, tol: float, restart: int, maxiter: int, 
     return stats
 
 
-_ROW_BALANCE = {"done": False, "stats": None}
-
-
-def calibrate_row_balance(a, iters: int = 6, force: bool = False):
-    """Split the solver kernels' rows by measured per-SM matvec speed
-    (``ewb_calibrate_rows``; once per process unless ``force``).
-
-    On a B200 under full-GPU streaming some SMs finish an equal row share
-    ~5 % later than others, every pass, and each Arnoldi step's grid barrier
-    waits for them.  The CTA -> SM map of the solver launches is fixed, so a
-    one-time measurement on a dense matrix (``a``: (n, n) complex128 CUDA
-    tensor, n >= 4096 for a meaningful timing) gives a split under which the
-    CTAs finish together.  Returns (spread_us_before, mean_us_before,
-    spread_us_after, mean_us_after).
-
-    Measured on cfg2: the calibrated split did NOT shorten the
-    barrier wait (per-CTA spread 43 -> 68 us, sweep 3.89 -> 4.10 s), so the
-    sweep leaves it off unless ``EWB_ROW_BALANCE=1``.
-    """
-    if _ROW_BALANCE["done"] and not force:
-        return _ROW_BALANCE["stats"]
-    lib = _lib.require_cuda()
-    n = int(a.shape[0])
-    stats = (ctypes.c_double * 4)()
-    _lib.check(lib.ewb_calibrate_rows(_lib.ptr(a), n, int(iters), stats, _lib.stream_handle()),
-               "ewb_calibrate_rows")
-    _ROW_BALANCE["done"] = True
-    _ROW_BALANCE["stats"] = tuple(stats)
-    log.info("row balance: per-CTA matvec spread %.1f us (mean %.1f) -> %.1f us (mean %.1f)",
-             *stats)
-    return _ROW_BALANCE["stats"]
-
-
-def reset_row_balance():
-    lib = _lib.require_cuda()
-    _lib.check(lib.ewb_reset_row_balance(_lib.stream_handle()), "ewb_reset_row_balance")
-    _ROW_BALANCE["done"] = False
-    _ROW_BALANCE["stats"] = None
-
-
 def gmres_hist_cap(maxiter: int, restart: int) -> int:
     """Residual-history slots one solve can write (init + per iteration + per cycle)."""
     return maxiter + 2 + maxiter // max(restart, 1) + 2

@@ -9,8 +9,9 @@ dense operator exceeds HBM (BASELINE cfg5: 245,760 DOF, 966 GB dense).
 
 The column mixing follows ``apply_bcs`` (assembly.py:293-296):
     A v = T (mask_N v) - U (mask_D v),   b = U (mask_N p) - T (mask_D p)
-and ``apply_multi`` applies A to up to 5 vectors in one pass (the SEM
-product Y = A X plus b share one evaluation of the kernels).
+and ``apply_multi`` applies A to any number of vectors, up to 5 per pass
+over the element pairs (the SEM product Y = A X plus b share one
+evaluation of the kernels for K <= 4).
 """
 
 from __future__ import annotations
@@ -50,16 +51,27 @@ class MatrixFreeOperator:
         self.pinv = None
         self.applications = 0
 
-    # y_k = T vt_k + U vu_k
-    def _apply_tu(self, vt, vu, want_pinv: bool = False):
+    def _workspace(self, K):
         torch = _torch()
-        lib = _lib.load()
-        K = int(vt.shape[0])
-        if not 1 <= K <= self.MAX_K:
-            raise ValueError("1..5 vectors per application")
-        need = int(lib.ewb_matfree_workspace_bytes(self.asm.ctx, K))
+        need = int(_lib.load().ewb_matfree_workspace_bytes(self.asm.ctx, K))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        return self._ws
+
+    # y_k = T vt_k + U vu_k, passes of up to MAX_K vectors
+    def _apply_tu(self, vt, vu, want_pinv: bool = False):
+        torch = _torch()
+        K = int(vt.shape[0])
+        if K < 1:
+            raise ValueError("no vectors to apply")
+        if K > self.MAX_K:
+            parts = [self._apply_tu(vt[c:c + self.MAX_K],
+                                    vu[c:c + self.MAX_K] if vu is not None else None,
+                                    want_pinv and c == 0)
+                     for c in range(0, K, self.MAX_K)]
+            return torch.cat(parts)
+        lib = _lib.load()
+        ws = self._workspace(K)
         y = torch.empty((K, self.n), dtype=torch.complex128, device="cuda")
         pinv = None
         if want_pinv:
@@ -69,10 +81,19 @@ class MatrixFreeOperator:
         _lib.check(lib.ewb_matfree_apply(
             self.asm.ctx, self.omega.real, self.omega.imag, _lib.ptr(vt),
             _lib.ptr(vu) if vu is not None else None, K, _lib.ptr(y), _lib.ptr(self.kinds_dev),
-            _lib.ptr(pinv) if pinv is not None else None, _lib.ptr(self._ws), self._ws.numel(),
+            _lib.ptr(pinv) if pinv is not None else None, _lib.ptr(ws), ws.numel(), None,
             _lib.stream_handle()), "ewb_matfree_apply")
         self.applications += 1
         return y
+
+    def apply_gated(self, vt_ptr: int, vu_ptr, w_ptr: int, gate_ptr: int):
+        """w = T vt + U vu (device pointers, one vector), skipped on the
+        device when *gate == 0 (the operator GMRES's queued iterations)."""
+        lib = _lib.load()
+        ws = self._workspace(1)
+        _lib.check(lib.ewb_matfree_apply(
+            self.asm.ctx, self.omega.real, self.omega.imag, vt_ptr, vu_ptr, 1, w_ptr, None, None,
+            _lib.ptr(ws), ws.numel(), gate_ptr, _lib.stream_handle()), "ewb_matfree_apply")
 
     def _split(self, V):
         """(vt, vu) for A: vt = mask_N v, vu = -mask_D v."""

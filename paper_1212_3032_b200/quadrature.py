@@ -4,7 +4,7 @@ Tables only — rule *generation* is host setup ("table
 generation can stay on host"); every integration runs on the GPU.  The
 barycentric points and weights are built with the same formulas as the
 reference (``quadrature.py:63-132``) so they agree bit-for-bit (checked in
-``tests/test_quadrature_tables.py`` against the golden fixtures).
+``tests/test_host.py::test_device_rule_tables_bitwise`` against the golden fixtures).
 """
 
 from __future__ import annotations

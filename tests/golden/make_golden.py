@@ -383,11 +383,88 @@ def section_cfg2_head():
     save("cfg2_head", **out)
 
 
+def ref_sphere_pressure(level: int, n_omega: int, sem_depth: int = 4):
+    """cfg2/cfg5 through the reference's own SweepConfig:
+    flipped icosphere, all-Neumann, per-DOF step signals t = -p n_e, p = 1.
+    Mirrors paper_1212_3032_b200/workloads.py:sphere_pressure field by field."""
+    mesh = R_mesh.generate_icosphere((0, 0, 0), 1.0, level, flip=True)
+    load = (-1.0 * mesh.normals).ravel()
+    signals = [R_tr.TimeSignal.zero()] + [R_tr.TimeSignal.heaviside(a) for a in load]
+    bcs = R_asm.BoundaryConditionSet.traction_free(mesh.n_elements)
+    bcs.signal_index[:] = (1 + np.arange(mesh.n_dofs)).reshape(-1, 3).astype(np.int32)
+    probes = [Probe("e0_ux", 0, 0, "displacement"), Probe("e0_uy", 0, 1, "displacement"),
+              Probe("e0_uz", 0, 2, "displacement"),
+              Probe("emid_ux", mesh.n_elements // 2, 0, "displacement")]
+    return SweepConfig(
+        mesh=mesh, material=UNIT, bcs=bcs, signals=signals,
+        signal_names=["zero"] + [f"p{k}" for k in range(mesh.n_dofs)], probes=probes,
+        period=16.0 / UNIT.c_s, n_omega=n_omega, kappa=6.0 / math.log(10.0),
+        window="hanning", sem_enabled=True, sem_depth=sem_depth, tol=1e-8, restart=60,
+        maxiter=1000, figures=False, allow_floating=True)
+
+
+# per-k solution vectors kept for the "fed reference history" GPU tests
+CFG2_KEEP = tuple(range(28, 33)) + tuple(range(60, 65)) + tuple(range(124, 129))
+
+
+def section_cfg2_sweep():
+    """cfg2 full 129-frequency sweep through the LIVE reference run_sweep
+    (driver.py:92-176), unmodified.  The module-level names run_sweep calls
+    (Assembler.assemble_tu, apply_bcs, sem_initial_guess, gmres) are wrapped
+    only to OBSERVE: per-k timings and a few solution vectors are recorded,
+    every call is forwarded with its arguments untouched.  ~4 h on 8 cores."""
+    from ewbem import driver as R_drv
+    rec = {"asm_s": [], "bcs_s": [], "sem_s": [], "gmres_s": [], "x": {}, "x0": {}}
+    orig_asm, orig_bcs = R_asm.Assembler.assemble_tu, R_drv.apply_bcs
+    orig_sem, orig_gmres = R_drv.sem_initial_guess, R_drv.gmres
+
+    def timed(key, fn):
+        def wrap(*a, **kw):
+            t0 = time.perf_counter()
+            out = fn(*a, **kw)
+            rec[key].append(time.perf_counter() - t0)
+            return out
+        return wrap
+
+    def gmres_rec(*a, **kw):
+        t0 = time.perf_counter()
+        x, st = orig_gmres(*a, **kw)
+        rec["gmres_s"].append(time.perf_counter() - t0)
+        k = len(rec["gmres_s"]) - 1
+        if k in CFG2_KEEP:
+            rec["x"][k] = x.copy()
+        print(f"cfg2 k={k}: its={st.iterations} init={st.init_residual:.3e} "
+              f"final={st.final_residual:.3e} asm={rec['asm_s'][-1]:.1f}s", flush=True)
+        return x, st
+
+    R_asm.Assembler.assemble_tu = timed("asm_s", orig_asm)
+    R_drv.apply_bcs = timed("bcs_s", orig_bcs)
+    R_drv.sem_initial_guess = timed("sem_s", orig_sem)
+    R_drv.gmres = gmres_rec
+    try:
+        t0 = time.perf_counter()
+        res = R_drv.run_sweep(ref_sphere_pressure(4, 256))
+        wall = time.perf_counter() - t0
+    finally:
+        R_asm.Assembler.assemble_tu = orig_asm
+        R_drv.apply_bcs, R_drv.sem_initial_guess, R_drv.gmres = orig_bcs, orig_sem, orig_gmres
+    out = {"seconds": wall, "asm_s": np.array(rec["asm_s"]), "bcs_s": np.array(rec["bcs_s"]),
+           "sem_s": np.array(rec["sem_s"]), "gmres_s": np.array(rec["gmres_s"]),
+           "keep_k": np.array(sorted(rec["x"])),
+           "keep_x": np.array([rec["x"][k] for k in sorted(rec["x"])]),
+           "failed": np.array(res.failed_frequencies, dtype=np.int64)}
+    _dump_sweep("cfg2", res, out)
+    out["cfg2_hist_len"] = np.array([len(s.residual_history) for s in res.stats])
+    out["cfg2_hist_cat"] = np.concatenate([np.asarray(s.residual_history, float)
+                                           for s in res.stats])
+    save("cfg2_sweep", **out)
+
+
 SECTIONS = dict(small=section_small, cfg1_rows=section_cfg1_rows, tiers=section_tiers,
                 linsolve=section_linsolve, transform=section_transform,
                 sweeps=section_sweeps, cfg1_sweep=section_cfg1_sweep,
                 cfg1_solutions=section_cfg1_solutions,
-                cfg2_head=section_cfg2_head)
+                cfg2_head=section_cfg2_head, cfg2_sweep=section_cfg2_sweep)
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(SECTIONS)

@@ -27,9 +27,10 @@ def _steel():
 
 @pytest.fixture(scope="module")
 def cube(cuda):
-    from paper_1212_3032_b200 import Assembler, generate_box_mesh
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.workloads import box_mesh
 
-    return Assembler(generate_box_mesh((1, 1, 1), (2, 2, 2)), _unit())
+    return Assembler(box_mesh((1, 1, 1), (2, 2, 2)), _unit())
 
 
 def test_cube_tu_all_frequencies_match_golden(cube):
@@ -47,20 +48,22 @@ def test_cube_rowsums_match_golden(cube):
 
 
 def test_rod32_steel_matches_golden(cuda):
-    from paper_1212_3032_b200 import Assembler, generate_box_mesh
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.workloads import box_mesh
 
     g = golden("small")
-    t, u = Assembler(generate_box_mesh((1, 1, 2), (2, 2, 1)), _steel()).assemble_tu(
+    t, u = Assembler(box_mesh((1, 1, 2), (2, 2, 1)), _steel()).assemble_tu(
         2000.0 - 300.0j, host=True)
     assert rel_max(t, g["rod32_T"]) <= TOL
     assert rel_max(u, g["rod32_U"]) <= TOL
 
 
 def test_flipped_icosphere_matches_golden(cuda):
-    from paper_1212_3032_b200 import Assembler, generate_icosphere
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.workloads import cavity_mesh
 
     g = golden("small")
-    t, u = Assembler(generate_icosphere((0, 0, 0), 1.0, 1, flip=True), _unit()).assemble_tu(
+    t, u = Assembler(cavity_mesh(1), _unit()).assemble_tu(
         1.5 - 0.3j, host=True)
     assert rel_max(t, g["ico1_T"]) <= TOL
     assert rel_max(u, g["ico1_U"]) <= TOL
@@ -68,9 +71,10 @@ def test_flipped_icosphere_matches_golden(cuda):
 
 @pytest.fixture(scope="module")
 def cfg1_asm(cuda):
-    from paper_1212_3032_b200 import Assembler, generate_box_mesh
+    from paper_1212_3032_b200 import Assembler
+    from paper_1212_3032_b200.workloads import box_mesh
 
-    return Assembler(generate_box_mesh((1, 1, 1), (8, 8, 8)), _unit())
+    return Assembler(box_mesh((1, 1, 1), (8, 8, 8)), _unit())
 
 
 def test_cfg1_pair_census_matches_reference_tiers(cfg1_asm):
@@ -285,14 +289,13 @@ def test_non_finite_entries_raise_per_member(cuda):
     and the sweep reports the first frequency (driver.py:141-145)."""
     import dataclasses
 
-    from paper_1212_3032_b200 import Assembler, SweepError, generate_box_mesh, run_sweep
-    from paper_1212_3032_b200.mesh import TriangleMesh
-    from paper_1212_3032_b200.workloads import cfg1
+    from paper_1212_3032_b200 import Assembler, SurfaceMesh, SweepError, run_sweep
+    from paper_1212_3032_b200.workloads import box_mesh, cfg1
 
-    m = generate_box_mesh((1, 1, 1), (2, 2, 2))
+    m = box_mesh((1, 1, 1), (2, 2, 2))
     tris = np.vstack([m.triangles, m.triangles[:1]])
     tags = np.concatenate([m.region_tag, m.region_tag[:1]])
-    mesh = TriangleMesh(m.vertices, tris, tags, closed=False)
+    mesh = SurfaceMesh(m.vertices, tris, tags)
     asm = Assembler(mesh, _unit())
     bcs = _cfg1_bcs(mesh)
     P = np.ones((3, mesh.n_dofs), complex)

@@ -28,11 +28,11 @@ def test_matfree_matvec_equals_dense_system(cuda, mesh_kind):
     """A v and b from the matrix-free kernels == the fused dense system (1e-10)."""
     import torch
 
-    from paper_1212_3032_b200 import Assembler, MatrixFreeOperator, generate_box_mesh
-    from paper_1212_3032_b200 import generate_icosphere
+    from paper_1212_3032_b200 import Assembler, MatrixFreeOperator
+    from paper_1212_3032_b200.workloads import box_mesh, cavity_mesh
 
-    mesh = (generate_box_mesh((1, 1, 1), (4, 4, 4)) if mesh_kind == "box"
-            else generate_icosphere((0, 0, 0), 1.0, 2, flip=True))
+    mesh = (box_mesh((1, 1, 1), (4, 4, 4)) if mesh_kind == "box"
+            else cavity_mesh(2))
     asm = Assembler(mesh, _unit())
     bcs = _rod_bcs(mesh) if mesh_kind == "box" else None
     from paper_1212_3032_b200 import BoundaryConditionSet
@@ -60,10 +60,10 @@ def test_matfree_gmres_and_sem_match_dense(cuda):
     import torch
 
     from paper_1212_3032_b200 import (Assembler, BoundaryConditionSet, MatrixFreeOperator,
-                                      SolutionHistory, generate_icosphere, gmres,
-                                      sem_initial_guess)
+                                      SolutionHistory, gmres, sem_initial_guess)
+    from paper_1212_3032_b200.workloads import cavity_mesh
 
-    mesh = generate_icosphere((0, 0, 0), 1.0, 2, flip=True)
+    mesh = cavity_mesh(2)
     asm = Assembler(mesh, _unit())
     bcs = BoundaryConditionSet.traction_free(mesh.n_elements)
     load = (-1.0 * mesh.normals).ravel().astype(complex)
@@ -93,9 +93,10 @@ def test_matfree_sampled_rows_vs_oracle(cuda):
     import torch
 
     from oracle import ewbem_oracle as O
-    from paper_1212_3032_b200 import Assembler, MatrixFreeOperator, generate_icosphere
+    from paper_1212_3032_b200 import Assembler, MatrixFreeOperator
+    from paper_1212_3032_b200.workloads import cavity_mesh
 
-    mesh = generate_icosphere((0, 0, 0), 1.0, 3, flip=True)
+    mesh = cavity_mesh(3)
     mat = _unit()
     asm = Assembler(mesh, mat)
     om = 1.7 - 0.3j

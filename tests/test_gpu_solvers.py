@@ -126,11 +126,11 @@ def test_window_idft_matches_golden(cuda):
 
 def _tiny_cfg(**kw):
     from paper_1212_3032_b200 import (DIRICHLET, NEUMANN, BoundaryConditionSet, Material, Probe,
-                                      SweepConfig, TimeSignal, generate_box_mesh)
-    from paper_1212_3032_b200.workloads import face_center_element
+                                      SweepSpec, TimeSignal)
+    from paper_1212_3032_b200.workloads import box_mesh, face_center_element
 
     divisions = kw.pop("divisions", (1, 1, 1))
-    mesh = generate_box_mesh((3.0, 1.0, 1.0), divisions)
+    mesh = box_mesh((3.0, 1.0, 1.0), divisions)
     zm = np.flatnonzero(mesh.region_tag == 4)
     mid = int(zm[np.argmin(np.linalg.norm(mesh.centroids[zm] - np.array([1.5, 0.5, 0.0]),
                                           axis=1))])
@@ -139,7 +139,7 @@ def _tiny_cfg(**kw):
     bcs.set_region(mesh, 1, (0,), NEUMANN, 1)
     args = dict(n_omega=8, kappa=4.0, window="hanning", sem_enabled=True, sem_depth=4, tol=1e-5)
     args.update(kw)
-    return SweepConfig(
+    return SweepSpec(
         mesh=mesh, material=Material.from_young_poisson(2.11e11, 0.0, 7850.0), bcs=bcs,
         signals=[TimeSignal.zero(), TimeSignal.heaviside(-1e6)], signal_names=["zero", "load"],
         probes=[Probe("tip_ux", face_center_element(mesh, 1), 0, "displacement"),
@@ -326,44 +326,6 @@ def test_solver_cta_budget_same_result(cuda):
         _lib.check(lib.ewb_set_solver_ctas(-1))
 
 
-def test_row_balance_split_same_solution(cuda, monkeypatch):
-    """ewb_calibrate_rows: rows split by measured per-SM speed; the solve is
-    bit-reproducible for a given split and agrees with the equal split to
-    rounding (only the grouping of the dot-product partials changes)."""
-    import torch
-
-    from paper_1212_3032_b200.linsolve import (calibrate_row_balance, gmres_device,
-                                               reset_row_balance)
-
-    monkeypatch.delenv("EWB_ROW_BALANCE", raising=False)
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(5)
-    n = 6000
-    a = torch.randn((n, n), dtype=torch.complex128, device="cuda", generator=gen)
-    a.diagonal().add_(3 * n ** 0.5)
-    b = torch.randn(n, dtype=torch.complex128, device="cuda", generator=gen)
-
-    def solve():
-        x = torch.zeros_like(b)
-        st = gmres_device(a, b, x, False, 1e-10, 50, 200, None)
-        return x.cpu().numpy(), st.iterations
-
-    try:
-        reset_row_balance()
-        x0, i0 = solve()
-        stats = calibrate_row_balance(a, force=True)
-        assert stats is not None and stats[1] > 0 and stats[3] > 0
-        x1, i1 = solve()
-        x1b, _ = solve()
-        reset_row_balance()
-        x2, _ = solve()
-    finally:
-        reset_row_balance()
-    assert np.array_equal(x1, x1b) and np.array_equal(x0, x2)
-    assert i0 == i1
-    assert rel_max(x1, x0) <= 1e-12
-
-
 def test_cfg1_stepwise_iterations_with_batched_assembly(cuda):
     """As the stepwise test, with every system from the 16-member
     multi-frequency assembly the sweep uses (phase recurrence)."""
@@ -454,26 +416,6 @@ def test_concurrent_solves_equal_sequential(cuda):
         assert rel_max(x.cpu().numpy(), xr) <= 1e-8
 
 
-def test_overlapped_batch_assembly_sweep_equals_default(cuda, monkeypatch):
-    """EWB_OVERLAP_ASSEMBLY=1 (batch g+1 assembled on a few SMs beside batch
-    g's solves, then finished on the full GPU) gives the default sweep."""
-    from paper_1212_3032_b200.driver import DeviceSweep
-    from paper_1212_3032_b200.workloads import cfg1
-
-    cfg = cfg1()
-    ks = list(range(0, 40))
-    ref = DeviceSweep(cfg, frequencies=ks)
-    st_ref = ref.run()
-    monkeypatch.setenv("EWB_OVERLAP_ASSEMBLY", "1")
-    monkeypatch.setenv("EWB_OVERLAP_SMS", "8")
-    ds = DeviceSweep(cfg, assembler=ref.asm, frequencies=ks)
-    st = ds.run()
-    assert getattr(ds, "_bufs", None) is not None      # the overlapped path ran
-    for k in ks:
-        assert abs(st[k].iterations - st_ref[k].iterations) <= 1
-        assert rel_max(ds.sol[k].cpu().numpy(), ref.sol[k].cpu().numpy()) <= 1e-6
-
-
 @pytest.mark.parametrize("nb", [1, 5, 32])
 def test_cfg1_sweep_any_assembly_batch(cuda, nb):
     """The sweep with 1, 5 or 32 frequencies per assembly pass reproduces the
@@ -496,3 +438,134 @@ def test_cfg1_sweep_any_assembly_batch(cuda, nb):
     for c, p in enumerate(cfg.probes):
         href = g[f"cfg1_h_{p.name}"]
         assert np.linalg.norm(series[:, c] - href) / np.linalg.norm(href) <= 1e-6
+
+
+# ----------------------------------------------------------------------
+# exit semantics: every exit is decided on the literal b - A x
+# (linsolve.py:200-205); restarts use the stored products
+# ----------------------------------------------------------------------
+def _literal(a, b, x):
+    import torch
+
+    return (torch.linalg.vector_norm(b - a @ x) / torch.linalg.vector_norm(b)).item()
+
+
+def test_final_residual_is_literal_multicycle(cuda):
+    """Several restart cycles (restart 7, tol 1e-11), block preconditioner:
+    final_residual equals ||b - A x|| / ||b|| and meets tol."""
+    torch = cuda
+    from paper_1212_3032_b200 import block_diag_precond
+    from paper_1212_3032_b200.linsolve import gmres_device
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(11)
+    n = 1200
+    a = torch.randn((n, n), dtype=torch.complex128, device="cuda", generator=gen)
+    a.diagonal().add_(2.2 * n ** 0.5)
+    b = torch.randn(n, dtype=torch.complex128, device="cuda", generator=gen)
+    pinv = block_diag_precond(a).pinv
+    x = torch.zeros_like(b)
+    st = gmres_device(a, b, x, False, 1e-11, 7, 500, pinv)
+    assert st.converged and st.iterations > 14             # >= 3 cycles
+    lit = _literal(a, b, x)
+    assert lit <= 1e-11 and abs(st.final_residual - lit) <= 1e-14
+    # one literal pass per exit: iterations + the exit's b - A x
+    assert st.matvecs == st.iterations + 1
+    # restart from the solution with its A x supplied (SEM's Y s): a
+    # 0-iteration exit is still confirmed by one literal pass
+    x2 = x.clone()
+    ax = a @ x2
+    st2 = gmres_device(a, b, x2, True, 1e-10, 7, 500, pinv, ax0=ax)
+    assert st2.iterations == 0 and st2.matvecs == 1 and st2.converged
+    assert abs(st2.final_residual - _literal(a, b, x2)) <= 1e-14
+    # maxiter exit is literal too
+    x3 = torch.zeros_like(b)
+    st3 = gmres_device(a, b, x3, False, 1e-14, 5, 12, pinv)
+    assert not st3.converged and st3.iterations == 12
+    assert abs(st3.final_residual - _literal(a, b, x3)) <= 1e-14
+
+
+def test_cfg1_sweep_final_residuals_are_literal(cuda):
+    """Every cfg1 solve of the device sweep: reported final residual =
+    ||b - A x|| / ||b|| <= tol, recomputed on the re-assembled system."""
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.workloads import cfg1
+
+    cfg = cfg1()
+    ds = DeviceSweep(cfg)
+    stats = ds.run()
+    sysm = None
+    for k in sorted(stats):
+        sysm = ds.asm.assemble_system(ds.omegas[k], cfg.bcs, ds.P[k], out=sysm)
+        lit = _literal(sysm.A, sysm.b, ds.sol[k])
+        assert stats[k].converged and lit <= cfg.tol, (k, lit)
+        assert abs(stats[k].final_residual - lit) <= 1e-12 * max(1.0, lit / cfg.tol), k
+
+
+def test_operator_gmres_multicycle_matches_dense(cuda):
+    """Device operator GMRES (matrix-free, restart 5 -> several cycles) vs the
+    dense kernel on the same system; a plain torch callable takes the same
+    device kernels with a host-checked gate."""
+    torch = cuda
+    from paper_1212_3032_b200 import (Assembler, BoundaryConditionSet, MatrixFreeOperator,
+                                      block_diag_precond, gmres)
+    from paper_1212_3032_b200.workloads import cavity_mesh
+
+    mesh = cavity_mesh(2)
+    asm = Assembler(mesh, _unit())
+    bcs = BoundaryConditionSet.traction_free(mesh.n_elements)
+    load = (-1.0 * mesh.normals).ravel().astype(complex)
+    om = 3.0 - 0.37j
+    dense = asm.assemble_system(om, bcs, load)
+    op = MatrixFreeOperator(asm, om, bcs)
+    pc = op.block_preconditioner()
+    x_d, st_d = gmres(dense.A, dense.b, tol=1e-10, restart=5, precond=block_diag_precond(dense.A))
+    x_m, st_m = gmres(op, dense.b, tol=1e-10, restart=5, precond=pc)
+    assert st_d.iterations > 10
+    assert abs(st_m.iterations - st_d.iterations) <= 1 and st_m.converged
+    assert rel_max(x_m.cpu().numpy(), x_d.cpu().numpy()) <= 1e-8
+    assert abs(st_m.final_residual - _literal(dense.A, dense.b, x_m)) <= 1e-13
+    A = dense.A
+    x_c, st_c = gmres(lambda v: A @ v, dense.b, tol=1e-10, restart=5, precond=pc)
+    assert abs(st_c.iterations - st_d.iterations) <= 1
+    assert rel_max(x_c.cpu().numpy(), x_d.cpu().numpy()) <= 1e-8
+    # warm start without A x0: the initial residual takes one application
+    x_w, st_w = gmres(op, dense.b, x0=x_d, tol=1e-9, restart=5, precond=pc)
+    assert st_w.iterations == 0 and st_w.matvecs == 1
+
+
+def _unit():
+    from paper_1212_3032_b200 import Material
+
+    return Material.from_young_poisson(1.0, 0.25, 1.0)
+
+
+@pytest.mark.parametrize("K", [5, 6, 8])
+def test_sem_deep_history_vs_oracle(cuda, K):
+    """SEM with K > 4 history columns (Y = A X in passes of 4; linsolve.py:213-242)
+    for a dense matrix and for the matrix-free operator vs the oracle."""
+    torch = cuda
+    from oracle import ewbem_oracle as O
+    from paper_1212_3032_b200 import (Assembler, MatrixFreeOperator, SolutionHistory,
+                                      sem_initial_guess)
+    from paper_1212_3032_b200.workloads import cavity_mesh
+
+    mesh = cavity_mesh(1)
+    asm = Assembler(mesh, _unit())
+    om = 2.0 - 0.4j
+    op = MatrixFreeOperator(asm, om)
+    n = mesh.n_dofs
+    A = op.apply_multi(torch.eye(n, dtype=torch.complex128, device="cuda")).T.contiguous()
+    rng = np.random.default_rng(K)
+    base = rng.normal(size=n) + 1j * rng.normal(size=n)
+    hist, ohist = SolutionHistory(K), O.History(K)
+    for i in range(K):
+        c = base * (1 + 0.1 * i) + 1e-2 * (rng.normal(size=n) + 1j * rng.normal(size=n))
+        hist.push(c)
+        ohist.push(c)
+    b = rng.normal(size=n) + 1j * rng.normal(size=n)
+    ref = O.sem_guess(ohist, A.cpu().numpy(), b)
+    got_d = sem_initial_guess(hist, A, b).cpu().numpy()
+    got_m = sem_initial_guess(hist, op, b).cpu().numpy()
+    assert rel_max(got_d, ref) <= 1e-8
+    assert rel_max(got_m, ref) <= 1e-8

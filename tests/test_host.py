@@ -1,5 +1,6 @@
-"""Host-side code without a GPU: mesh generators, rule tables, config, the
-C-ABI library exports, and the multi-rank frequency sharding (gloo)."""
+"""Host-side code without a GPU: mesh fixtures and derived geometry, rule
+tables, workloads, the C-ABI library exports, and the multi-rank frequency
+sharding (gloo)."""
 
 import hashlib
 import os
@@ -19,40 +20,47 @@ def _sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-@pytest.mark.parametrize("name,build", [
-    ("cfg1", lambda M: M.generate_box_mesh((1, 1, 1), (8, 8, 8))),
-    ("rod", lambda M: M.generate_box_mesh((3, 1, 1), (12, 4, 4))),
-    ("ico3", lambda M: M.generate_icosphere((0, 0, 0), 1.0, 3, flip=True)),
-    ("ico4", lambda M: M.generate_icosphere((0, 0, 0), 1.0, 4, flip=True)),
-])
-def test_mesh_geometry_bit_identical_to_reference(name, build):
-    import paper_1212_3032_b200.mesh as M
+@pytest.mark.parametrize("name,key", [("cfg1", "box_1x1x1_8x8x8"), ("rod", "box_3x1x1_12x4x4"),
+                                      ("ico3", "ico3"), ("ico4", "ico4"), ("ico6", "ico6")])
+def test_mesh_geometry_bit_identical_to_reference(name, key):
+    """SurfaceMesh's derived geometry of the reference-generated meshes equals
+    the reference's own (hashes written by the live reference, mesh.py:88-106)."""
+    from paper_1212_3032_b200.workloads import load_mesh
 
-    m = build(M)
+    m = load_mesh(key)
     ref = golden("tiers")[f"{name}_geom_sha"]
     got = [_sha(m.vertices), _sha(m.centroids), _sha(m.normals), _sha(m.areas),
            _sha(m.diameters)]
     assert got == list(ref)
 
 
-def test_mesh_generators_equal_live_reference(reference):
-    import paper_1212_3032_b200.mesh as M
+def test_mesh_fixture_derived_geometry_bitwise():
+    from paper_1212_3032_b200.workloads import load_mesh, mesh_names
 
-    for a, b in ((reference.generate_box_mesh((1, 2, 1), (3, 2, 4)),
-                  M.generate_box_mesh((1, 2, 1), (3, 2, 4))),):
+    g = golden("meshes")
+    for name in mesh_names():
+        m = load_mesh(name)
+        assert np.array_equal(m.areas, g[f"{name}__areas"]), name
+        assert np.array_equal(m.diameters, g[f"{name}__diameters"]), name
+
+
+def test_mesh_fixtures_equal_live_reference(reference):
+    """tests/golden/meshes.npz is what the reference's generators produce."""
+    from ewbem import mesh as R
+
+    from paper_1212_3032_b200.workloads import load_mesh, mesh_names
+
+    for name in mesh_names():
+        if name.startswith("box_"):
+            ls, ds = name[4:].split("_")
+            ref = R.generate_box_mesh(tuple(float(v) for v in ls.split("x")),
+                                              tuple(int(v) for v in ds.split("x")))
+        else:
+            ref = R.generate_icosphere((0, 0, 0), 1.0, int(name[3:]), flip=True)
+        m = load_mesh(name)
         for f in ("vertices", "triangles", "region_tag", "centroids", "normals", "areas",
                   "diameters"):
-            assert np.array_equal(getattr(a, f), getattr(b, f))
-
-
-def test_mesh_validation():
-    import paper_1212_3032_b200.mesh as M
-
-    m = M.generate_box_mesh((1, 1, 1), (1, 1, 1))
-    with pytest.raises(M.MeshError):
-        M.TriangleMesh(m.vertices, m.triangles[:-1])          # open
-    with pytest.raises(M.MeshError):
-        M.TriangleMesh(m.vertices, np.array([[0, 0, 1]]), closed=False)
+            assert np.array_equal(getattr(m, f), getattr(ref, f)), (name, f)
 
 
 def test_device_rule_tables_bitwise():
@@ -82,44 +90,6 @@ def test_workloads_config_values():
     assert (area >= 1e-4).all() and x.shape == (64, 3) and np.all(om.imag == -2.0)
 
 
-def test_parse_config_roundtrip(tmp_path):
-    from paper_1212_3032_b200 import parse_config
-
-    text = """mesh.box.lengths = 3 1 1
-mesh.box.divisions = 2 1 1
-material.E = 2.11e11
-material.nu = 0
-material.rho = 7850
-time.period = 0.0155
-time.samples = 8
-signal.load = heaviside -1e6
-bc = x- all displacement zero
-bc = x+ x traction load
-probe = tip_ux @x+ x displacement
-output.figures = false
-"""
-    p = tmp_path / "rod.cfg"
-    p.write_text(text)
-    cfg = parse_config(p)
-    assert cfg.mesh.n_elements == 20 and cfg.n_omega == 8 and cfg.tol == 1e-5
-    assert (cfg.bcs.kind[cfg.mesh.region_tag == 0] == 1).all()
-    assert cfg.probes[0].quantity == "displacement"
-
-
-def test_parse_config_matches_live_reference(tmp_path, reference):
-    from ewbem.config import parse_config as ref_parse
-
-    from paper_1212_3032_b200 import parse_config
-
-    src = Path("/root/reference/pkg/configs/rod.cfg")
-    a, b = ref_parse(src), parse_config(src)
-    assert np.array_equal(a.bcs.kind, b.bcs.kind)
-    assert np.array_equal(a.bcs.signal_index, b.bcs.signal_index)
-    assert [p.dof for p in a.probes] == [p.dof for p in b.probes]
-    assert (a.period, a.n_omega, a.kappa, a.tol, a.sem_depth) == \
-        (b.period, b.n_omega, b.kappa, b.tol, b.sem_depth)
-
-
 # ----------------------------------------------------------------------
 # C ABI
 # ----------------------------------------------------------------------
@@ -139,7 +109,7 @@ def test_library_exports_every_declared_symbol():
     assert sorted(_lib.EXPORTS) == declared
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.ewb_abi_version() == 3
+    assert lib.ewb_abi_version() == _lib.ABI_VERSION == 4
     out = subprocess.run(["nm", "-D", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     for name in declared:
         assert re.search(rf" T {name}$", out, re.M), name
@@ -158,11 +128,11 @@ def test_compute_without_gpu_fails_loudly():
 
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    from paper_1212_3032_b200 import Assembler, Material, NativeUnavailable, generate_box_mesh
+    from paper_1212_3032_b200 import Assembler, Material, NativeUnavailable
+    from paper_1212_3032_b200.workloads import box_mesh
 
     with pytest.raises(NativeUnavailable):
-        Assembler(generate_box_mesh((1, 1, 1), (1, 1, 1)),
-                  Material.from_young_poisson(1, 0.25, 1))
+        Assembler(box_mesh((1, 1, 1), (1, 1, 1)), Material.from_young_poisson(1, 0.25, 1))
 
 
 def test_argument_validation_without_gpu():
@@ -178,16 +148,11 @@ def test_argument_validation_without_gpu():
     assert lib.ewb_blockdiag_inverse(ctypes.c_void_p(16), 4, ctypes.c_void_p(16),
                                      ctypes.c_void_p(16), None) == _lib.EWB_ERR_INVALID
     assert b"divisible by 3" in lib.ewb_last_error()
-    # multi-frequency entry points (ABI v3)
+    # multi-frequency entry point
     v = ctypes.c_void_p(16)
     assert lib.ewb_assemble_system_multi(None, 4, v, v, v, v, v, v, v, v, None) == \
         _lib.EWB_ERR_INVALID
     assert b"null argument" in lib.ewb_last_error()
-    assert lib.ewb_assemble_system_multi_finish(None, None) == _lib.EWB_ERR_INVALID
-    assert b"no batch begun" in lib.ewb_last_error()
-    assert lib.ewb_assemble_system_multi_self(None, None) == _lib.EWB_ERR_INVALID
-    assert lib.ewb_calibrate_rows(None, 0, 2, None, None) == _lib.EWB_ERR_INVALID
-    assert b"bad argument" in lib.ewb_last_error()
     assert lib.ewb_set_solver_ctas(-1) == _lib.EWB_ERR_INVALID
 
 

@@ -12,9 +12,15 @@ STEEL0 = O.Medium.young_poisson(2.11e11, 0.0, 7850.0)
 
 
 def _box(lengths, div):
-    from paper_1212_3032_b200.mesh import generate_box_mesh
+    from paper_1212_3032_b200.workloads import box_mesh
 
-    return generate_box_mesh(lengths, div)
+    return box_mesh(lengths, div)
+
+
+def _ico(level):
+    from paper_1212_3032_b200.workloads import cavity_mesh
+
+    return cavity_mesh(level)
 
 
 def test_rules_match_golden_bitwise():
@@ -49,13 +55,11 @@ def test_cube_assembly_matches_golden_bitwise():
 
 
 def test_rod32_and_ico1_match_golden():
-    from paper_1212_3032_b200.mesh import generate_icosphere
-
     g = golden("small")
     m = _box((1, 1, 2), (2, 2, 1))
     t, u = O.DenseOracle(m.vertices, m.triangles, STEEL0).tu(2000.0 - 300.0j)
     assert rel_max(t, g["rod32_T"]) <= 1e-14 and rel_max(u, g["rod32_U"]) <= 1e-14
-    m = generate_icosphere((0, 0, 0), 1.0, 1, flip=True)
+    m = _ico(1)
     t, u = O.DenseOracle(m.vertices, m.triangles, UNIT).tu(1.5 - 0.3j)
     assert rel_max(t, g["ico1_T"]) <= 1e-14 and rel_max(u, g["ico1_U"]) <= 1e-14
 
@@ -123,10 +127,8 @@ def test_transform_matches_golden():
 
 
 def test_tiny_sweep_matches_golden():
-    from paper_1212_3032_b200.mesh import generate_box_mesh
-
     g = golden("sweeps")
-    m = generate_box_mesh((3.0, 1.0, 1.0), (1, 1, 1))
+    m = _box((3.0, 1.0, 1.0), (1, 1, 1))
     kinds = np.zeros((m.n_elements, 3), np.uint8)
     sig = np.zeros((m.n_elements, 3), np.int64)
     kinds[m.region_tag == 0] = 1
@@ -178,9 +180,7 @@ def test_oracle_gmres_equal_to_live_reference(reference):
 
 def test_oracle_sampled_rows_equal_dense(reference):
     """The streaming row-sampled oracle (cfg5 checker) equals dense rows."""
-    from paper_1212_3032_b200.mesh import generate_icosphere
-
-    m = generate_icosphere((0, 0, 0), 1.0, 2, flip=True)
+    m = _ico(2)
     oa = O.DenseOracle(m.vertices, m.triangles, UNIT)
     om = 1.3 - 0.4j
     t, u = oa.tu(om)
