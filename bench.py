@@ -16,8 +16,9 @@ and the device->host read-back of histories/stats included).
 
 `--impl reference` times the reference algorithm on the host CPU (the numpy
 oracle port under oracle/, since the Python reference cannot travel to the
-GPU box): a seeded column sample of the assembly plus scaled dense-matrix
-timings, extrapolated to one full sweep (see `cpu_sweep_estimate`).
+GPU box), on every host core (oracle/parallel.py): the chained sweep from
+k = 0, one complete frequency per step; the s/sweep value is measured setup
++ n_freq x the mean measured frequency.
 Multi-GPU (torchrun): SEM makes the sweep sequential, so N ranks run N
 replica sweeps (scaling "weak"); time = max over ranks of CUDA-event time.
 """
@@ -53,6 +54,7 @@ def parse_args(argv=None):
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="cfg2", choices=("cfg2", "cfg1", "cfg3", "cfg4", "cfg5"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 matrix-free block")
     return ap.parse_args(argv)
 
 
@@ -118,54 +120,6 @@ def measured_peaks():
 # ----------------------------------------------------------------------
 # CPU side: the reference algorithm (numpy oracle port), bounded sample
 # ----------------------------------------------------------------------
-def _time_dense_parts(n_full: int, n_sample: int, passes_per_freq: float, seed: int):
-    """Scaled timings of apply_bcs, block_diag_precond and the zgemv passes."""
-    from oracle import ewbem_oracle as O
-
-    rng = np.random.default_rng(seed)
-    ns = n_sample - n_sample % 3
-    t = rng.normal(size=(ns, ns)) + 1j * rng.normal(size=(ns, ns))
-    u = rng.normal(size=(ns, ns)) + 1j * rng.normal(size=(ns, ns))
-    kinds = np.zeros(ns, np.uint8)
-    p = rng.normal(size=ns) + 1j * rng.normal(size=ns)
-    t0 = time.perf_counter()
-    a, b = O.apply_bcs(t, u, kinds, p)
-    t1 = time.perf_counter()
-    nb = min(ns // 3, 512)
-    O.block_precond(a[: 3 * nb, : 3 * nb])
-    t2 = time.perf_counter()
-    # zgemv at a bandwidth-representative size (matrix >> LLC), scaled by N^2
-    ng = min(6144, n_full)
-    big = np.ones((ng, ng), dtype=complex)
-    vg = np.ones(ng, dtype=complex)
-    reps = 3
-    big @ vg   # BLAS thread start-up outside the timing
-    t2b = time.perf_counter()
-    for _ in range(reps):
-        big @ vg
-    t3 = time.perf_counter()
-    gemv_s = (t3 - t2b) / reps * (n_full / ng) ** 2
-    del big
-    # assemble_tu's dense bookkeeping: two zeroed (n_e,3,n_e,3) arrays, the
-    # per-column block scatter u_mat[rows,:,j,:] = ... and the finite check
-    # (assembly.py:229-253)
-    ne = ns // 3
-    blk = rng.normal(size=(ne, 3, 3)) + 0j
-    t4 = time.perf_counter()
-    tm = np.zeros((ne, 3, ne, 3), dtype=complex)
-    um = np.zeros((ne, 3, ne, 3), dtype=complex)
-    rows = np.arange(ne)
-    for j in range(ne):
-        tm[rows, :, j, :] = blk
-        um[rows, :, j, :] = blk
-    ok = np.isfinite(tm).all() and np.isfinite(um).all()
-    t5 = time.perf_counter()
-    assert ok
-    scale = (n_full / ns) ** 2
-    return dict(apply_bcs=(t1 - t0) * scale, precond=(t2 - t1) * (n_full / 3) / nb,
-                gemv=gemv_s * passes_per_freq, scatter=(t5 - t4) * scale)
-
-
 def host_info() -> dict:
     """CPU model, core count, numpy BLAS and thread settings of the host the
     CPU baseline ran on (report them beside the number)."""
@@ -192,47 +146,29 @@ def host_info() -> dict:
             "blas": blas, "thread_env": threads}
 
 
-def cpu_sweep_estimate(cfg, n_cols: int, freq_ids, seed: int, passes_per_freq: float):
-    """Extrapolated CPU seconds for one full sweep of ``cfg`` (reference algorithm).
-
-    Sample: ``n_cols`` seeded columns of the assembly (prep + static pass +
-    dynamic assembly at the frequencies ``freq_ids``), scaled by n_e / n_cols;
-    apply_bcs / block preconditioner / zgemv timed on a smaller dense matrix
-    and scaled by (N / n_sample)^2; GMRES = passes_per_freq zgemv passes per
-    frequency (the reference's SEM does K separate matvecs).
-    """
+def oracle_inputs(cfg) -> dict:
+    """The sweep inputs of ``cfg`` as the oracle's plain arrays."""
     from oracle import ewbem_oracle as O
 
     m = cfg.mesh
-    med = O.Medium(cfg.material.lam, cfg.material.mu, cfg.material.rho)
-    eta = O.eta_from_kappa(cfg.kappa, cfg.period)
-    om = O.frequency_grid(cfg.period, cfg.n_omega, eta)
-    rng = np.random.default_rng(seed)
-    cols = np.sort(rng.choice(m.n_elements, size=min(n_cols, m.n_elements), replace=False))
-    t0 = time.perf_counter()
-    dyn = []
-    prep = static = 0.0
-    for i, k in enumerate(freq_ids):
-        s = O.column_sample_seconds(m.vertices, m.triangles, med, cols, om[k])
-        dyn.append(s["dynamic"])
-        if i == 0:
-            prep, static = s["prep"], s["static"]
-    scale = m.n_elements / len(cols)
-    dense = _time_dense_parts(m.n_dofs, 3072, passes_per_freq, seed)
-    nf = len(om)
-    per_freq = statistics.mean(dyn) * scale + dense["scatter"] + dense["apply_bcs"] + \
-        dense["precond"] + dense["gemv"]
-    total = (prep + static) * scale + nf * per_freq
-    wall = time.perf_counter() - t0
-    return dict(value=total, sample=(
-        f"{len(cols)} of {m.n_elements} assembly columns (seed {seed}) at k={list(freq_ids)}, "
-        f"scaled x{scale:.1f}; apply_bcs/precond/zgemv timed at N=3072 and scaled by N^2; "
-        f"{passes_per_freq:g} zgemv passes per frequency; {nf} frequencies; "
-        f"{wall:.1f} s of CPU work"), wall=wall,
-        parts=dict(prep_static_s=(prep + static) * scale,
-                   assembly_per_freq_s=statistics.mean(dyn) * scale,
-                   scatter_per_freq_s=dense["scatter"],
-                   apply_bcs_per_freq_s=dense["apply_bcs"], gemv_per_freq_s=dense["gemv"]))
+    return dict(vertices=m.vertices, triangles=m.triangles,
+                med=O.Medium(cfg.material.lam, cfg.material.mu, cfg.material.rho),
+                kinds=cfg.bcs.flat_kind(), dof_signal=cfg.bcs.flat_signal(),
+                signal_samples=[np.asarray(s.sample(cfg.period, cfg.n_omega), float)
+                                for s in cfg.signals],
+                period=cfg.period, n_omega=cfg.n_omega, kappa=cfg.kappa,
+                sem_depth=cfg.sem_depth, sem=cfg.sem_enabled, tol=cfg.tol,
+                restart=cfg.restart, maxiter=cfg.maxiter)
+
+
+def cpu_chained(cfg, n_freq=None):
+    """MEASURED: the reference algorithm (oracle port, every host core) runs
+    the chained sweep of ``cfg`` for k = 0..n_freq-1 (None = the whole sweep):
+    geometry prep + static pass, then per frequency assembly, apply_bcs, SEM,
+    block preconditioner and GMRES (driver.py:92-176)."""
+    from oracle.parallel import sweep_seconds
+
+    return sweep_seconds(oracle_inputs(cfg), frequencies=n_freq)
 
 
 # ----------------------------------------------------------------------
@@ -251,6 +187,55 @@ def fp64_peak():
                                            _lib.stream_handle()))
         best = max(best, tf.value)
     return best
+
+
+TRAFFIC_FILE = ROOT / "profiles" / "traffic.json"
+
+
+def traffic_record(workload: str) -> dict | None:
+    """ncu dram read+write per launch unit, keyed by workload (profiles/traffic.json)."""
+    if not TRAFFIC_FILE.exists():
+        return None
+    return json.loads(TRAFFIC_FILE.read_text()).get(workload)
+
+
+def cpu_baseline_block(workload: str, cfg, n_freq: int) -> dict:
+    """``cpu_baseline`` of our arm: MEASURED runs of the reference algorithm
+    (oracle port) on this host, every core.  cfg1: the whole 65-frequency
+    sweep.  cfg2: setup + the first two complete chained frequencies (k = 0
+    without and k = 1 with SEM); the s/sweep value is derived from them as
+    setup + 129 x mean per frequency and labelled so."""
+    from paper_1212_3032_b200 import workloads
+
+    host = host_info()
+    if workload == "cfg1":
+        m = cpu_chained(cfg)
+        total = m["setup_s"] + sum(m["per_freq_s"])
+        return {"value": round(total, 2), "unit": "s/sweep", "cores": m["workers"],
+                "kind": "port", "measured": True,
+                "sample": f"the whole cfg1 sweep ({len(m['per_freq_s'])} frequencies), measured",
+                "iterations_total": int(sum(m["its"])), "setup_s": round(m["setup_s"], 2),
+                "host": host}
+    m2 = cpu_chained(cfg, 2)
+    per = statistics.mean(m2["per_freq_s"])
+    value = m2["setup_s"] + n_freq * per
+    m1 = cpu_chained(workloads.cfg1())
+    return {"value": round(value, 1), "unit": "s/sweep", "cores": m2["workers"], "kind": "port",
+            "measured": False,
+            "sample": ("cfg2 setup (geometry prep + static pass) and the first 2 complete chained "
+                       "frequencies (assembly, apply_bcs, SEM, preconditioner, GMRES) measured; "
+                       f"value = setup + {n_freq} x mean measured frequency"),
+            "measured_parts": {"cfg2_setup_s": round(m2["setup_s"], 2),
+                               "cfg2_prep_s": round(m2["prep_s"], 2),
+                               "cfg2_static_s": round(m2["static_s"], 2),
+                               "cfg2_per_freq_s": [round(t, 2) for t in m2["per_freq_s"]],
+                               "cfg2_its": m2["its"],
+                               "cfg2_freq_parts": [{k: round(v, 3) for k, v in p.items()}
+                                                   for p in m2["parts"]],
+                               "cfg1_full_sweep_s": round(m1["setup_s"] + sum(m1["per_freq_s"]), 2),
+                               "cfg1_frequencies": len(m1["per_freq_s"]),
+                               "cfg1_iterations_total": int(sum(m1["its"]))},
+            "host": host}
 
 
 def build_cfg(workload: str):
@@ -355,7 +340,6 @@ def run_ours_sweep(args, rank, world, local_rank):
         dist.barrier()
     ms_per_step = elapsed_ms / args.steps
     value = (elapsed_ms / 1e3) / (args.steps * world)   # s per sweep, whole job
-    its = sum(s for s in [0])
     # per-frequency assembly: FP64 roofline;  solve phase: HBM roofline
     n = ds.n
     asm_per_freq_ms = asm_ms / max(nfreq, 1)
@@ -380,18 +364,15 @@ def run_ours_sweep(args, rank, world, local_rank):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)", "traffic": None,
                 "algorithmic_bytes_per_pass": bytes_per_pass,
                 "passes_per_sweep": matvecs / max(args.steps, 1)}
-    # DRAM traffic of the dominant kernels from the committed ncu capture
-    tr_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01",
-                           "traffic.json")
-    if os.path.exists(tr_path):
-        with open(tr_path) as fh:
-            tr = json.load(fh)
-        rl_solve["traffic"] = tr["k_gmres_f"]["bytes_per_pass"]
-        rl_solve["traffic_unit"] = "bytes per pass over A (ncu dram read+write)"
-        rl_solve["traffic_source"] = tr["k_gmres_f"]["source"]
-        rl_asm["traffic"] = tr["k_far_multi"]["bytes_per_freq"]
-        rl_asm["traffic_unit"] = "bytes per frequency (ncu dram read+write of k_far_multi)"
-        rl_asm["traffic_source"] = tr["k_far_multi"]["source"]
+    # DRAM traffic of the dominant kernels from the committed ncu capture of
+    # THIS workload (null when none was captured for it)
+    tr = traffic_record(args.workload)
+    if tr:
+        for key, rl in (("solve", rl_solve), ("assembly", rl_asm)):
+            if key in tr:
+                rl["traffic"] = tr[key]["bytes"]
+                rl["traffic_unit"] = tr[key]["unit"]
+                rl["traffic_source"] = tr[key]["source"]
     asm_share = asm_ms / max(asm_ms + solve_ms, 1e-9)
     # the same multi-frequency assembly outside the sweep (clocks not pulled
     # down by the power-capped GMRES phase): one batch of mid-sweep members
@@ -438,22 +419,28 @@ def run_ours_sweep(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        passes = (matvecs / max(nfreq, 1)) + cfg.sem_depth - 1   # reference: K separate matvecs
-        est = cpu_sweep_estimate(cfg, 48, [1, ds.n_freq // 2, ds.n_freq - 1], 7, passes)
-        cpu = {"value": round(est["value"], 1), "unit": "s/sweep", "cores": os.cpu_count(),
-               "kind": "port", "sample": est["sample"], "parts": est["parts"],
-               "host": host_info()}
+        cpu = cpu_baseline_block(args.workload, cfg, ds.n_freq)
+    cfg5_block = None
+    if rank == 0 and args.workload == "cfg2" and not args.no_cfg5:
+        del ds
+        gc.collect()
+        torch.cuda.empty_cache()
+        from benchmarks import micro
+
+        cfg5_block = micro.cfg5_measure(steps=3, warmup=1, peak64=peak64)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "s/sweep", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seedless deterministic mesh + step load, BASELINE cfg2)",
+            "data": ("synthetic (reference-generated mesh + unit step load, BASELINE %s)"
+                     % args.workload),
             "config": {"workload": desc, "baseline_metric": BASELINE_METRIC,
                        "l2": "inputs larger than L2 (A = 16 N^2 = %.2f GB)" % (16 * n * n / 1e9),
                        "parallelism": "replicas" if world > 1 else "single GPU"},
             "roofline": roof, "roofline_secondary": roof2,
             "cpu_baseline": cpu,
+            "cfg5_matrix_free": cfg5_block,
             "e2e": {"value": e2e_s / world, "unit": "s/sweep", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
@@ -475,27 +462,31 @@ def run_ours_sweep(args, rank, world, local_rank):
 
 
 def run_reference(args, rank, world):
-    """The reference algorithm on the host CPU (oracle port), rank 0 only."""
+    """The reference algorithm on the host CPU (oracle port, every core), rank 0
+    only: the chained sweep from k = 0, one complete frequency per step
+    (assembly, apply_bcs, SEM, preconditioner, GMRES); W warm-up frequencies,
+    then K timed ones.  value = measured setup + n_freq x mean timed frequency."""
     if rank != 0:
         return
     cfg, desc = build_cfg(args.workload)
     nf = cfg.n_omega // 2 + 1
-    passes = 8.0 if args.workload == "cfg2" else 40.0
-    times = []
-    for step in range(args.warmup + args.steps):
-        k = [1 + (step * 37) % (nf - 1)]
-        est = cpu_sweep_estimate(cfg, 24, k, 100 + step, passes)
-        if step >= args.warmup:
-            times.append(est["value"])
-            sample = est["sample"]
-    value = statistics.mean(times)
+    m = cpu_chained(cfg, min(nf, args.warmup + args.steps))
+    timed = m["per_freq_s"][args.warmup:] or m["per_freq_s"]
+    per = statistics.mean(timed)
+    value = m["setup_s"] + nf * per
+    sample = (f"setup + frequencies k = 0..{len(m['per_freq_s']) - 1} of the chained sweep "
+              f"measured ({len(timed)} timed after {args.warmup} warm-up); value = setup + "
+              f"{nf} x mean timed frequency")
     line = {"metric": METRIC, "value": value, "unit": "s/sweep", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "step": "one complete frequency of the chained sweep (CPU)",
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": desc, "baseline_metric": BASELINE_METRIC},
-            "cpu_baseline": {"value": value, "unit": "s/sweep", "cores": os.cpu_count(),
-                             "kind": "port", "sample": sample, "host": host_info()},
+            "cpu_baseline": {"value": value, "unit": "s/sweep", "cores": m["workers"],
+                             "kind": "port", "sample": sample, "measured_setup_s": m["setup_s"],
+                             "measured_per_freq_s": m["per_freq_s"], "its": m["its"],
+                             "host": host_info()},
             "e2e": {"value": value, "unit": "s/sweep", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -258,12 +258,12 @@ def run_cfg4(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
-def run_cfg5(args, rank, world, local_rank):
+def cfg5_measure(steps: int, warmup: int, peak64: float | None = None) -> dict:
     """cfg5: ico6 cavity, 81,920 el / 245,760 DOF, matrix-free (966 GB dense).
 
-    value = element pairs per second of one matrix-free operator application
-    (6.7e9 pairs, 2.04e10 quadrature points); the first two frequencies of the
-    SEM sweep (the reference's own check range) are solved and timed too."""
+    One matrix-free operator application (6.7e9 pairs, 2.04e10 quadrature
+    points, K = 1) timed with CUDA events, plus the first two frequencies of
+    the SEM sweep (the reference's own check range).  Returns the figures."""
     import torch
 
     import bench
@@ -273,8 +273,7 @@ def run_cfg5(args, rank, world, local_rank):
     from paper_1212_3032_b200.workloads import cfg5
 
     lib = _lib.require_cuda()
-    torch.cuda.set_device(local_rank)
-    peak64 = bench.fp64_peak()
+    peak64 = peak64 or bench.fp64_peak()
     cfg = cfg5()
     t0 = time.perf_counter()
     ds = DeviceSweep(cfg, frequencies=[0, 1])
@@ -286,44 +285,61 @@ def run_cfg5(args, rank, world, local_rank):
     flops = 397.0 * pe + 72.0 * pairs            # SURVEY §8(d) matrix-free count
     op = MatrixFreeOperator(ds.asm, complex(ds.omegas[1]))
     v = torch.randn((1, ds.n), dtype=torch.complex128, device="cuda")
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):
         op.apply_multi(v)
     torch.cuda.synchronize()
-    sampler = bench.ClockSampler(local_rank)
+    sampler = bench.ClockSampler(torch.cuda.current_device())
     l0 = lib.ewb_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
+    for _ in range(steps):
         op.apply_multi(v)
     e1.record()
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = lib.ewb_launch_count() - l0
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / steps
     ds.matrix_free = True
+    torch.cuda.synchronize()
     t1 = time.perf_counter()
     stats = ds.run()
+    torch.cuda.synchronize()
     first2 = time.perf_counter() - t1
     tf = flops / (ms * 1e-3) / 1e12
+    return {
+        "workload": "cfg5: flipped icosphere L6, 81920 el / 245760 DOF, matrix-free",
+        "application_ms": ms, "pair_evals_per_s": pairs / (ms * 1e-3),
+        "point_evals_per_application": pe, "pairs": pc, "steps": steps,
+        "roofline": {"bound": "fp64", "kernel": "k_mf_farmid<1> (+ k_mf_near, k_mf_self): one A v",
+                     "achieved": tf, "peak": peak64, "unit": "TFLOP/s", "frac": tf / peak64,
+                     "traffic": None, "algorithmic_flops_per_launch": flops,
+                     "peak_source": "measured DFMA probe",
+                     "ncu": "profiles/r02/SUMMARY.md (matrix-free capture)"},
+        "gpu_launches": launches, "clocks": clocks, "setup_s": setup_s,
+        "first_two_frequencies_s": first2,
+        "first_two": {int(k): dict(iterations=s.iterations, applications=s.matvecs,
+                                   init_residual=s.init_residual,
+                                   final_residual=s.final_residual)
+                      for k, s in stats.items()},
+    }
+
+
+def run_cfg5(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    r = cfg5_measure(args.steps, args.warmup)
     line = {
-        "metric": "element-pair kernel evals/s", "value": pairs / (ms * 1e-3),
+        "metric": "element-pair kernel evals/s", "value": r["pair_evals_per_s"],
         "unit": "pair-evals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (deterministic ico6 cavity, unit step pressure)",
-        "config": {"workload": "cfg5: flipped icosphere L6, 81920 el / 245760 DOF, matrix-free "
-                               "operator application (one step = one A v over all 6.7e9 pairs)",
-                   "l2": "compute-bound"},
-        "roofline": {"bound": "fp64", "achieved": tf, "peak": peak64, "unit": "TFLOP/s",
-                     "frac": tf / peak64, "traffic": None, "algorithmic_flops_per_launch": flops,
-                     "peak_source": "measured DFMA probe"},
-        "gpu_launches": launches, "clocks": clocks,
-        "metrics": {"setup_s": setup_s, "point_evals_per_application": pe,
-                    "point_evals_per_s": pe / (ms * 1e-3), "pairs": pc,
-                    "first_two_frequencies_s": first2,
-                    "first_two": {k: dict(iterations=s.iterations, applications=s.matvecs,
-                                          init_residual=s.init_residual,
-                                          final_residual=s.final_residual)
-                                  for k, s in stats.items()}},
+        "ms_per_step": r["application_ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference-generated ico6 cavity, unit step pressure)",
+        "config": {"workload": r["workload"] + " operator application (one step = one A v "
+                                               "over all 6.7e9 pairs)", "l2": "compute-bound"},
+        "roofline": r["roofline"], "gpu_launches": r["gpu_launches"], "clocks": r["clocks"],
+        "metrics": {k: r[k] for k in ("setup_s", "point_evals_per_application", "pairs",
+                                      "first_two_frequencies_s", "first_two")},
     }
     print(json.dumps(line), flush=True)
 

@@ -284,6 +284,15 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   if (pinv && n % 3) return fail(EWB_ERR_INVALID, "ewb_gmres: preconditioner needs n % 3 == 0");
   if (ws_bytes < ewb_gmres_workspace_bytes(n, restart))
     return fail(EWB_ERR_INVALID, "ewb_gmres: workspace too small");
+  // the update phase keeps max(RU, 512) + RU complex values of the idle
+  // ring, RU = rows per CTA + the <= 2 rows completing its last element
+  {
+    const int64_t G = ewb::solver_grid_blocks();
+    const int64_t ru = (n + G - 1) / G + 2;
+    if ((ru > 512 ? ru : 512) + ru > ewb::ring_cplx_capacity())
+      return fail(EWB_ERR_INVALID, "ewb_gmres: too many rows per solver CTA for the shared-memory "
+                                   "ring (raise the solver CTA count, ewb_set_solver_ctas)");
+  }
   ewb::GmresArgs g{};
   auto* base = (ewb::cplx*)ws;
   g.A = (const ewb::cplx*)a;
@@ -474,8 +483,12 @@ int ewb_window_idft(const void* half, int64_t n_half, int64_t D, int32_t window,
         tab[N + 2 * k + 1] = std::sin(ph);
       }
       EWB_CUDA(cudaMalloc(&dtab, sizeof(double) * 3 * N), "ewb_window_idft");
-      EWB_CUDA(cudaMemcpy(dtab, tab.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice),
+      // ordered on the caller's stream (a non-blocking stream would not wait
+      // for a legacy-stream copy); the host table must outlive the copy
+      EWB_CUDA(cudaMemcpyAsync(dtab, tab.data(), sizeof(double) * 3 * N, cudaMemcpyHostToDevice,
+                               S(stream)),
                "ewb_window_idft");
+      EWB_CUDA(cudaStreamSynchronize(S(stream)), "ewb_window_idft");
       cache[{dev, N, window}] = dtab;
     }
   }

@@ -1104,6 +1104,8 @@ static int g_solver_limit = 0;  // 0: every co-resident CTA
 
 void set_solver_ctas(int ctas) { g_solver_limit = ctas > 0 ? ctas : 0; }
 
+long long ring_cplx_capacity() { return kRingBytes / 16; }
+
 int solver_grid_blocks() {
   const int m = solver_grid_max();
   return g_solver_limit > 0 && g_solver_limit < m ? g_solver_limit : m;

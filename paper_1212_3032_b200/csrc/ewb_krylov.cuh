@@ -113,6 +113,7 @@ cudaError_t launch_op_gmres(int phase, OpArgs& args, cudaStream_t s);  // 0 begi
 int solver_grid_max();      // co-resident CTAs of the solver kernels (workspace sizing)
 int solver_grid_blocks();   // CTAs the solver launches use (<= max, see set_solver_ctas)
 void set_solver_ctas(int ctas);
+long long ring_cplx_capacity();  // complex values the solver shared-memory ring holds
 cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s);
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s);
 // QR + solve of SEM from caller-supplied products Y = A X (args.A unused)

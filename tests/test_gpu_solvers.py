@@ -203,20 +203,55 @@ def test_cfg1_stepwise_iterations_equal_reference(cuda):
     assert max(abs(d) for d in diffs) <= 1, diffs
 
 
+def _reference_solver_chain(ds, cfg):
+    """The reference's solver (the oracle: bitwise equal to linsolve.py's
+    sem_initial_guess / block_diag_precond / gmres) run as the chained sweep
+    (driver.py:128-153) on the SAME systems the device sweep assembled —
+    re-assembled here in the sweep's own batches (bit-reproducible kernels)
+    and read back.  Returns the per-k iteration counts."""
+    from oracle import ewbem_oracle as O
+
+    nb = ds.batch_size()
+    hist = O.History(cfg.sem_depth)
+    its = []
+    batch = None
+    for k0 in range(0, ds.n_freq, nb):
+        ks = list(range(k0, min(ds.n_freq, k0 + nb)))
+        batch = ds.asm.assemble_system_multi([ds.omegas[k] for k in ks], cfg.bcs,
+                                             ds.P[ks[0]:ks[-1] + 1], out=batch, check=False)
+        for f in range(len(ks)):
+            m = batch.member(f)
+            a, b = m.A.cpu().numpy(), m.b.cpu().numpy()
+            x0 = O.sem_guess(hist, a, b) if len(hist) else None
+            pc, _ = O.block_precond(a)
+            x, st = O.gmres(a, b, x0=x0, tol=cfg.tol, restart=cfg.restart, maxiter=cfg.maxiter,
+                            precond=pc)
+            its.append(st.iterations)
+            hist.push(x)
+    return np.array(its)
+
+
 def test_cfg1_sweep_matches_reference_run(cuda):
     """BASELINE cfg1 end to end (65 SEM-chained solves, tol 1e-8, K=2).
 
-    Histories within 1e-6.  Iteration counts: each solve stops within tol
-    with a rounding-different iterate, and SEM feeds it forward, so the
-    chained counts drift like the reference's own rerun on another CPU
-    (9/65 frequencies off, max 2).  Bar: |d| <= 1 on >= 95 %
-    of frequencies, <= 2 everywhere, total within 1 %."""
+    Iterations +-1 on EVERY frequency against the reference's solver chained
+    over the same assembled systems, on this box (the same-input comparison).
+    Against the reference's own run (golden, reference-assembled matrices):
+    histories 1e-6; counts differ by <= 2 at a few k.  That residue is the
+    chain's sensitivity, not the solver: the reference's own solver chained
+    over our matrices (which equal the reference's to 2.3e-15 of max|A|)
+    shows the same deviation from the golden run (tools/diag_chain.py:
+    k = 4 -> -2, k = 5 -> -1 for both)."""
     from paper_1212_3032_b200 import run_sweep
+    from paper_1212_3032_b200.driver import DeviceSweep
     from paper_1212_3032_b200.workloads import cfg1
 
     g = golden("cfg1_sweep")
-    res = run_sweep(cfg1())
+    cfg = cfg1()
+    res = run_sweep(cfg)
     its = np.array([s.iterations for s in res.stats])
+    ref_same = _reference_solver_chain(DeviceSweep(cfg), cfg)
+    assert np.abs(its - ref_same).max() <= 1, (its - ref_same).tolist()
     d = np.abs(its - g["cfg1_its"])
     assert d.max() <= 2 and (d <= 1).mean() >= 0.95, d
     assert abs(its.sum() - g["cfg1_its"].sum()) <= 0.01 * g["cfg1_its"].sum()
@@ -418,9 +453,9 @@ def test_concurrent_solves_equal_sequential(cuda):
 
 @pytest.mark.parametrize("nb", [1, 5, 32])
 def test_cfg1_sweep_any_assembly_batch(cuda, nb):
-    """The sweep with 1, 5 or 32 frequencies per assembly pass reproduces the
-    reference's cfg1 histories (1e-6) and iteration counts (as the default-batch
-    end-to-end test)."""
+    """The sweep with 1, 5 or 32 frequencies per assembly pass: iterations +-1
+    on every k against the reference's solver chained over the same systems,
+    histories 1e-6 against the reference's run (as the default-batch test)."""
     from paper_1212_3032_b200.driver import DeviceSweep
     from paper_1212_3032_b200.transform import windowed_inverse_device
     from paper_1212_3032_b200.workloads import cfg1
@@ -431,6 +466,8 @@ def test_cfg1_sweep_any_assembly_batch(cuda, nb):
     assert ds.batch_size() == nb
     st = ds.run()
     its = np.array([st[k].iterations for k in sorted(st)])
+    ref_same = _reference_solver_chain(ds, cfg)
+    assert np.abs(its - ref_same).max() <= 1, (its - ref_same).tolist()
     d = np.abs(its - g["cfg1_its"])
     assert d.max() <= 2 and (d <= 1).mean() >= 0.95, d
     series, _ = windowed_inverse_device(ds.probe_half(cfg.probes), cfg.window, ds.eta, cfg.period)
