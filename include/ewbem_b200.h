@@ -280,6 +280,14 @@ int ewb_pair_kernels_reduce(const double* x_dev, int64_t P, const double* tri_de
 int ewb_fp64_peak_probe(int64_t iters, int32_t blocks_per_sm, double* tflops_host,
                         double* ms_host, void* stream);
 
+/* Debug-build self checks (library built with -DEWB_DEBUG_CHECKS; the
+ * stand-in for compute-sanitizer): *failures = device-side
+ * invariant violations recorded since the last reset (index bounds,
+ * ring-slot bookkeeping, scratch capacity), *first_site = the first
+ * violated check's id (0 if none).  A release build reports *failures = -1.
+ * reset != 0 clears the counters after reading.  Synchronises the device. */
+int ewb_debug_checks(int64_t* failures, int64_t* first_site, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

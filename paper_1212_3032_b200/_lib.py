@@ -28,7 +28,7 @@ EXPORTS = (
     "ewb_opgmres_workspace_bytes", "ewb_opgmres_buffers", "ewb_opgmres_phase", "ewb_window_idft",
     "ewb_matfree_workspace_bytes", "ewb_matfree_apply",
     "ewb_pair_kernels_blocks", "ewb_pair_kernels_workspace_bytes",
-    "ewb_pair_kernels_reduce", "ewb_fp64_peak_probe",
+    "ewb_pair_kernels_reduce", "ewb_fp64_peak_probe", "ewb_debug_checks",
 )
 
 EWB_OK, EWB_ERR_INVALID, EWB_ERR_CUDA, EWB_ERR_NONFINITE = 0, 1, 2, 3
@@ -93,15 +93,20 @@ _SIGS = {
     "ewb_pair_kernels_workspace_bytes": (I64, [I64, I64, I32]),
     "ewb_pair_kernels_reduce": (I32, [P, I64, P, I64, P, P, I32, D, D, D, P, P, P, I64, P]),
     "ewb_fp64_peak_probe": (I32, [I64, I32, P, P, P]),
+    "ewb_debug_checks": (I32, [P, P, I32]),
 }
 
 
 def load(path: os.PathLike | None = None):
-    """Load (once) and return the ctypes library.  Raises NativeUnavailable."""
+    """Load (once) and return the ctypes library.  Raises NativeUnavailable.
+
+    ``EWB_LIBRARY`` selects another build of the same ABI (the debug-check
+    build of DESIGN.md §4, ``paper_1212_3032_b200/variants/debug.so``)."""
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    env = os.environ.get("EWB_LIBRARY")
+    p = Path(path) if path else (Path(env) if env else LIB_PATH)
     if not p.exists():
         raise NativeUnavailable(
             f"{p} is not built; run `python -m paper_1212_3032_b200.build` "

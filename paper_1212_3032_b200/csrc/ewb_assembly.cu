@@ -30,6 +30,7 @@
 #include "ewb_ctx.cuh"
 
 namespace ewb {
+EWB_DEBUG_TU(assembly)
 
 // point_triangle_distance (mesh.py:165-204) for one point.
 __device__ double point_tri_distance(double px, double py, double pz, const double v[9]) {
@@ -361,6 +362,8 @@ __global__ void __launch_bounds__(128, 3) k_near(Geo g, Phys<DYN> ph, PairOut o,
   if (wp >= n_near) return;
   const int p = g.near_order[wp];
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
+  EWB_DCHECK(p >= 0 && p < n_near && i >= 0 && i < g.n_e && j >= 0 && j < g.n_e && i != j &&
+                 L >= 1 && L <= kMaxNearLevel, 204);
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
   const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
@@ -829,6 +832,7 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
           const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
           unsigned ex = 0;
           cplx* Af = o.A + (size_t)f * N * N;
+          EWB_DCHECK(3LL * i + 2 < N && 3LL * j + 2 < N && f < nf && nf <= kMaxBatch, 201);
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
@@ -854,7 +858,10 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           warp_sum(bc[a]);
-          if (lane == 0) o.bpart[((size_t)f * ntile + t) * N + 3 * i + a] = bc[a];
+          if (lane == 0) {
+            EWB_DCHECK(t < ntile && 3LL * i + a < N, 202);
+            o.bpart[((size_t)f * ntile + t) * N + 3 * i + a] = bc[a];
+          }
         }
       }
     }
@@ -873,6 +880,7 @@ __global__ void __launch_bounds__(128, 3) k_mid_multi(Geo g, FreqBatch fb, SysBa
   const int f = (int)(idx / n_mid), p = (int)(idx % n_mid);
   const FreqConst& fc0 = fb.fc[0];
   const int i = g.mid_row[p], j = g.mid_j[p];
+  EWB_DCHECK(i >= 0 && i < g.n_e && j >= 0 && j < g.n_e && i != j, 203);
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
   const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
@@ -967,6 +975,8 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
   if (wp >= n_near) return;
   const int p = g.near_order[wp];
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
+  EWB_DCHECK(p >= 0 && p < n_near && i >= 0 && i < g.n_e && j >= 0 && j < g.n_e && i != j &&
+                 L >= 1 && L <= kMaxNearLevel, 204);
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
   const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];
@@ -1088,6 +1098,7 @@ __global__ void __launch_bounds__(128, 3) k_self_multi(Geo g, FreqBatch fb, SysB
     const cplx* bp = o.bpart + (size_t)f * ntile * N;
     const int m0 = g.mid_ptr[j], m1 = g.mid_ptr[j + 1];
     const int q0 = g.near_ptr[j], q1 = g.near_ptr[j + 1];
+    EWB_DCHECK(0 <= m0 && m0 <= m1 && m1 <= n_mid && 0 <= q0 && q0 <= q1 && q1 <= n_near, 205);
     for (int a = 0; a < 3; ++a) {
       cplx s = {0.0, 0.0}, sm = {0.0, 0.0}, sn = {0.0, 0.0};
       for (int t = lane; t < ntile; t += 32) s = s + bp[(size_t)t * N + 3 * j + a];
@@ -1437,6 +1448,13 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
   if (err) return err;
   FreqBatch fb = make_batch(c, nf, ore, oim);
   const bool recur = fb.recur != 0;
+  if (kDebugChecks) {  // the b partials of every tile / pair must be written before the sum
+    const size_t n3 = 3 * (size_t)c.n_e;
+    err = dbg_poison(c.bpart_m, (size_t)nf * c.n_tiles * n3 * 16, s);
+    if (!err) err = dbg_poison(c.bmid_m, (size_t)nf * 3 * c.n_mid * 16, s);
+    if (!err) err = dbg_poison(c.bnear_m, (size_t)nf * 3 * c.n_near * 16, s);
+    if (err) return err;
+  }
   SysBatch o{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
   const int n = c.n_e;
   const long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;

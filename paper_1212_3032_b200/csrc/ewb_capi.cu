@@ -172,6 +172,11 @@ static int check_omega(double ore, double oim, const char* who) {
 int ewb_assemble_tu(ewb_ctx* ctx, double ore, double oim, void* t, void* u, void* stream) {
   if (!ctx || !t || !u) return fail(EWB_ERR_INVALID, "ewb_assemble_tu: null argument");
   if (int rc = check_omega(ore, oim, "ewb_assemble_tu")) return rc;
+  {
+    const size_t nn = 9 * (size_t)ctx->c.n_e * ctx->c.n_e * 16;
+    EWB_CUDA(ewb::dbg_poison(t, nn, S(stream)), "ewb_assemble_tu");
+    EWB_CUDA(ewb::dbg_poison(u, nn, S(stream)), "ewb_assemble_tu");
+  }
   EWB_CUDA(ewb::launch_assemble_tu(ctx->c, ore, oim, (ewb::cplx*)t, (ewb::cplx*)u, S(stream)),
            "ewb_assemble_tu");
   return EWB_OK;
@@ -182,6 +187,12 @@ int ewb_assemble_system(ewb_ctx* ctx, double ore, double oim, const uint8_t* kin
   if (!ctx || !kinds || !p || !a || !b || !pinv)
     return fail(EWB_ERR_INVALID, "ewb_assemble_system: null argument");
   if (int rc = check_omega(ore, oim, "ewb_assemble_system")) return rc;
+  {
+    const size_t N = 3 * (size_t)ctx->c.n_e;
+    EWB_CUDA(ewb::dbg_poison(a, N * N * 16, S(stream)), "ewb_assemble_system");
+    EWB_CUDA(ewb::dbg_poison(b, N * 16, S(stream)), "ewb_assemble_system");
+    EWB_CUDA(ewb::dbg_poison(pinv, 3 * N * 16, S(stream)), "ewb_assemble_system");
+  }
   EWB_CUDA(ewb::launch_assemble_system(ctx->c, ore, oim, kinds, (const ewb::cplx*)p,
                                        (ewb::cplx*)a, (ewb::cplx*)b, (ewb::cplx*)pinv, S(stream)),
            "ewb_assemble_system");
@@ -197,6 +208,12 @@ int ewb_assemble_system_multi(ewb_ctx* ctx, int32_t nf, const double* ore, const
     return fail(EWB_ERR_INVALID, "ewb_assemble_system_multi: nf must be in [1, EWB_MAX_BATCH]");
   for (int f = 0; f < nf; ++f)
     if (int rc = check_omega(ore[f], oim[f], "ewb_assemble_system_multi")) return rc;
+  {  // every entry of A, b, P^{-1} must have a writer
+    const size_t N = 3 * (size_t)ctx->c.n_e;
+    EWB_CUDA(ewb::dbg_poison(a, nf * N * N * 16, S(stream)), "ewb_assemble_system_multi");
+    EWB_CUDA(ewb::dbg_poison(b, nf * N * 16, S(stream)), "ewb_assemble_system_multi");
+    EWB_CUDA(ewb::dbg_poison(pinv, nf * 3 * N * 16, S(stream)), "ewb_assemble_system_multi");
+  }
   EWB_CUDA(ewb::launch_assemble_system_multi(ctx->c, nf, ore, oim, kinds, (const ewb::cplx*)p,
                                              (ewb::cplx*)a, (ewb::cplx*)b, (ewb::cplx*)pinv,
                                              flags, S(stream)),
@@ -319,6 +336,7 @@ int ewb_gmres(const void* a, const void* b, const void* pinv, void* x, int32_t h
   g.has_x0 = has_x0;
   g.hist_cap = hist_cap;
   g.tol = tol;
+  EWB_CUDA(ewb::dbg_poison(ws, (size_t)ws_bytes, S(stream)), "ewb_gmres");
   EWB_CUDA(ewb::launch_gmres(g, S(stream)), "ewb_gmres");
   return EWB_OK;
 }
@@ -350,6 +368,7 @@ int ewb_sem_guess(const void* a, const void* b, const void* xh, int32_t K, int64
   s.n = n;
   s.K = K;
   s.rank_tol = rank_tol;
+  EWB_CUDA(ewb::dbg_poison(ws, (size_t)ws_bytes, S(stream)), "ewb_sem_guess");
   EWB_CUDA(ewb::launch_sem(s, S(stream)), "ewb_sem_guess");
   return EWB_OK;
 }
@@ -563,6 +582,10 @@ int ewb_matfree_apply(ewb_ctx* ctx, double ore, double oim, const void* vt, cons
   if (int rc = check_omega(ore, oim, "ewb_matfree_apply")) return rc;
   if (ws_bytes < (int64_t)ewb::mf_workspace_bytes(ctx->c, K))
     return fail(EWB_ERR_INVALID, "ewb_matfree_apply: workspace too small");
+  if (!gate) {  // a gated call may skip its work and must leave y alone
+    EWB_CUDA(ewb::dbg_poison(ws, (size_t)ws_bytes, S(stream)), "ewb_matfree_apply");
+    EWB_CUDA(ewb::dbg_poison(y, (size_t)K * 3 * ctx->c.n_e * 16, S(stream)), "ewb_matfree_apply");
+  }
   EWB_CUDA(ewb::launch_matfree(ctx->c, ore, oim, (const ewb::cplx*)vt, (const ewb::cplx*)vu, K,
                                (ewb::cplx*)y, kinds, (ewb::cplx*)pinv, ws, gate, S(stream)),
            "ewb_matfree_apply");
@@ -641,6 +664,36 @@ int ewb_fp64_peak_probe(int64_t iters, int32_t blocks_per_sm, double* tflops, do
   if (!tflops || !ms || iters < 1 || blocks_per_sm < 1)
     return fail(EWB_ERR_INVALID, "ewb_fp64_peak_probe: bad argument");
   EWB_CUDA(ewb::fp64_peak_probe(iters, blocks_per_sm, tflops, ms, S(stream)), "ewb_fp64_peak_probe");
+  return EWB_OK;
+}
+
+int ewb_debug_checks(int64_t* failures, int64_t* first_site, int32_t reset) {
+  if (!failures || !first_site) return fail(EWB_ERR_INVALID, "ewb_debug_checks: null argument");
+  EWB_CUDA(cudaDeviceSynchronize(), "ewb_debug_checks");
+  if (!ewb::kDebugChecks) {
+    *failures = -1;
+    *first_site = 0;
+    return EWB_OK;
+  }
+  unsigned long long v[4][2];
+  ewb::dbg_fetch_assembly(v[0]);
+  ewb::dbg_fetch_krylov(v[1]);
+  ewb::dbg_fetch_matfree(v[2]);
+  ewb::dbg_fetch_spectral(v[3]);
+  int64_t total = 0, site = 0;
+  for (auto& t : v) {
+    total += (int64_t)t[0];
+    if (!site && t[0]) site = (int64_t)t[1];
+  }
+  *failures = total;
+  *first_site = site;
+  if (reset) {
+    ewb::dbg_reset_assembly();
+    ewb::dbg_reset_krylov();
+    ewb::dbg_reset_matfree();
+    ewb::dbg_reset_spectral();
+  }
+  EWB_CUDA(cudaGetLastError(), "ewb_debug_checks");
   return EWB_OK;
 }
 

@@ -28,6 +28,41 @@ namespace ewb {
 void note_launch();
 #define EWB_NOTE ::ewb::note_launch(),
 
+// Debug build (-DEWB_DEBUG_CHECKS; read through ewb_debug_checks in the C
+// ABI): device-side invariant checks (index bounds, ring-slot bookkeeping,
+// scratch capacity) count violations and keep the first violated site per
+// translation unit, and every workspace is filled with NaN before a call so
+// a read of a word the kernels never wrote poisons the results the parity
+// tests compare.  This stands in for compute-sanitizer, which the GPU pool
+// does not run.  The release build compiles all of it away.
+#ifdef EWB_DEBUG_CHECKS
+static __device__ unsigned long long g_ewb_dbg[2];
+#define EWB_DCHECK(cond, site)                                        \
+  do {                                                                \
+    if (!(cond) && atomicAdd(&::ewb::g_ewb_dbg[0], 1ull) == 0ull)     \
+      ::ewb::g_ewb_dbg[1] = (unsigned long long)(site);               \
+  } while (0)
+#define EWB_DEBUG_TU(name)                                            \
+  void dbg_fetch_##name(unsigned long long* o) {                      \
+    cudaMemcpyFromSymbol(o, g_ewb_dbg, sizeof(g_ewb_dbg));            \
+  }                                                                   \
+  void dbg_reset_##name() {                                           \
+    const unsigned long long z[2] = {0ull, 0ull};                     \
+    cudaMemcpyToSymbol(g_ewb_dbg, z, sizeof(z));                      \
+  }
+inline cudaError_t dbg_poison(void* p, size_t bytes, cudaStream_t s) {
+  return p && bytes ? cudaMemsetAsync(p, 0xff, bytes, s) : cudaSuccess;   // all-ones = NaN
+}
+constexpr bool kDebugChecks = true;
+#else
+#define EWB_DCHECK(cond, site) ((void)0)
+#define EWB_DEBUG_TU(name)                                            \
+  void dbg_fetch_##name(unsigned long long* o) { o[0] = o[1] = 0ull; } \
+  void dbg_reset_##name() {}
+inline cudaError_t dbg_poison(void*, size_t, cudaStream_t) { return cudaSuccess; }
+constexpr bool kDebugChecks = false;
+#endif
+
 constexpr double kSeriesSwitch = 0.35;   // kernels.py:36 (strict <)
 constexpr double kFarRatio = 4.0;        // quadrature.py:206 far_threshold
 constexpr double kNearRatio = 1.5;       // quadrature.py:207 near_threshold

@@ -25,6 +25,7 @@
 namespace cg = cooperative_groups;
 
 namespace ewb {
+EWB_DEBUG_TU(krylov)
 
 // one 512-thread CTA per SM: register cap 65536 / 512 = 128 per thread
 // (a 256-thread CTA streamed a pass in 749 us instead of 525 us)
@@ -136,6 +137,8 @@ __device__ __forceinline__ void ring_init(Ring& R, bool evict_first) {
 __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cplx* A, long long n,
                                            long long row0, int nrows, long long c0, int tc) {
   const int b = pos % kNS;
+  EWB_DCHECK(nrows >= 1 && nrows <= kRR && tc >= 1 && tc <= kTC && row0 >= 0 &&
+                 row0 + nrows <= n && c0 >= 0 && c0 + tc <= n, 101);
   const uint32_t bar = smem_u32(&R.bar[b]);
   const uint32_t bytes = (uint32_t)(nrows * tc * 16);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
@@ -295,8 +298,12 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
       }
     }
     __syncwarp();
-    if ((threadIdx.x & 31) == 0 &&
-        atomicAdd(&s_rel[pos % kNS], 1) == kSolveWarps - 1) {  // last reader of the slot
+    int rel_old = -1;
+    if ((threadIdx.x & 31) == 0) {
+      rel_old = atomicAdd(&s_rel[pos % kNS], 1);
+      EWB_DCHECK(rel_old >= 0 && rel_old < kSolveWarps, 102);
+    }
+    if (rel_old == kSolveWarps - 1) {  // last reader of the slot
       s_rel[pos % kNS] = 0;
       if (s + kNS < S) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -334,6 +341,10 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
       ++t;
     }
   }
+#ifdef EWB_DEBUG_CHECKS
+  __syncthreads();
+  if (threadIdx.x < kNS) EWB_DCHECK(s_rel[threadIdx.x] == 0, 103);  // every slot released
+#endif
   R.pos += (unsigned)S;
 }
 
@@ -424,8 +435,12 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
         }
     }
     __syncwarp();
-    if ((threadIdx.x & 31) == 0 &&
-        atomicAdd(&s_rel[pos % kNS], 1) == kSolveWarps - 1) {  // last reader of the slot
+    int rel_old = -1;
+    if ((threadIdx.x & 31) == 0) {
+      rel_old = atomicAdd(&s_rel[pos % kNS], 1);
+      EWB_DCHECK(rel_old >= 0 && rel_old < kSolveWarps, 102);
+    }
+    if (rel_old == kSolveWarps - 1) {  // last reader of the slot
       s_rel[pos % kNS] = 0;
       if (s + kNS < S) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -463,6 +478,10 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
       ++t;
     }
   }
+#ifdef EWB_DEBUG_CHECKS
+  __syncthreads();
+  if (threadIdx.x < kNS) EWB_DCHECK(s_rel[threadIdx.x] == 0, 103);  // every slot released
+#endif
   R.pos += (unsigned)S;
 }
 
@@ -699,6 +718,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(Gmre
       cplx* gsm = scr;
       {
         const int tri = j * (j - 1) / 2;
+        if (threadIdx.x == 0) EWB_DCHECK(tri <= kRingBytes / 16, 105);
         for (int q = threadIdx.x; q < tri; q += blockDim.x) {
           // packed index q -> (i, l), i >= 1, l < i
           int i = (int)((1.0 + sqrt(1.0 + 8.0 * q)) * 0.5);
@@ -756,6 +776,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(Gmre
         const int nc = max(1, min(nv, kSolveThreads / max(RU, 1)));
         cplx* pu = scr;            // [nc][RU] chunk partials
         cplx* su = scr + nc * RU;  // [RU] u
+        if (threadIdx.x == 0) EWB_DCHECK(RU >= 0 && nc * RU + RU <= kRingBytes / 16, 104);
         for (int p = threadIdx.x; p < nc * RU; p += blockDim.x) {
           const int r = p % RU, c = p / RU;
           const int i0 = c * nv / nc, i1 = (c + 1) * nv / nc;
@@ -860,6 +881,7 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_gmres_f(Gmre
     // the upper triangle of H staged (packed) into the idle ring first.
     {
       cplx* hsm = ring.buf;
+      if (threadIdx.x == 0) EWB_DCHECK(used * (used + 1) / 2 <= kRingBytes / 16, 106);
       for (int i = 0; i < used; ++i)
         for (int k = i + threadIdx.x; k < used; k += blockDim.x)
           hsm[i * used - i * (i - 1) / 2 + (k - i)] = a.H[(size_t)i * kMaxRestart + k];
@@ -957,6 +979,7 @@ __device__ void sem_body(cg::grid_group& grid, GridRed& R, const SemArgs& a) {
   __shared__ int nkeep;
   if (threadIdx.x == 0) {
     nkeep = a.K;
+    EWB_DCHECK(a.K >= 1 && a.K <= kMaxSem, 107);
     for (int c = 0; c < a.K; ++c) keep[c] = c;
   }
   __syncthreads();

@@ -114,6 +114,15 @@ int solver_grid_max();      // co-resident CTAs of the solver kernels (workspace
 int solver_grid_blocks();   // CTAs the solver launches use (<= max, see set_solver_ctas)
 void set_solver_ctas(int ctas);
 long long ring_cplx_capacity();  // complex values the solver shared-memory ring holds
+// debug build (-DEWB_DEBUG_CHECKS): per translation unit violation count + first site
+void dbg_fetch_assembly(unsigned long long* o);
+void dbg_fetch_krylov(unsigned long long* o);
+void dbg_fetch_matfree(unsigned long long* o);
+void dbg_fetch_spectral(unsigned long long* o);
+void dbg_reset_assembly();
+void dbg_reset_krylov();
+void dbg_reset_matfree();
+void dbg_reset_spectral();
 cudaError_t launch_gmres(GmresArgs& args, cudaStream_t s);
 cudaError_t launch_sem(SemArgs& args, cudaStream_t s);
 // QR + solve of SEM from caller-supplied products Y = A X (args.A unused)

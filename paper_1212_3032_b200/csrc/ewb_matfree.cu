@@ -24,6 +24,7 @@
 #include "ewb_ctx.cuh"
 
 namespace ewb {
+EWB_DEBUG_TU(matfree)
 
 constexpr int kMfTile = 32;
 constexpr int kMfMaxK = 5;
@@ -213,6 +214,8 @@ __global__ void __launch_bounds__(128) k_mf_near(Geo g, Phys<true> ph, MfArgs m,
   if (wp >= n_near) return;
   const int p = g.near_order[wp];   // deepest level first (uniform CTAs)
   const int i = g.near_row[p], j = g.near_j[p], L = g.near_lvl[p];
+  EWB_DCHECK(p >= 0 && p < n_near && i >= 0 && i < g.n_e && j >= 0 && j < g.n_e && i != j &&
+                 L >= 1 && L <= kMaxNearLevel, 301);
   const long long N = 3LL * g.n_e;
   const double xi = g.cx[i], yi = g.cy[i], zi = g.cz[i];
   const double nx = g.nx[j], ny = g.ny[j], nz = g.nz[j], ar = g.area[j];

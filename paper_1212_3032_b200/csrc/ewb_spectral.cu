@@ -11,6 +11,7 @@
 #include "ewb_common.cuh"
 
 namespace ewb {
+EWB_DEBUG_TU(spectral)
 
 __global__ void k_window_idft(const cplx* half, long long n_half, long long D, const double* win,
                               const cplx* tw, double eta_dt, double* out, double* residue) {
