@@ -113,7 +113,11 @@ def load(path: os.PathLike | None = None):
             "(there is no CPU fallback for the B200 path)")
     lib = ctypes.CDLL(str(p))
     for name, (res, args) in _SIGS.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and p != LIB_PATH:
+            continue   # an older A/B build (tools/build_variant.py) without this entry point
+        if fn is None:
+            raise NativeUnavailable(f"{p} does not export {name}")
         fn.restype = res
         fn.argtypes = args
     if lib.ewb_abi_version() != ABI_VERSION:

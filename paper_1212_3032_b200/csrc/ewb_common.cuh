@@ -180,12 +180,12 @@ __device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), ld
 // per use in an unrolled loop (measured: 5.7 % of k_far_multi's issued
 // instructions); a __constant__ value is read straight from the constant bank.
 struct NumConst {
-  double two, three, four, nine, far_sw, series_sw;
+  double two, three, four, nine, far_sw, series_sw, six, fifteen, half;
 };
 #ifdef EWB_STRICT_SWITCH
-static __constant__ NumConst c_num = {2.0, 3.0, 4.0, 9.0, 0.35, 0.35};
+static __constant__ NumConst c_num = {2.0, 3.0, 4.0, 9.0, 0.35, 0.35, 6.0, 15.0, 0.5};
 #else
-static __constant__ NumConst c_num = {2.0, 3.0, 4.0, 9.0, 0.1, 0.35};  // far_sw = kFarSwitch
+static __constant__ NumConst c_num = {2.0, 3.0, 4.0, 9.0, 0.1, 0.35, 6.0, 15.0, 0.5};  // far_sw = kFarSwitch
 #endif
 
 // Four radial brackets  phi*r, psi*r, dphi/dr*r^2, dpsi/dr*r^2.

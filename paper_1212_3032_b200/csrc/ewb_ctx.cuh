@@ -123,6 +123,7 @@ struct FreqBatch {
   int nf;
   int recur;                         // 1: step the phase factors across the batch
   double dks, dkp;                   // Re(ks), Re(kp) step between consecutive members
+  double cr2, c4r;                   // ratio - 2, 4 - ratio (ratio = c_p^2 / c_s^2)
 };
 
 // Outputs of a multi-frequency system assembly; member f of every array

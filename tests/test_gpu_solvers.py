@@ -298,6 +298,35 @@ def test_cfg2_head_matches_reference(cuda):
         hist[0] = x
 
 
+def test_cfg2_full_sweep_matches_reference_run(cuda):
+    """BASELINE cfg2 (the headline) end to end: all 129 SEM-chained solves of
+    run_sweep against the live reference's own 129-frequency run
+    (tests/golden/make_golden.py cfg2_sweep, driver.py:92-176): iterations
+    +-1 per k, SEM initial residuals, probe histories 1e-6 relative L2,
+    no failed frequency, and every reported final residual <= tol."""
+    from conftest import GOLDEN
+    from paper_1212_3032_b200 import run_sweep
+    from paper_1212_3032_b200.workloads import cfg2
+
+    if not (GOLDEN / "cfg2_sweep.npz").exists():
+        pytest.skip("cfg2_sweep.npz not generated")
+    g = golden("cfg2_sweep")
+    res = run_sweep(cfg2())
+    its = np.array([s.iterations for s in res.stats])
+    d = its - g["cfg2_its"]
+    assert np.abs(d).max() <= 1, d.tolist()
+    init = np.array([s.init_residual for s in res.stats])
+    # the SEM guess lands near tol (SURVEY App. B-3): compare the initial
+    # residual where it is well above the floor the two products round to
+    big = g["cfg2_init"] > 1e-6
+    assert np.allclose(init[big], g["cfg2_init"][big], rtol=1e-4)
+    for name in g["cfg2_probes"]:
+        h, href = res.histories[str(name)], g[f"cfg2_h_{name}"]
+        assert np.linalg.norm(h - href) / np.linalg.norm(href) <= 1e-6, name
+    assert not res.failed_frequencies and len(g["failed"]) == 0
+    assert all(s.converged and s.final_residual <= 1e-8 for s in res.stats)
+
+
 def test_sem_ax0_and_gmres_start_from_it(cuda):
     """SEM's A x0 (= Y s, ABI v2) equals A @ x0, and GMRES started from it
     takes the same iterations to the same solution as with b - A x0."""
