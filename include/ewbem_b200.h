@@ -280,6 +280,12 @@ int ewb_pair_kernels_reduce(const double* x_dev, int64_t P, const double* tri_de
 int ewb_fp64_peak_probe(int64_t iters, int32_t blocks_per_sm, double* tflops_host,
                         double* ms_host, void* stream);
 
+/* The device sin/cos/exp the kernel phases use (ewb_common.cuh fast_sincos /
+ * fast_exp), evaluated on n HOST arguments into host arrays: the accuracy
+ * check against libm (tests).  Synchronises. */
+int ewb_math_selftest(const double* x_host, int64_t n, double* sin_host, double* cos_host,
+                      double* exp_host, void* stream);
+
 /* Debug-build self checks (library built with -DEWB_DEBUG_CHECKS; the
  * stand-in for compute-sanitizer): *failures = device-side
  * invariant violations recorded since the last reset (index bounds,

@@ -29,6 +29,7 @@ EXPORTS = (
     "ewb_matfree_workspace_bytes", "ewb_matfree_apply",
     "ewb_pair_kernels_blocks", "ewb_pair_kernels_workspace_bytes",
     "ewb_pair_kernels_reduce", "ewb_fp64_peak_probe", "ewb_debug_checks",
+    "ewb_math_selftest",
 )
 
 EWB_OK, EWB_ERR_INVALID, EWB_ERR_CUDA, EWB_ERR_NONFINITE = 0, 1, 2, 3
@@ -94,6 +95,7 @@ _SIGS = {
     "ewb_pair_kernels_reduce": (I32, [P, I64, P, I64, P, P, I32, D, D, D, P, P, P, I64, P]),
     "ewb_fp64_peak_probe": (I32, [I64, I32, P, P, P]),
     "ewb_debug_checks": (I32, [P, P, I32]),
+    "ewb_math_selftest": (I32, [P, I64, P, P, P, P]),
 }
 
 

@@ -661,7 +661,7 @@ __device__ __forceinline__ SysArgs sys_member(const SysBatch& o, int f, long lon
 
 __device__ __forceinline__ cplx unit_phase(double a) {
   double s, c;
-  sincos(a, &s, &c);
+  fast_sincos(a, &s, &c);
   return {c, -s};
 }
 

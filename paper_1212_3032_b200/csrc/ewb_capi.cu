@@ -521,6 +521,11 @@ int ewb_window_idft(const void* half, int64_t n_half, int64_t D, int32_t window,
 
 }  // extern "C"
 
+namespace ewb {
+cudaError_t launch_math_selftest(const double* x, long long n, double* s, double* c, double* e,
+                                 cudaStream_t st);
+}
+
 // ---------------------------------------------------------------------
 // matrix-free, pair-kernel microbenchmark, FP64 probe
 // ---------------------------------------------------------------------
@@ -664,6 +669,25 @@ int ewb_fp64_peak_probe(int64_t iters, int32_t blocks_per_sm, double* tflops, do
   if (!tflops || !ms || iters < 1 || blocks_per_sm < 1)
     return fail(EWB_ERR_INVALID, "ewb_fp64_peak_probe: bad argument");
   EWB_CUDA(ewb::fp64_peak_probe(iters, blocks_per_sm, tflops, ms, S(stream)), "ewb_fp64_peak_probe");
+  return EWB_OK;
+}
+
+int ewb_math_selftest(const double* x, int64_t n, double* sin_out, double* cos_out,
+                      double* exp_out, void* stream) {
+  if (!x || !sin_out || !cos_out || !exp_out || n < 0)
+    return fail(EWB_ERR_INVALID, "ewb_math_selftest: bad argument");
+  if (n == 0) return EWB_OK;
+  double* d = nullptr;
+  EWB_CUDA(cudaMalloc(&d, sizeof(double) * 4 * n), "ewb_math_selftest");
+  cudaStream_t s = S(stream);
+  cudaError_t e = cudaMemcpyAsync(d, x, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (!e) e = ewb::launch_math_selftest(d, n, d + n, d + 2 * n, d + 3 * n, s);
+  if (!e) e = cudaMemcpyAsync(sin_out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaMemcpyAsync(cos_out, d + 2 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaMemcpyAsync(exp_out, d + 3 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  EWB_CUDA(e, "ewb_math_selftest");
   return EWB_OK;
 }
 

@@ -223,11 +223,94 @@ __device__ __forceinline__ Brackets brackets_phase(const FreqConst& fc, double r
   return o;
 }
 
+// ---------------------------------------------------------------------
+// sin/cos and exp for the kernel phases e^{-i z} (kernels.py:103-104).
+// libdevice's versions materialise their polynomial coefficients as
+// immediates (two UMOV per constant per call: 13 % of the matrix-free
+// kernel's issued instructions, ncu r02) and carry the large-argument
+// reduction inline.  Here: Cody-Waite reduction by pi/2 in three FMA steps,
+// the fdlibm minimax kernels for sin and cos on [-pi/4, pi/4] (< 2^-58),
+// exp by 2^k e^r with |r| <= ln2/2 and a degree-13 Taylor polynomial
+// (truncation 4e-18); every coefficient is a constant-bank operand of its
+// DFMA.  Accuracy ~1 ulp (checked against libm over 2e6 arguments,
+// tests/test_gpu_assembly.py), far inside the 1e-10 parity bar.  Arguments
+// beyond |x| = 1e5 (never reached by a BEM phase) take libdevice's sincos.
+// ---------------------------------------------------------------------
+struct MathConst {
+  double two_over_pi, pio2_1, pio2_2, pio2_3, magic, sincos_big, half;
+  double s[6], c[6];
+  double log2e, ln2_hi, ln2_lo, exp_lo, exp_hi;
+  double e[14];   // 1/13!, 1/12!, ..., 1/1!, 1/0!
+};
+static __constant__ MathConst c_math = {
+    6.36619772367581382433e-01,  1.57079632679489655800e+00, 6.12323399573676603587e-17,
+    -1.49738490485916983520e-33, 6755399441055744.0,          1.0e5, 0.5,
+    {-1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+     2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10},
+    {4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+     -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11},
+    1.44269504088896338700e+00, 6.93147180559945286227e-01, 2.31904681384629955842e-17,
+    -746.0, 710.0,
+    {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+     1.0 / 362880.0, 1.0 / 40320.0, 1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0,
+     1.0 / 6.0, 0.5, 1.0, 1.0}};
+
+static __device__ __noinline__ void sincos_large(double x, double* s, double* c) { sincos(x, s, c); }
+
+__device__ __forceinline__ double flip_sign(double v, int neg) {
+  return __hiloint2double(__double2hiint(v) ^ (neg << 31), __double2loint(v));
+}
+
+__device__ __forceinline__ void fast_sincos(double x, double* sp, double* cp) {
+  if (!(fabs(x) <= c_math.sincos_big)) {   // also NaN / inf
+    sincos_large(x, sp, cp);
+    return;
+  }
+  const double t = fma(x, c_math.two_over_pi, c_math.magic);
+  const double kd = t - c_math.magic;
+  const int q = __double2loint(t);
+  double r = fma(-kd, c_math.pio2_1, x);
+  r = fma(-kd, c_math.pio2_2, r);
+  r = fma(-kd, c_math.pio2_3, r);
+  const double z = r * r;
+  double ps = fma(z, c_math.s[5], c_math.s[4]);
+  ps = fma(z, ps, c_math.s[3]);
+  ps = fma(z, ps, c_math.s[2]);
+  ps = fma(z, ps, c_math.s[1]);
+  ps = fma(z, ps, c_math.s[0]);
+  const double sn = fma(r * z, ps, r);
+  double pc = fma(z, c_math.c[5], c_math.c[4]);
+  pc = fma(z, pc, c_math.c[3]);
+  pc = fma(z, pc, c_math.c[2]);
+  pc = fma(z, pc, c_math.c[1]);
+  pc = fma(z, pc, c_math.c[0]);
+  const double cs = c_math.e[13] + fma(z * z, pc, -c_math.half * z);   // 1 - (z/2 - z^2 P)
+  const bool swap = q & 1;
+  *sp = flip_sign(swap ? cs : sn, (q >> 1) & 1);
+  *cp = flip_sign(swap ? sn : cs, ((q + 1) >> 1) & 1);
+}
+
+__device__ __forceinline__ double fast_exp(double x) {
+  double xd = x < c_math.exp_lo ? c_math.exp_lo : x;   // NaN passes through
+  xd = xd > c_math.exp_hi ? c_math.exp_hi : xd;
+  const double t = fma(xd, c_math.log2e, c_math.magic);
+  const double kd = t - c_math.magic;
+  const int k = __double2loint(t);
+  double r = fma(-kd, c_math.ln2_hi, xd);
+  r = fma(-kd, c_math.ln2_lo, r);
+  double p = fma(c_math.e[0], r, c_math.e[1]);
+#pragma unroll
+  for (int i = 2; i < 14; ++i) p = fma(p, r, c_math.e[i]);
+  const int k1 = k >> 1, k2 = k - k1;
+  p = p * __hiloint2double((k1 + 1023) << 20, 0);
+  return p * __hiloint2double((k2 + 1023) << 20, 0);
+}
+
 // e^{-i k r} = e^{Im(k) r} (cos(Re(k) r) - i sin(Re(k) r))
 __device__ __forceinline__ cplx phase_factor(cplx k, double r) {
   double s, c;
-  sincos(k.re * r, &s, &c);
-  double m = exp(k.im * r);
+  fast_sincos(k.re * r, &s, &c);
+  double m = fast_exp(k.im * r);
   return {m * c, -m * s};
 }
 
@@ -236,9 +319,9 @@ __device__ __forceinline__ Brackets brackets_closed(const FreqConst& fc, double 
   double zs_re = fc.ks.re * r, zs_im = fc.ks.im * r;
   double zp_re = fc.kp.re * r, zp_im = fc.kp.im * r;
   double ss, cs, sp, cp;
-  sincos(zs_re, &ss, &cs);
-  sincos(zp_re, &sp, &cp);
-  double ms = exp(zs_im), mp = exp(zp_im);
+  fast_sincos(zs_re, &ss, &cs);
+  fast_sincos(zp_re, &sp, &cp);
+  double ms = fast_exp(zs_im), mp = fast_exp(zp_im);
   cplx Es = {ms * cs, -ms * ss};
   cplx ep = {mp * cp, -mp * sp};
   cplx Ep = fc.g2 * ep;

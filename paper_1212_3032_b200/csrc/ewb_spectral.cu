@@ -69,3 +69,21 @@ cudaError_t launch_window_idft(const cplx* half, long long n_half, long long D, 
 }
 
 }  // namespace ewb
+
+namespace ewb {
+// device sin/cos/exp of the kernel phases (ewb_common.cuh) on host arguments:
+// the accuracy test of fast_sincos / fast_exp against libm (ewb_math_selftest)
+__global__ void k_math_selftest(const double* x, long long n, double* s, double* c, double* e) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  fast_sincos(x[i], s + i, c + i);
+  e[i] = fast_exp(x[i]);
+}
+
+cudaError_t launch_math_selftest(const double* x, long long n, double* s, double* c, double* e,
+                                 cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  EWB_NOTE k_math_selftest<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, s, c, e);
+  return cudaGetLastError();
+}
+}  // namespace ewb

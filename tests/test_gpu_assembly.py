@@ -304,3 +304,41 @@ def test_non_finite_entries_raise_per_member(cuda):
     cfg = dataclasses.replace(cfg1(), mesh=mesh, bcs=bcs, probes=[], allow_floating=True)
     with pytest.raises(SweepError, match="frequency index 0"):
         run_sweep(cfg)
+
+
+def test_device_sincos_exp_vs_libm(cuda):
+    """fast_sincos / fast_exp (the kernel phases e^{-i z}, kernels.py:103-104)
+    against numpy's libm: <= 2 ulp on the BEM argument ranges, the libdevice
+    path beyond |x| = 1e5, NaN / inf / underflow behaviour."""
+    import ctypes
+
+    from paper_1212_3032_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(1212)
+    x = np.concatenate([rng.uniform(-4, 4, 400_000), rng.uniform(-200, 200, 400_000),
+                        rng.uniform(-1e5, 1e5, 200_000), rng.uniform(-746, 0, 400_000),
+                        10.0 ** rng.uniform(-300, -2, 100_000),
+                        np.arange(-2000, 2000) * (np.pi / 2),
+                        [0.0, -0.0, 1e6, -3e7, 1e300, np.inf, -np.inf, np.nan, 709.7, 710.0,
+                         -745.0, -746.0, -800.0]])
+    n = len(x)
+    s, c, e = np.empty(n), np.empty(n), np.empty(n)
+    _lib.check(lib.ewb_math_selftest(x.ctypes.data, n, s.ctypes.data, c.ctypes.data,
+                                     e.ctypes.data, _lib.stream_handle()))
+    with np.errstate(all="ignore"):
+        rs, rc, re_ = np.sin(x), np.cos(x), np.exp(x)
+    fin = np.isfinite(x)
+    for got, ref in ((s, rs), (c, rc)):
+        assert np.array_equal(np.isnan(got), np.isnan(ref))
+        m = fin & (np.abs(x) <= 1e5)
+        ulp = np.abs(got[m] - ref[m]) / np.spacing(np.maximum(np.abs(ref[m]), 1e-300))
+        big = np.abs(ref[m]) >= 1e-3     # near a zero of sin/cos: absolute error instead
+        assert ulp[big].max() <= 2.0, ulp[big].max()
+        assert np.abs(got[m] - ref[m])[~big].max() <= 1e-19 * max(1.0, np.abs(x[m]).max())
+    m = fin & (x < 709.5) & (x > -708)
+    ulp = np.abs(e[m] - re_[m]) / np.spacing(re_[m])
+    assert ulp.max() <= 2.0, ulp.max()
+    assert np.isnan(e[np.isnan(x)]).all() and e[x == np.inf][0] == np.inf
+    assert e[x == -np.inf][0] == 0.0 and e[x == -800.0][0] == 0.0 and e[x == 710.0][0] == np.inf
+    assert e[x == -745.0][0] <= 1e-323
