@@ -153,15 +153,29 @@ def test_cfg3_subsample_vs_reference(cuda):
     assert rel_max(yt.cpu().numpy(), g["yt"]) <= 1e-10
 
 
-@pytest.mark.parametrize("n", [4096, 8192])
+_CFG4 = {}
+
+
+def _cfg4_systems(n):
+    """The 8 seeded cfg4-i systems of size n (host arrays, built once per run)."""
+    from paper_1212_3032_b200.workloads import cfg4_random_system
+
+    if n not in _CFG4:
+        _CFG4[n] = [cfg4_random_system(n, seed) for seed in range(8)]
+    return _CFG4[n]
+
+
+CFG4_SIZES = [4096, 8192, 16384]   # BASELINE cfg4
+
+
+@pytest.mark.parametrize("n", CFG4_SIZES)
 def test_cfg4_gemv_batched_vs_numpy(cuda, n):
     """ewb_gemv_batched on the 8 seeded cfg4-i systems vs numpy (<= 1e-12)."""
     torch = cuda
     from paper_1212_3032_b200 import _lib
-    from paper_1212_3032_b200.workloads import cfg4_random_system
 
     lib = _lib.load()
-    sys_ = [cfg4_random_system(n, seed) for seed in range(8)]
+    sys_ = _cfg4_systems(n)
     A = torch.from_numpy(np.stack([a for a, _ in sys_])).cuda()
     X = torch.from_numpy(np.stack([b for _, b in sys_])).cuda()
     Y = torch.empty_like(X)
@@ -172,19 +186,19 @@ def test_cfg4_gemv_batched_vs_numpy(cuda, n):
         assert rel_max(Yh[i], a @ b) <= 1e-12
 
 
-@pytest.mark.parametrize("n", [4096, 8192])
+@pytest.mark.parametrize("n", CFG4_SIZES)
 def test_cfg4_gmres_vs_reference(cuda, n):
     """GMRES (restart 50, tol 1e-8, no preconditioner) on the 8 seeded cfg4-i
     systems: iteration counts within +-1 of the reference's gmres, solutions
     1e-8, final residual = literal ||b - A x|| / ||b||."""
     torch = cuda
     from paper_1212_3032_b200 import gmres
-    from paper_1212_3032_b200.workloads import cfg4_random_system
 
     g = golden("cfg4_gmres")
+    if f"n{n}_its" not in g:
+        pytest.skip(f"no reference golden for n = {n}")
     its_ref, x_ref = g[f"n{n}_its"], g[f"n{n}_x"]
-    for seed in range(8):
-        a, b = cfg4_random_system(n, seed)
+    for seed, (a, b) in enumerate(_cfg4_systems(n)):
         ad = torch.from_numpy(a).cuda()
         x, st = gmres(ad, b, tol=1e-8, restart=50, maxiter=1000)
         assert abs(st.iterations - int(its_ref[seed])) <= 1
