@@ -298,6 +298,37 @@ def test_cfg2_head_matches_reference(cuda):
         hist[0] = x
 
 
+def test_cfg2_stepwise_iterations_equal_reference(cuda):
+    """BASELINE cfg2 at k = 32, 64, 128 (low, middle, top of the sweep): fed the
+    live reference's own four previous solutions (cfg2_sweep.npz), our SEM +
+    GMRES reproduce the reference's iteration count (+-1), SEM initial
+    residual and solution (1e-6)."""
+    import torch
+
+    from conftest import GOLDEN
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.linsolve import gmres_device, sem_device
+    from paper_1212_3032_b200.workloads import cfg2
+
+    if not (GOLDEN / "cfg2_sweep.npz").exists():
+        pytest.skip("cfg2_sweep.npz not generated")
+    g = golden("cfg2_sweep")
+    keep = {int(k): x for k, x in zip(g["keep_k"], g["keep_x"])}
+    cfg = cfg2()
+    ds = DeviceSweep(cfg, frequencies=[0])
+    x = torch.zeros(ds.n, dtype=torch.complex128, device="cuda")
+    sysm = None
+    for k in (32, 64, 128):
+        sysm = ds.asm.assemble_system(ds.omegas[k], cfg.bcs, ds.P[k], out=sysm)
+        hist = torch.from_numpy(np.stack([keep[k - 1 - i] for i in range(4)])).cuda()
+        sem_device(sysm.A, sysm.b, hist, 1e-10, x)
+        st = gmres_device(sysm.A, sysm.b, x, True, cfg.tol, cfg.restart, cfg.maxiter, sysm.pinv)
+        assert abs(st.iterations - int(g["cfg2_its"][k])) <= 1, (k, st.iterations, g["cfg2_its"][k])
+        assert abs(st.init_residual - g["cfg2_init"][k]) <= 1e-4 * g["cfg2_init"][k], k
+        assert rel_max(x.cpu().numpy(), keep[k]) <= 1e-6, k
+        assert st.converged and st.final_residual <= cfg.tol
+
+
 def test_cfg2_full_sweep_matches_reference_run(cuda):
     """BASELINE cfg2 (the headline) end to end: all 129 SEM-chained solves of
     run_sweep against the live reference's own 129-frequency run
