@@ -405,6 +405,7 @@ def ref_sphere_pressure(level: int, n_omega: int, sem_depth: int = 4):
 
 # per-k solution vectors kept for the "fed reference history" GPU tests
 CFG2_KEEP = tuple(range(28, 33)) + tuple(range(60, 65)) + tuple(range(124, 129))
+CFG2_KEEP_ALL = False   # cfg2_solutions: every k (the full stepwise test), 31 MB
 
 
 def section_cfg2_sweep():
@@ -431,7 +432,7 @@ def section_cfg2_sweep():
         x, st = orig_gmres(*a, **kw)
         rec["gmres_s"].append(time.perf_counter() - t0)
         k = len(rec["gmres_s"]) - 1
-        if k in CFG2_KEEP:
+        if CFG2_KEEP_ALL or k in CFG2_KEEP:
             rec["x"][k] = x.copy()
         print(f"cfg2 k={k}: its={st.iterations} init={st.init_residual:.3e} "
               f"final={st.final_residual:.3e} asm={rec['asm_s'][-1]:.1f}s", flush=True)
@@ -457,14 +458,30 @@ def section_cfg2_sweep():
     out["cfg2_hist_len"] = np.array([len(s.residual_history) for s in res.stats])
     out["cfg2_hist_cat"] = np.concatenate([np.asarray(s.residual_history, float)
                                            for s in res.stats])
+    if CFG2_KEEP_ALL:
+        save("cfg2_solutions", k=out["keep_k"], x=out["keep_x"], its=out["cfg2_its"],
+             init=out["cfg2_init"])
+        return
     save("cfg2_sweep", **out)
+
+
+def section_cfg2_solutions():
+    """The same live-reference cfg2 run, keeping every per-k solution (the
+    stepwise test feeds each frequency the reference's own history)."""
+    global CFG2_KEEP_ALL
+    CFG2_KEEP_ALL = True
+    try:
+        section_cfg2_sweep()
+    finally:
+        CFG2_KEEP_ALL = False
 
 
 SECTIONS = dict(small=section_small, cfg1_rows=section_cfg1_rows, tiers=section_tiers,
                 linsolve=section_linsolve, transform=section_transform,
                 sweeps=section_sweeps, cfg1_sweep=section_cfg1_sweep,
                 cfg1_solutions=section_cfg1_solutions,
-                cfg2_head=section_cfg2_head, cfg2_sweep=section_cfg2_sweep)
+                cfg2_head=section_cfg2_head, cfg2_sweep=section_cfg2_sweep,
+                cfg2_solutions=section_cfg2_solutions)
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(SECTIONS)

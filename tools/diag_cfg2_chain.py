@@ -36,12 +36,16 @@ def main():
            "hist_rel": {str(nm): float(np.linalg.norm(res.histories[str(nm)] - g[f"cfg2_h_{nm}"])
                                        / np.linalg.norm(g[f"cfg2_h_{nm}"]))
                         for nm in g["cfg2_probes"]},
-           "gpu_total": int(its.sum()), "golden_total": int(g["cfg2_its"].sum())}
+           "gpu_total": int(its.sum()), "golden_total": int(g["cfg2_its"].sum()),
+           "spec_rel_gpu": {str(nm): (np.abs(np.asarray(res.half_spectra[str(nm)]) - g[f"cfg2_s_{nm}"])
+                                      / np.abs(g[f"cfg2_s_{nm}"]).max()).tolist()
+                            for nm in g["cfg2_probes"]}}
     if "--no-chain" not in sys.argv:
         ds = DeviceSweep(cfg)
         nb = ds.batch_size()
         hist = O.History(cfg.sem_depth)
         och, batch, t0 = [], None, time.perf_counter()
+        probe_vals = {p.name: [] for p in cfg.probes}
         for k0 in range(0, ds.n_freq, nb):
             ks = list(range(k0, min(ds.n_freq, k0 + nb)))
             batch = ds.asm.assemble_system_multi([ds.omegas[k] for k in ks], cfg.bcs,
@@ -55,10 +59,27 @@ def main():
                                 maxiter=cfg.maxiter, precond=pc)
                 och.append(st.iterations)
                 hist.push(x)
+                for p in cfg.probes:          # all-Neumann: displacement = unknown
+                    probe_vals[p.name].append(x[p.dof])
                 print(f"k={ks[f]} gpu={its[ks[f]]} ref_solver={st.iterations} "
                       f"golden={g['cfg2_its'][ks[f]]} {time.perf_counter() - t0:.0f}s",
                       file=sys.stderr, flush=True)
         och = np.array(och)
+        eta = O.eta_from_kappa(cfg.kappa, cfg.period)
+        h_ref_solver = {}
+        for nm, vals in probe_vals.items():
+            series, _ = O.inverse_transform(O.conjugate_fill(np.array(vals)), cfg.window, eta,
+                                            cfg.period)
+            h_ref_solver[nm] = series
+        out["hist_rel_ref_solver_vs_golden"] = {
+            nm: float(np.linalg.norm(h_ref_solver[nm] - g[f"cfg2_h_{nm}"])
+                      / np.linalg.norm(g[f"cfg2_h_{nm}"])) for nm in h_ref_solver}
+        out["hist_rel_gpu_vs_ref_solver"] = {
+            nm: float(np.linalg.norm(res.histories[nm] - h_ref_solver[nm])
+                      / np.linalg.norm(h_ref_solver[nm])) for nm in h_ref_solver}
+        out["spec_rel_ref_solver"] = {
+            nm: (np.abs(np.array(vals) - g[f"cfg2_s_{nm}"]) / np.abs(g[f"cfg2_s_{nm}"]).max()).tolist()
+            for nm, vals in probe_vals.items()}
         out.update(ref_solver_its=och.tolist(), d_ref_solver=(its - och).tolist(),
                    ref_solver_vs_golden=(och - g["cfg2_its"]).tolist(),
                    chain_seconds=time.perf_counter() - t0)
