@@ -86,31 +86,43 @@ __device__ void grid_sum(cg::grid_group& grid, GridRed& R, double (&v)[C]) {
 }
 
 // ---------------------------------------------------------------------
-// TMA (cp.async.bulk) matvec.  Row groups of kRR rows are dealt to CTAs
-// round-robin; each CTA streams its groups through a kNS-stage ring of
-// shared-memory tiles (kRR rows x kTC columns = 32 KB), one bulk copy per
-// row segment, completion tracked by a transaction-count mbarrier per
-// stage.  Thread t owns column t % kTC of every tile for kRR/2 rows; the
-// per-row sums are reduced across the CTA at the end of each row group.
-// Up to kNS x 32 KB = 192 KB per SM are in flight with no register cost.
+// TMA (cp.async.bulk) matvec.  Each CTA streams its row blocks through a
+// kNS-stage ring of shared-memory tiles (kRR rows x kTC columns), one bulk
+// copy per row segment, completion tracked by a transaction-count mbarrier
+// per stage.  Thread t owns column t % kTC of every tile (or kCpt columns
+// when the tile is wider than the CTA) for kRpt rows; the per-row sums are
+// reduced across the CTA at the end of each row block.  kNS x 96 KB =
+// 192 KB per SM are in flight with no register cost.
 // ---------------------------------------------------------------------
+// Ring geometry: 12 rows x 512 columns x 16 B = 96 KB per stage, 2 stages.
+// The row segments are 8 KB bulk copies; measured on cfg2 (A/B in one job,
+// tools/sweep_time.py): 16 x 256 x 3 (4 KB copies) 3.63 s of solves per
+// sweep, 8 x 512 x 3 3.39 s, 12 x 512 x 2 3.31 s, 4 x 1024 x 2-3 (16 KB
+// copies, two columns per thread) 3.54 s; cfg4 GEMV 7.04 -> 7.35 TB/s.
+// Fewer, larger copies per byte are what the TMA path rewards.
 #ifndef EWB_RING_RR
-#define EWB_RING_RR 16
+#define EWB_RING_RR 12
 #endif
 #ifndef EWB_RING_TC
-#define EWB_RING_TC 256
+#define EWB_RING_TC 512
 #endif
 #ifndef EWB_RING_NS
-#define EWB_RING_NS 3
+#define EWB_RING_NS 2
 #endif
 constexpr int kRR = EWB_RING_RR;
 constexpr int kTC = EWB_RING_TC;
 constexpr int kNS = EWB_RING_NS;
 constexpr int kStageElems = kRR * kTC;
 constexpr int kRingBytes = kNS * kStageElems * 16;
-constexpr int kSlices = kSolveThreads / kTC;     // row slices per tile
+// Thread mapping of a tile: kTC <= kSolveThreads -> kSlices row slices,
+// thread = (slice, column), kRpt rows each; kTC > kSolveThreads -> one slice,
+// thread = kCpt columns (col + m kSolveThreads) x all kRR rows.
+constexpr int kSlices = kTC <= kSolveThreads ? kSolveThreads / kTC : 1;   // row slices per tile
 constexpr int kRpt = kRR / kSlices;              // rows per thread
-static_assert(kSolveThreads % kTC == 0 && kRR % kSlices == 0, "tile geometry");
+constexpr int kCpt = kTC <= kSolveThreads ? 1 : kTC / kSolveThreads;      // columns per thread
+constexpr int kColSpan = kTC <= kSolveThreads ? kTC : kSolveThreads;      // threads per slice
+static_assert((kSolveThreads % kTC == 0 || kTC % kSolveThreads == 0) && kRR % kSlices == 0,
+              "tile geometry");
 
 struct Ring {
   cplx* buf;            // dynamic shared memory, kNS stages
@@ -257,43 +269,59 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int u = 0; u < S && u < kNS; ++u) issue(u);
   }
-  const int col = threadIdx.x % kTC, slice = threadIdx.x / kTC;
+  const int col = threadIdx.x % kColSpan, slice = threadIdx.x / kColSpan;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   cplx acc[kRpt][K];
 #pragma unroll
   for (int r = 0; r < kRpt; ++r)
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
-  cplx xn[K];  // x for the stage being consumed (prefetched one stage ahead)
+  cplx xn[kCpt][K];  // x for the stage being consumed (prefetched one stage ahead)
 #pragma unroll
-  for (int k = 0; k < K; ++k) xn[k] = col < n ? ldg(x + k * n + col) : cplx{0.0, 0.0};
+  for (int m = 0; m < kCpt; ++m)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = col + m * kColSpan;
+      xn[m][k] = c < n ? ldg(x + k * n + c) : cplx{0.0, 0.0};
+    }
   int q = 0, t = 0;
   long long row0 = r0;
   int nrows = rows / nblk;
   for (int s = 0; s < S; ++s) {
     const long long c0 = (long long)t * kTC;
     const int tc = t == ntile - 1 ? last_tc : kTC;
-    cplx xv[K];
+    cplx xv[kCpt][K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) xv[k] = xn[k];
+    for (int m = 0; m < kCpt; ++m)
+#pragma unroll
+      for (int k = 0; k < K; ++k) xv[m][k] = xn[m][k];
     {  // prefetch the next stage's x
       const long long cn = (t == ntile - 1 ? 0 : c0 + kTC) + col;
 #pragma unroll
-      for (int k = 0; k < K; ++k) xn[k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
+      for (int m = 0; m < kCpt; ++m)
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          xn[m][k] = cn + m * kColSpan < n ? ldg(x + k * n + cn + m * kColSpan) : cplx{0.0, 0.0};
     }
     if (t == max(0, ntile - 1 - kEpiPrefetch)) pre(row0, nrows);
     const unsigned pos = R.pos + (unsigned)s;
     ring_wait(R, pos);
-    if (col < tc) {
+    {
       const cplx* tile = R.buf + (size_t)(pos % kNS) * kStageElems;
 #pragma unroll
-      for (int r = 0; r < kRpt; ++r) {
-        const int row = slice * kRpt + r;
-        if (row < nrows) {
-          double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + col);
-          cplx av = {a2.x, a2.y};
+      for (int m = 0; m < kCpt; ++m) {
+        const int c = col + m * kColSpan;
+        if (c < tc) {
 #pragma unroll
-          for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[k]);
+          for (int r = 0; r < kRpt; ++r) {
+            const int row = slice * kRpt + r;
+            if (row < nrows) {
+              double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + c);
+              cplx av = {a2.x, a2.y};
+#pragma unroll
+              for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xv[m][k]);
+            }
+          }
         }
       }
     }

