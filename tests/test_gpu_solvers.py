@@ -329,6 +329,58 @@ def test_cfg2_stepwise_iterations_equal_reference(cuda):
         assert st.converged and st.final_residual <= cfg.tol
 
 
+def test_cfg2_stepwise_all_frequencies(cuda):
+    """BASELINE cfg2, all 129 frequencies, through the sweep's own
+    multi-frequency assembly batches: each frequency fed the live reference's
+    four previous solutions (tests/golden/cfg2_solutions.npz, the reference's
+    run_sweep) reproduces the reference's iteration count (+-1) and solution
+    (1e-6), and the probe histories built from these per-frequency solutions
+    match the reference's (1e-6 relative L2) — per-frequency parity without the
+    chain's sensitivity (test_cfg2_full_sweep_matches_reference_run)."""
+    import torch
+
+    from conftest import GOLDEN
+    from paper_1212_3032_b200.driver import DeviceSweep
+    from paper_1212_3032_b200.linsolve import gmres_device, sem_device
+    from paper_1212_3032_b200.transform import windowed_inverse_device
+    from paper_1212_3032_b200.workloads import cfg2
+
+    if not (GOLDEN / "cfg2_solutions.npz").exists():
+        pytest.skip("cfg2_solutions.npz not generated")
+    g = golden("cfg2_solutions")
+    gs = golden("cfg2_sweep")
+    xs, its_ref = g["x"], g["its"]
+    cfg = cfg2()
+    ds = DeviceSweep(cfg, frequencies=[0])
+    nf, nb = ds.n_freq, 16
+    assert xs.shape == (nf, ds.n)
+    x = torch.zeros(ds.n, dtype=torch.complex128, device="cuda")
+    half = torch.zeros((nf, len(cfg.probes)), dtype=torch.complex128, device="cuda")
+    dofs = torch.tensor([p.dof for p in cfg.probes], device="cuda")
+    d, sol_err, batch = [], 0.0, None
+    for k0 in range(0, nf, nb):
+        ks = list(range(k0, min(nf, k0 + nb)))
+        batch = ds.asm.assemble_system_multi([ds.omegas[k] for k in ks], cfg.bcs,
+                                             ds.P[ks[0]:ks[-1] + 1], out=batch, check=False)
+        for f, k in enumerate(ks):
+            m = batch.member(f)
+            if k:
+                hist = torch.from_numpy(np.stack([xs[k - 1 - i] for i in range(min(4, k))])).cuda()
+                sem_device(m.A, m.b, hist, 1e-10, x)
+            st = gmres_device(m.A, m.b, x, k > 0, cfg.tol, cfg.restart, cfg.maxiter, m.pinv)
+            d.append(st.iterations - int(its_ref[k]))
+            assert st.converged and st.final_residual <= cfg.tol, k
+            sol_err = max(sol_err, rel_max(x.cpu().numpy(), xs[k]))
+            half[k] = x[dofs]      # all-Neumann: the probe displacements are unknowns
+    assert max(abs(v) for v in d) <= 1, d
+    assert sol_err <= 1e-6, sol_err
+    series, _ = windowed_inverse_device(half, cfg.window, ds.eta, cfg.period)
+    series = series.cpu().numpy()
+    for c, p in enumerate(cfg.probes):
+        href = gs[f"cfg2_h_{p.name}"]
+        assert np.linalg.norm(series[:, c] - href) / np.linalg.norm(href) <= 1e-6, p.name
+
+
 def test_cfg2_full_sweep_matches_reference_run(cuda):
     """BASELINE cfg2 (the headline) end to end: all 129 SEM-chained solves of
     run_sweep against the live reference's own 129-frequency run
