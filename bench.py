@@ -426,7 +426,7 @@ def run_ours_sweep(args, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_block(args.workload, cfg, ds.n_freq)
-    cfg5_block = None
+    cfg5_block = other_metrics = None
     if rank == 0 and args.workload == "cfg2" and not args.no_cfg5:
         del ds
         gc.collect()
@@ -434,6 +434,9 @@ def run_ours_sweep(args, rank, world, local_rank):
         from benchmarks import micro
 
         cfg5_block = micro.cfg5_measure(steps=3, warmup=1, peak64=peak64)
+        # the other two metrics BASELINE.json names, on their own configs
+        other_metrics = {"cfg3_pair_kernels": micro.cfg3_measure(3, 2, peak64),
+                         "cfg4_gemv": micro.cfg4_gemv_measure()}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "s/sweep", "n_gpus": world,
@@ -447,6 +450,7 @@ def run_ours_sweep(args, rank, world, local_rank):
             "roofline": roof, "roofline_secondary": roof2,
             "cpu_baseline": cpu,
             "cfg5_matrix_free": cfg5_block,
+            "baseline_metrics_other_configs": other_metrics,
             "e2e": {"value": e2e_s / world, "unit": "s/sweep", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,

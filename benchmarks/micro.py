@@ -31,6 +31,100 @@ def _peaks():
     return bench.measured_peaks()
 
 
+def cfg3_measure(steps: int, warmup: int, peak64: float) -> dict:
+    """cfg3 pair kernels (2^14 x 2^14 x 16, fused U/T reduction), CUDA events."""
+    import torch
+
+    from paper_1212_3032_b200 import _lib
+    from paper_1212_3032_b200.workloads import UNIT, cfg3_inputs
+
+    lib = _lib.require_cuda()
+    x, tris, omegas, xv = cfg3_inputs()
+    P, M, F = len(x), len(tris), len(omegas)
+    xd = torch.from_numpy(x).cuda()
+    td = torch.from_numpy(tris.reshape(M, 9).copy()).cuda()
+    vd = torch.from_numpy(xv.copy()).cuda()
+    om = np.ascontiguousarray(np.stack([omegas.real, omegas.imag], axis=1))
+    yu = torch.empty((F, P, 3), dtype=torch.complex128, device="cuda")
+    yt = torch.empty_like(yu)
+    ws_bytes = int(lib.ewb_pair_kernels_workspace_bytes(P, M, F))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+
+    def step():
+        _lib.check(lib.ewb_pair_kernels_reduce(
+            _lib.ptr(xd), P, _lib.ptr(td), M, _lib.ptr(vd), om.ctypes.data, F, UNIT.lam,
+            UNIT.mu, UNIT.rho, _lib.ptr(yu), _lib.ptr(yt), _lib.ptr(ws), ws_bytes,
+            _lib.stream_handle()))
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    evals = float(P) * M * F
+    tf = evals / (ms * 1e-3) * PAIR_FLOPS / 1e12
+    return {"workload": f"cfg3: {P} points x {M} triangles x {F} omega, gauss7, fused U/T "
+                        "reduction", "metric": "element-pair kernel evals/s",
+            "value": evals / (ms * 1e-3), "unit": "pair-evals/s", "ms_per_launch": ms,
+            "roofline": {"bound": "fp64", "achieved": tf, "peak": peak64, "unit": "TFLOP/s",
+                         "frac": tf / peak64, "algorithmic_flops_per_launch": evals * PAIR_FLOPS,
+                         "peak_source": "measured DFMA probe"}}
+
+
+def cfg4_gemv_measure(n: int = 16384, batch: int = 8, reps: int = 5) -> dict:
+    """cfg4 batched complex128 GEMV (8 seeded diagonally dominant systems,
+    device-generated), CUDA events; HBM roofline."""
+    import torch
+
+    from paper_1212_3032_b200 import _lib
+
+    lib = _lib.require_cuda()
+    hbm = float(_peaks().get("hbm_gbs", 6650.0))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    A = torch.empty((batch, n, n), dtype=torch.complex128, device="cuda")
+    for s_ in range(batch):
+        A[s_] = torch.complex(torch.randn((n, n), generator=g, device="cuda", dtype=torch.float64),
+                              torch.randn((n, n), generator=g, device="cuda",
+                                          dtype=torch.float64)) / math.sqrt(2.0)
+        A[s_].diagonal().add_(3.0 * math.sqrt(n))
+    b = torch.complex(torch.randn((batch, n), generator=g, device="cuda", dtype=torch.float64),
+                      torch.randn((batch, n), generator=g, device="cuda", dtype=torch.float64))
+    y = torch.empty_like(b)
+
+    def step():
+        _lib.check(lib.ewb_gemv_batched(_lib.ptr(A), _lib.ptr(b), _lib.ptr(y), n, batch,
+                                        _lib.stream_handle()))
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    gbs = batch * (16.0 * n * n + 32.0 * n) / (ms * 1e-3) / 1e9
+    ref = A[batch - 1] @ b[batch - 1]
+    err = float((y[batch - 1] - ref).abs().max() / ref.abs().max())
+    del A, b, y
+    torch.cuda.empty_cache()
+    return {"workload": f"cfg4: batched dense complex128 matvec, {batch} systems, N={n}",
+            "metric": "complex matvec HBM GB/s", "value": gbs, "unit": "GB/s",
+            "ms_per_launch": ms, "relerr_vs_torch": err,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": gbs / hbm,
+                         "algorithmic_bytes_per_launch": batch * (16.0 * n * n + 32.0 * n),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}}
+
+
 def run_cfg3(args, rank, world, local_rank):
     import torch
 
