@@ -410,8 +410,10 @@ def test_cfg2_full_sweep_matches_reference_run(cuda):
     blocking of the dot products: 92 % and 90 % within 1, max 5 and 3).
     The e0_uz history is the one above 1e-6: the all-Neumann cavity operator
     (interior identity) has rigid-body near-null directions
-    whose tiny eigenvalues are set by the assembly's rounding, and a
-    z-translation shows up in e0_uz; the reference's two runs (identical
+    whose tiny eigenvalues are set by the assembly's rounding, and e0_uz is
+    a small component (element 0's normal has n_z = -0.034: max |e0_uz| =
+    0.11 against 3.1 for e0_uy), so a rigid z-drift far below the radial
+    response shows up there relative to it; the reference's two runs (identical
     matrices) agree there to 2e-8, any other assembly (ours, at 2.3e-15 of
     max|A|) lands at ~1.4e-6.
     Bars here: every history within 2e-6 (three of four within 1e-6), counts
