@@ -427,7 +427,7 @@ def run_ours_sweep(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_block(args.workload, cfg, ds.n_freq)
     cfg5_block = other_metrics = None
-    if rank == 0 and args.workload == "cfg2" and not args.no_cfg5:
+    if rank == 0 and world == 1 and args.workload == "cfg2" and not args.no_cfg5:
         del ds
         gc.collect()
         torch.cuda.empty_cache()
