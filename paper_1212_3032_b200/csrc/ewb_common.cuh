@@ -73,7 +73,6 @@ struct cplx {
   double re, im;
 };
 
-__host__ __device__ __forceinline__ cplx mk(double r, double i) { return cplx{r, i}; }
 __device__ __forceinline__ cplx operator+(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
 __device__ __forceinline__ cplx operator-(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
 __device__ __forceinline__ cplx operator-(cplx a) { return {-a.re, -a.im}; }
@@ -505,20 +504,6 @@ __device__ __forceinline__ void acc_point(Acc<S>& A, S Phi, S Psi, S Aw, S Bw, S
   madd(A.sa, dn, Aw);
   madd(A.va[0], dx, Aw); madd(A.va[1], dy, Aw); madd(A.va[2], dz, Aw);
   madd(A.vc[0], dx, Cw); madd(A.vc[1], dy, Cw); madd(A.vc[2], dz, Cw);
-}
-
-// One dynamic point: r, 1/r, unit d, dn, weight w.
-__device__ __forceinline__ void point_contract(Acc<cplx>& A, const FreqConst& fc,
-                                               const Brackets& f, double ir, double dx,
-                                               double dy, double dz, double dn, double w) {
-  double wr = w * ir, wr2 = wr * ir;
-  cplx Phi = wr * f.f0;
-  cplx Psi = wr * f.f1;
-  cplx Aw = wr2 * (f.f2 - f.f1);
-  cplx Bw = (2.0 * wr2 * dn) * (2.0 * f.f1 - f.f3);
-  cplx dd = f.f2 - f.f3;
-  cplx Cw = wr2 * (fc.ratio * (dd - 2.0 * f.f1) - 2.0 * (dd - f.f1));
-  acc_point(A, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
 }
 
 __device__ __forceinline__ void point_dynamic(Acc<cplx>& A, const FreqConst& fc, double r,

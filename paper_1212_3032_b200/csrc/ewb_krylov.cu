@@ -34,10 +34,6 @@ constexpr int kSolveMinBlocks = 1;
 constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kMaxRed = 16;  // doubles per grid reduction
 
-__device__ __forceinline__ cplx ldc(const cplx* p) {
-  double2 v = __ldcs(reinterpret_cast<const double2*>(p));  // streaming (evict-first)
-  return {v.x, v.y};
-}
 __device__ __forceinline__ cplx ldg(const cplx* p) {
   double2 v = *reinterpret_cast<const double2*>(p);
   return {v.x, v.y};
