@@ -748,3 +748,41 @@ def test_sem_deep_history_vs_oracle(cuda, K):
     got_m = sem_initial_guess(hist, op, b).cpu().numpy()
     assert rel_max(got_d, ref) <= 1e-8
     assert rel_max(got_m, ref) <= 1e-8
+
+
+def test_solver_rows_per_cta_capacity_rejected(cuda):
+    """ewb_gmres refuses (ValueError, no launch) a CTA budget whose rows per
+    CTA overflow the update phase's shared-memory scratch, instead of
+    overrunning it; the same size with enough CTAs solves."""
+    torch = cuda
+    from paper_1212_3032_b200 import _lib
+    from paper_1212_3032_b200.linsolve import gmres_device
+
+    lib = _lib.load()
+    cap = 12288                               # complex values the ring holds
+    n_bad = 2 * (cap // 2 - 2) + 16           # 2 CTAs: rows per CTA + 2 > cap / 2
+    a = torch.zeros((n_bad, n_bad), dtype=torch.complex128, device="cuda")
+    a.diagonal().fill_(2.0)
+    b = torch.ones(n_bad, dtype=torch.complex128, device="cuda")
+    x = torch.zeros_like(b)
+    try:
+        _lib.check(lib.ewb_set_solver_ctas(2))
+        with pytest.raises(ValueError, match="rows per solver CTA"):
+            gmres_device(a, b, x, False, 1e-8, 10, 100, None)
+    finally:
+        _lib.check(lib.ewb_set_solver_ctas(0))
+    st = gmres_device(a, b, x, False, 1e-8, 10, 100, None)
+    assert st.converged and rel_max(x.cpu().numpy(), 0.5 * np.ones(n_bad)) <= 1e-14
+
+
+def test_sem_depth_beyond_device_cap_rejected_up_front(cuda):
+    """A reference config may ask for any SEM depth; the device SEM keeps up to
+    8 columns and refuses a deeper one before any assembly or solve."""
+    from dataclasses import replace
+
+    from paper_1212_3032_b200.driver import MAX_SEM_DEPTH, DeviceSweep
+    from paper_1212_3032_b200.workloads import cfg1
+
+    cfg = replace(cfg1(n_omega=8, divisions=(2, 2, 2)), sem_depth=MAX_SEM_DEPTH + 1)
+    with pytest.raises(ValueError, match="sem_depth"):
+        DeviceSweep(cfg)
