@@ -690,49 +690,6 @@ constexpr size_t far_smem(int bd) {
 }
 constexpr size_t kFarMultiSmem = far_smem(128);
 
-// The five weighted scalars of one closed-form point straight from the
-// phase factors.  With D = E_s t_s - E_p t_p (t = -i/z - 1/z^2, the 1/z
-// terms of kernels.py:105-119), G_s = -i z_s E_s and G_p = -i z_p E_p, the
-// brackets are linear in (E_s, E_p, D, G_s, G_p):
-//   f0 = E_s + D,  f1 = E_s - E_p + 3D,  f2 = G_s - 2E_s + E_p - 3D,
-//   f3 = G_s - G_p - 4E_s + 4E_p - 9D,
-// and so are the weighted scalars of kernels.py:330-333 (wu, wt carry the
-// rule weight, 1/r and 1/(4 pi mu) or 1/(4 pi r^2); wb = 2 wt dn):
-//   Phi = wu f0,  Psi = wu f1,  Aw = wt (f2 - f1) = wt (G_s - 3E_s + 2E_p - 6D),
-//   Bw = wb (2f1 - f3) = wb (6(E_s - E_p) + 15D + G_p - G_s),
-//   Cw = wt (ratio (f2 - f3 - 2f1) - 2 (f2 - f3 - f1))
-//      = wt ((ratio - 2) G_p + (4 - ratio) E_p - 2E_s - 6D).
-// Same values as the factored brackets (brackets_closed with the phase
-// factors given) + the scalar formulas, rounding apart, with ~35 % fewer
-// FP64 instructions per point.
-struct Weighted5 {
-  cplx Phi, Psi, Aw, Bw, Cw;
-};
-__device__ __forceinline__ Weighted5 weights_phase(cplx ks, cplx kp, cplx iks, cplx ikp, double r,
-                                                   double ir, cplx Es, cplx Ep, double wu,
-                                                   double wt, double wb, double cr2, double c4r) {
-  const cplx qs = iks * ir, qp = ikp * ir;
-  const cplx qs2 = qs * qs, qp2 = qp * qp;
-  const cplx ts = {qs.im - qs2.re, -qs.re - qs2.im};
-  const cplx tp = {qp.im - qp2.re, -qp.re - qp2.im};
-  cplx D = Es * ts;
-  D.re = fma(-Ep.re, tp.re, fma(Ep.im, tp.im, D.re));
-  D.im = fma(-Ep.re, tp.im, fma(-Ep.im, tp.re, D.im));
-  const cplx Gs = Es * cplx{ks.im * r, -ks.re * r};
-  const cplx Gp = Ep * cplx{kp.im * r, -kp.re * r};
-  const cplx dE = Es - Ep;
-  Weighted5 w;
-  w.Phi = wu * (Es + D);
-  w.Psi = {wu * fma(c_num.three, D.re, dE.re), wu * fma(c_num.three, D.im, dE.im)};
-  w.Aw = {wt * fma(-c_num.six, D.re, fma(c_num.two, Ep.re, fma(-c_num.three, Es.re, Gs.re))),
-          wt * fma(-c_num.six, D.im, fma(c_num.two, Ep.im, fma(-c_num.three, Es.im, Gs.im)))};
-  w.Bw = {wb * fma(c_num.fifteen, D.re, fma(c_num.six, dE.re, Gp.re - Gs.re)),
-          wb * fma(c_num.fifteen, D.im, fma(c_num.six, dE.im, Gp.im - Gs.im))};
-  w.Cw = {wt * fma(-c_num.six, D.re, fma(-c_num.two, Es.re, fma(c4r, Ep.re, cr2 * Gp.re))),
-          wt * fma(-c_num.six, D.im, fma(-c_num.two, Es.im, fma(c4r, Ep.im, cr2 * Gp.im)))};
-  return w;
-}
-
 // exponent bits: all ones <=> Inf or NaN (integer pipe, not FP64)
 __device__ __forceinline__ unsigned expo(double v) {
   return (unsigned)__double2hiint(v) & 0x7ff00000u;
