@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EWB_ABI_VERSION 4
+#define EWB_ABI_VERSION 5
 
 enum ewb_status {
   EWB_OK = 0,
@@ -260,6 +260,15 @@ int ewb_matfree_apply(ewb_ctx* ctx, double omega_re, double omega_im, const void
                       const void* vu_dev, int32_t K, void* y_dev, const uint8_t* kinds_dev,
                       void* pinv_dev, void* workspace_dev, int64_t workspace_bytes,
                       const int32_t* gate_dev, void* stream);
+/* The same with per-vector masks: bit k of t_mask / u_mask clear = vt_k /
+ * vu_k is known to be zero and its block product is skipped (the K + 1
+ * vector pass of an all-Neumann frequency: b has vt = 0, SEM's columns vu = 0).
+ * Bits at or beyond K are rejected. */
+int ewb_matfree_apply_masked(ewb_ctx* ctx, double omega_re, double omega_im, const void* vt_dev,
+                             const void* vu_dev, int32_t K, uint32_t t_mask, uint32_t u_mask,
+                             void* y_dev, const uint8_t* kinds_dev, void* pinv_dev,
+                             void* workspace_dev, int64_t workspace_bytes,
+                             const int32_t* gate_dev, void* stream);
 
 /* Pair-kernel microbenchmark (BASELINE cfg3): P points x M triangles x F
  * frequencies with gauss7 on every pair (pair_geometry + integrated_blocks,

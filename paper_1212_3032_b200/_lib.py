@@ -26,14 +26,14 @@ EXPORTS = (
     "ewb_gmres_workspace_bytes", "ewb_gmres",
     "ewb_sem_workspace_bytes", "ewb_sem_guess", "ewb_sem_from_products",
     "ewb_opgmres_workspace_bytes", "ewb_opgmres_buffers", "ewb_opgmres_phase", "ewb_window_idft",
-    "ewb_matfree_workspace_bytes", "ewb_matfree_apply",
+    "ewb_matfree_workspace_bytes", "ewb_matfree_apply", "ewb_matfree_apply_masked",
     "ewb_pair_kernels_blocks", "ewb_pair_kernels_workspace_bytes",
     "ewb_pair_kernels_reduce", "ewb_fp64_peak_probe", "ewb_debug_checks",
     "ewb_math_selftest",
 )
 
 EWB_OK, EWB_ERR_INVALID, EWB_ERR_CUDA, EWB_ERR_NONFINITE = 0, 1, 2, 3
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class NativeUnavailable(RuntimeError):
@@ -90,6 +90,8 @@ _SIGS = {
     "ewb_window_idft": (I32, [P, I64, I64, I32, D, D, P, P, P]),
     "ewb_matfree_workspace_bytes": (I64, [P, I32]),
     "ewb_matfree_apply": (I32, [P, D, D, P, P, I32, P, P, P, P, I64, P, P]),
+    "ewb_matfree_apply_masked": (I32, [P, D, D, P, P, I32, ctypes.c_uint32, ctypes.c_uint32, P, P,
+                                       P, P, I64, P, P]),
     "ewb_pair_kernels_blocks": (I32, [P, I64, P, I64, P, I32, D, D, D, P, P, P]),
     "ewb_pair_kernels_workspace_bytes": (I64, [I64, I64, I32]),
     "ewb_pair_kernels_reduce": (I32, [P, I64, P, I64, P, P, I32, D, D, D, P, P, P, I64, P]),

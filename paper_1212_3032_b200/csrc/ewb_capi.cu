@@ -533,7 +533,7 @@ namespace ewb {
 size_t mf_workspace_bytes(const Context& c, int K);
 cudaError_t launch_matfree(Context& c, double ore, double oim, const cplx* vt, const cplx* vu,
                            int K, cplx* y, const uint8_t* kinds, cplx* pinv, void* ws,
-                           const int* gate, cudaStream_t s);
+                           const int* gate, cudaStream_t s, unsigned t_mask, unsigned u_mask);
 cudaError_t launch_pair_blocks(const double* x, long long P, const double* tri, long long M,
                                const FreqConst* fcs_dev, int F, const double* b7, const double* w7,
                                cplx* u, cplx* t, cudaStream_t s);
@@ -579,22 +579,35 @@ int64_t ewb_matfree_workspace_bytes(const ewb_ctx* ctx, int32_t K) {
   return (int64_t)ewb::mf_workspace_bytes(ctx->c, K);
 }
 
-int ewb_matfree_apply(ewb_ctx* ctx, double ore, double oim, const void* vt, const void* vu,
-                      int32_t K, void* y, const uint8_t* kinds, void* pinv, void* ws,
-                      int64_t ws_bytes, const int32_t* gate, void* stream) {
+int ewb_matfree_apply_masked(ewb_ctx* ctx, double ore, double oim, const void* vt,
+                             const void* vu, int32_t K, uint32_t t_mask, uint32_t u_mask, void* y,
+                             const uint8_t* kinds, void* pinv, void* ws, int64_t ws_bytes,
+                             const int32_t* gate, void* stream) {
   if (!ctx || !vt || !y || !ws) return fail(EWB_ERR_INVALID, "ewb_matfree_apply: null argument");
   if (K < 1 || K > 5) return fail(EWB_ERR_INVALID, "ewb_matfree_apply: K must be in [1, 5]");
   if (int rc = check_omega(ore, oim, "ewb_matfree_apply")) return rc;
   if (ws_bytes < (int64_t)ewb::mf_workspace_bytes(ctx->c, K))
     return fail(EWB_ERR_INVALID, "ewb_matfree_apply: workspace too small");
+  const uint32_t all = (1u << K) - 1u;
+  if ((t_mask & ~all) || (u_mask & ~all))
+    return fail(EWB_ERR_INVALID, "ewb_matfree_apply: mask bits beyond K");
   if (!gate) {  // a gated call may skip its work and must leave y alone
     EWB_CUDA(ewb::dbg_poison(ws, (size_t)ws_bytes, S(stream)), "ewb_matfree_apply");
     EWB_CUDA(ewb::dbg_poison(y, (size_t)K * 3 * ctx->c.n_e * 16, S(stream)), "ewb_matfree_apply");
   }
   EWB_CUDA(ewb::launch_matfree(ctx->c, ore, oim, (const ewb::cplx*)vt, (const ewb::cplx*)vu, K,
-                               (ewb::cplx*)y, kinds, (ewb::cplx*)pinv, ws, gate, S(stream)),
+                               (ewb::cplx*)y, kinds, (ewb::cplx*)pinv, ws, gate, S(stream),
+                               t_mask, u_mask),
            "ewb_matfree_apply");
   return EWB_OK;
+}
+
+int ewb_matfree_apply(ewb_ctx* ctx, double ore, double oim, const void* vt, const void* vu,
+                      int32_t K, void* y, const uint8_t* kinds, void* pinv, void* ws,
+                      int64_t ws_bytes, const int32_t* gate, void* stream) {
+  const uint32_t all = K >= 1 && K <= 5 ? (1u << K) - 1u : 0u;
+  return ewb_matfree_apply_masked(ctx, ore, oim, vt, vu, K, all, all, y, kinds, pinv, ws,
+                                  ws_bytes, gate, stream);
 }
 
 static int pair_prep(const double* omega_host, int32_t F, double lam, double mu, double rho,

@@ -77,6 +77,10 @@ struct MfArgs {
   int* flags;
   const int* gate;      // nullable: the application is skipped when *gate == 0
   int K, nchunk, chunk_cols;
+  // bit k clear: vt_k (t_mask) / vu_k (u_mask) is known to be zero and its
+  // product is skipped (b of an all-Neumann frequency has vt = 0, SEM's
+  // columns vu = 0: half the block applies of the K = 5 pass)
+  unsigned t_mask, u_mask;
 };
 #define EWB_MF_GATE \
   if (m.gate && *m.gate == 0) return;
@@ -193,8 +197,8 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        acc_apply_T(acc, nx, ny, nz, 1.0, s_vt[jj][k], y[k]);
-        if (USE_U) acc_apply_U(acc, 1.0, s_vu[jj][k], y[k]);
+        if ((m.t_mask >> k) & 1u) acc_apply_T(acc, nx, ny, nz, 1.0, s_vt[jj][k], y[k]);
+        if (USE_U && ((m.u_mask >> k) & 1u)) acc_apply_U(acc, 1.0, s_vu[jj][k], y[k]);
       }
     }
   }
@@ -242,9 +246,11 @@ __global__ void __launch_bounds__(128) k_mf_near(Geo g, Phys<true> ph, MfArgs m,
   if (lane != 0) return;
   for (int k = 0; k < K; ++k) {
     cplx vt[3], yk[3] = {{0, 0}, {0, 0}, {0, 0}};
-    for (int a = 0; a < 3; ++a) vt[a] = m.vt[(size_t)k * N + 3 * j + a];
-    acc_apply_T(acc, nx, ny, nz, ph.fc.inv4pi, vt, yk);
-    if (USE_U) {
+    if ((m.t_mask >> k) & 1u) {
+      for (int a = 0; a < 3; ++a) vt[a] = m.vt[(size_t)k * N + 3 * j + a];
+      acc_apply_T(acc, nx, ny, nz, ph.fc.inv4pi, vt, yk);
+    }
+    if (USE_U && ((m.u_mask >> k) & 1u)) {
       cplx vu[3];
       for (int a = 0; a < 3; ++a) vu[a] = m.vu[(size_t)k * N + 3 * j + a];
       acc_apply_U(acc, ph.fc.inv4pimu, vu, yk);
@@ -332,8 +338,8 @@ __global__ void __launch_bounds__(128) k_mf_self(Geo g, Phys<true> ph, MfArgs m)
     for (int a = 0; a < 3; ++a) {
       cplx s = {0.0, 0.0};
       for (int b = 0; b < 3; ++b) {
-        cfma(s, T[a][b], m.vt[(size_t)k * N + 3 * j + b]);
-        if (USE_U) cfma(s, U[a][b], m.vu[(size_t)k * N + 3 * j + b]);
+        if ((m.t_mask >> k) & 1u) cfma(s, T[a][b], m.vt[(size_t)k * N + 3 * j + b]);
+        if (USE_U && ((m.u_mask >> k) & 1u)) cfma(s, U[a][b], m.vu[(size_t)k * N + 3 * j + b]);
       }
       m.y[(size_t)k * N + 3 * j + a] = yk[a] + s;
     }
@@ -385,13 +391,14 @@ size_t mf_workspace_bytes(const Context& c, int K) {
 
 cudaError_t launch_matfree(Context& c, double ore, double oim, const cplx* vt, const cplx* vu,
                            int K, cplx* y, const uint8_t* kinds, cplx* pinv, void* ws,
-                           const int* gate, cudaStream_t s) {
+                           const int* gate, cudaStream_t s, unsigned t_mask, unsigned u_mask) {
   cudaError_t e = upload_series(s);
   if (e) return e;
   Phys<true> ph{freq_const(c, ore, oim)};
   MfArgs m{};
   m.vt = vt; m.vu = vu; m.y = y; m.kinds = kinds; m.pinv = pinv;
   m.diag_base = c.diag_base; m.flags = c.flags; m.K = K; m.gate = gate;
+  m.t_mask = t_mask; m.u_mask = u_mask;
   m.nchunk = mf_chunks(c);
   m.chunk_cols = (c.n_e + m.nchunk - 1) / m.nchunk;
   size_t N = 3 * (size_t)c.n_e;

@@ -59,7 +59,7 @@ class MatrixFreeOperator:
         return self._ws
 
     # y_k = T vt_k + U vu_k, passes of up to MAX_K vectors
-    def _apply_tu(self, vt, vu, want_pinv: bool = False):
+    def _apply_tu(self, vt, vu, want_pinv: bool = False, masks=None):
         torch = _torch()
         K = int(vt.shape[0])
         if K < 1:
@@ -78,11 +78,13 @@ class MatrixFreeOperator:
             if self.pinv is None:
                 self.pinv = torch.empty((self.n // 3, 3, 3), dtype=torch.complex128, device="cuda")
             pinv = self.pinv
-        _lib.check(lib.ewb_matfree_apply(
+        full = (1 << K) - 1
+        t_mask, u_mask = masks if masks is not None else (full, full)
+        _lib.check(lib.ewb_matfree_apply_masked(
             self.asm.ctx, self.omega.real, self.omega.imag, _lib.ptr(vt),
-            _lib.ptr(vu) if vu is not None else None, K, _lib.ptr(y), _lib.ptr(self.kinds_dev),
-            _lib.ptr(pinv) if pinv is not None else None, _lib.ptr(ws), ws.numel(), None,
-            _lib.stream_handle()), "ewb_matfree_apply")
+            _lib.ptr(vu) if vu is not None else None, K, t_mask, u_mask, _lib.ptr(y),
+            _lib.ptr(self.kinds_dev), _lib.ptr(pinv) if pinv is not None else None,
+            _lib.ptr(ws), ws.numel(), None, _lib.stream_handle()), "ewb_matfree_apply")
         self.applications += 1
         return y
 
@@ -126,10 +128,15 @@ class MatrixFreeOperator:
             y = self._apply_tu(bt.contiguous(), bu.contiguous(), want_pinv)
             return y[0], None
         vt, vu = self._split(V)
+        masks = None
         if vu is None:
+            # all-Neumann: the history columns have no U part and b no T part
             vu = torch.zeros_like(vt)
+            k = int(V.shape[0])
+            if k + 1 <= self.MAX_K:
+                masks = ((1 << k) - 1, 1 << k)
         y = self._apply_tu(torch.cat([vt, bt]).contiguous(), torch.cat([vu, bu]).contiguous(),
-                           want_pinv)
+                           want_pinv, masks)
         return y[-1], y[:-1]
 
     def block_preconditioner(self):
