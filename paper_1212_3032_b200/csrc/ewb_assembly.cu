@@ -678,6 +678,10 @@ __device__ __forceinline__ cplx unit_phase(double a) {
 #ifndef EWB_FARMULTI_MINB
 #define EWB_FARMULTI_MINB 3
 #endif
+#ifndef EWB_FARMULTI_THREADS
+#define EWB_FARMULTI_THREADS 128
+#endif
+constexpr int kFarThreads = EWB_FARMULTI_THREADS;
 #ifndef EWB_FAR_QUNROLL
 #define EWB_FAR_QUNROLL 3
 #endif
@@ -688,7 +692,7 @@ constexpr size_t far_smem(int bd) {
   return sizeof(double) * (kFarGeo * 3 * bd + 4 * 3 * 2 * bd) + sizeof(FreqConst) * kMaxBatch +
          sizeof(double) * (bd / 32) * 6 * kBredStride;
 }
-constexpr size_t kFarMultiSmem = far_smem(128);
+constexpr size_t kFarMultiSmem = far_smem(kFarThreads);
 
 // exponent bits: all ones <=> Inf or NaN (integer pipe, not FP64)
 __device__ __forceinline__ unsigned expo(double v) {
@@ -696,8 +700,11 @@ __device__ __forceinline__ unsigned expo(double v) {
 }
 __device__ __forceinline__ unsigned expo(cplx v) { return max(expo(v.re), expo(v.im)); }
 
-template <bool RECUR>
-__global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
+// SER = false: the host proved no far pair of the batch can reach the series
+// branch (min |k_s| x the far-pair distance bound >= the switch, make_batch),
+// so the kernel carries no out-of-line series call (fewer live registers).
+template <bool RECUR, bool SER>
+__global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
                                                                       SysBatch o) {
   extern __shared__ double sm_far[];
   const int BD = blockDim.x;
@@ -793,7 +800,7 @@ __global__ void __launch_bounds__(128, EWB_FARMULTI_MINB) k_far_multi(Geo g, Fre
             }
             const double wb = wt * dn2;
             Weighted5 w;
-            if (lds_d(&sfc[f].ks_abs) * rr < c_num.far_sw) {
+            if (SER && lds_d(&sfc[f].ks_abs) * rr < c_num.far_sw) {
               FreqConst fc = fc0;
               fc.ks = ks; fc.kp = kp; fc.g2 = lds_c(&sfc[f].g2);
               const Brackets br = brackets_series_cold(fc, rr);
@@ -1199,6 +1206,7 @@ cudaError_t setup_context(Context& c, const double* centroids, const double* nor
     }
     soa[(size_t)6 * n + e] = areas[e];
     soa[(size_t)7 * n + e] = diameters[e];
+    c.min_diam = e == 0 ? diameters[e] : fmin(c.min_diam, diameters[e]);
     for (int v = 0; v < 3; ++v)
       for (int k = 0; k < 3; ++k)  // vx block: [v][e]; vy, vz likewise
         soa[(size_t)(8 + 3 * k + v) * n + e] = corners[9 * e + 3 * v + k];
@@ -1430,14 +1438,29 @@ static cudaError_t ensure_multi_scratch(Context& c, int nf) {
 static void far_attrs() {
   static bool attr = false;
   if (attr) return;
-  cudaFuncSetAttribute(k_far_multi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_far_multi<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kFarMultiSmem);
-  cudaFuncSetAttribute(k_far_multi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_far_multi<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kFarMultiSmem);
+  cudaFuncSetAttribute(k_far_multi<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kFarMultiSmem);
+  cudaFuncSetAttribute(k_far_multi<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)kFarMultiSmem);
   attr = true;
 }
 
 static FreqBatch make_batch(Context& c, int nf, const double* ore, const double* oim);
+
+// True when no far pair of the batch can take the series branch: a far pair
+// has |c_i - c_j| >= 4 d_j (exact_tier) and every quadrature point of
+// element j lies within (2/3) d_j of its centroid (d_j = longest edge), so
+// r >= 3 d_j >= 3 min_j d_j; with a margin for rounding, 2.9 min d.  The
+// branch condition |k_s| r < kFarSwitch is then false for every point.
+static bool series_free(const Context& c, const FreqBatch& fb) {
+  double ks_min = fb.fc[0].ks_abs;
+  for (int f = 1; f < fb.nf; ++f) ks_min = fmin(ks_min, fb.fc[f].ks_abs);
+  return c.min_diam > 0.0 && ks_min * (2.9 * c.min_diam) >= kFarSwitch;
+}
 static cudaError_t launch_multi_rest(Context& c, const FreqBatch& fb, const SysBatch& o,
                                      cudaStream_t s);
 
@@ -1460,12 +1483,17 @@ cudaError_t launch_assemble_system_multi(Context& c, int nf, const double* ore,
   SysBatch o{kinds, prescribed, A, b, pinv, flags, c.bpart_m, c.bmid_m, c.bnear_m};
   const int n = c.n_e;
   const long long warps = (long long)((n + kFarRows - 1) / kFarRows) * c.n_tiles;
-  const unsigned fb_blocks = blocks_for(warps * 32, 128);
+  const unsigned fb_blocks = blocks_for(warps * 32, kFarThreads);
   far_attrs();
-  if (recur)
-    EWB_NOTE k_far_multi<true><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
+  const bool ser = !series_free(c, fb);
+  if (recur && ser)
+    EWB_NOTE k_far_multi<true, true><<<fb_blocks, kFarThreads, kFarMultiSmem, s>>>(c.g, fb, o);
+  else if (recur)
+    EWB_NOTE k_far_multi<true, false><<<fb_blocks, kFarThreads, kFarMultiSmem, s>>>(c.g, fb, o);
+  else if (ser)
+    EWB_NOTE k_far_multi<false, true><<<fb_blocks, kFarThreads, kFarMultiSmem, s>>>(c.g, fb, o);
   else
-    EWB_NOTE k_far_multi<false><<<fb_blocks, 128, kFarMultiSmem, s>>>(c.g, fb, o);
+    EWB_NOTE k_far_multi<false, false><<<fb_blocks, kFarThreads, kFarMultiSmem, s>>>(c.g, fb, o);
   return launch_multi_rest(c, fb, o, s);
 }
 

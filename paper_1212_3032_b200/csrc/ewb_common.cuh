@@ -589,12 +589,15 @@ __device__ __forceinline__ Weighted5 weights_brackets(const Brackets& f, double 
 // One dynamic point with the block constants folded into the weights:
 // wu = w / (4 pi mu r), wt = w / (4 pi r^2); series below |k_s r| < sw taken
 // out of line.  The accumulators then hold U and T contributions directly.
+// SER = false: the caller proved |k_s| r >= sw for every point it passes
+// (no out-of-line series call in the kernel, fewer live registers).
+template <bool SER = true>
 __device__ __forceinline__ void point_dynamic_scaled(Acc<cplx>& A, const FreqConst& fc,
                                                      double sw, double r, double ir, double dx,
                                                      double dy, double dz, double dn, double wu,
                                                      double wt) {
   const Brackets f =
-      fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
+      SER && fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
   const cplx Phi = wu * f.f0;
   const cplx Psi = wu * f.f1;
   const cplx Aw = wt * (f.f2 - f.f1);
@@ -610,6 +613,7 @@ __device__ __forceinline__ void point_dynamic_scaled(Acc<cplx>& A, const FreqCon
 //   (T v)_a += e v_a + n_a h + d_a g,   e = Aw dn, h = Aw s, g = Bw s + Cw nv
 // (~44 DP instead of 40 accumulator updates plus a third of a block apply),
 // and no 20-word accumulator is live: far fewer registers per thread.
+template <bool SER = true>
 __device__ __forceinline__ void point_apply_T(cplx y[3], const FreqConst& fc, double sw, double r,
                                               double ir, double dx, double dy, double dz,
                                               double dn, double wt, const cplx v[3], cplx nv,
@@ -617,7 +621,7 @@ __device__ __forceinline__ void point_apply_T(cplx y[3], const FreqConst& fc, do
   // (the linear-basis weights measured 1-4 % slower here at low frequency:
   // this product keeps the bracket form)
   const Brackets f =
-      fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
+      SER && fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
   const cplx Aw = wt * (f.f2 - f.f1);
   const cplx Bw = (c_num.two * wt * dn) * (c_num.two * f.f1 - f.f3);
   const cplx dd = f.f2 - f.f3;

@@ -147,6 +147,7 @@ struct Context {
   long long n_far = 0, n_mid = 0;    // off-diagonal pair counts per tier
   long long n_near_lvl[kMaxNearLevel + 1] = {0, 0, 0, 0, 0};
   double lam = 0, mu = 0, rho = 0;
+  double min_diam = 0;               // shortest longest-edge (far-pair distance bound)
   int exterior = 0;                  // 1: c + PV int T = I diagonal
   Geo g{};
   // owned device buffers

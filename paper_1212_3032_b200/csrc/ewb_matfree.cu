@@ -19,6 +19,7 @@
 // and the self term (warp per element): deterministic, no atomics.
 #include <cuda_runtime.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "ewb_ctx.cuh"
@@ -96,7 +97,10 @@ constexpr int kMfQUnroll = EWB_MF_QUNROLL;
 #ifndef EWB_MF1_MINB
 #define EWB_MF1_MINB 4
 #endif
-template <int K, bool USE_U>
+// SER = false: no far pair of this application can reach the series branch
+// (mf_launch checks |k_s| x the far-pair distance bound, as series_free in
+// ewb_assembly.cu); mid pairs always keep the check.
+template <int K, bool USE_U, bool SER>
 __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_MF_MINB)
     k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
   EWB_MF_GATE
@@ -157,28 +161,30 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
         cplx nv = nx * v[0];
         axpy(nv, ny, v[1]);
         axpy(nv, nz, v[2]);
-        auto point1 = [&](const double* yq, double wq) {
+        auto point1 = [&](const double* yq, double wq, auto ser) {
           double dx = yq[0] - xi, dy = yq[1] - yi, dz = yq[2] - zi;
           const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
           const double ir = rsqrt(r2);
           const double r = r2 * ir;
           dx *= ir; dy *= ir; dz *= ir;
           const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-          point_apply_T(y[0], ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn, wq * ir * ir * ct, v,
-                        nv, nx, ny, nz);
+          point_apply_T<decltype(ser)::value>(y[0], ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn,
+                                              wq * ir * ir * ct, v, nv, nx, ny, nz);
         };
         if (tier == 0) {
 #pragma unroll kMfQUnroll
-          for (int q = 0; q < 3; ++q) point1(&s_y[jj][3 * q], g.wfar[q]);
+          for (int q = 0; q < 3; ++q)
+            point1(&s_y[jj][3 * q], g.wfar[q], std::integral_constant<bool, SER>{});
         } else {
 #pragma unroll 1
-          for (int q = 0; q < 7; ++q) point1(&s_y[jj][9 + 3 * q], g.wmid[q]);
+          for (int q = 0; q < 7; ++q)
+            point1(&s_y[jj][9 + 3 * q], g.wmid[q], std::true_type{});
         }
         continue;
       }
       Acc<cplx> acc;
       acc_zero(acc);
-      auto point = [&](const double* yq, double wq) {
+      auto point = [&](const double* yq, double wq, auto ser) {
         double dx = yq[0] - xi, dy = yq[1] - yi, dz = yq[2] - zi;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const double ir = rsqrt(r2);
@@ -186,14 +192,16 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
         dx *= ir; dy *= ir; dz *= ir;
         const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
         const double wi = wq * ir;
-        point_dynamic_scaled(acc, ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn, wi * cu, wi * ir * ct);
+        point_dynamic_scaled<decltype(ser)::value>(acc, ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn,
+                                                   wi * cu, wi * ir * ct);
       };
       if (tier == 0) {
 #pragma unroll kMfQUnroll
-        for (int q = 0; q < 3; ++q) point(&s_y[jj][3 * q], g.wfar[q]);
+        for (int q = 0; q < 3; ++q)
+          point(&s_y[jj][3 * q], g.wfar[q], std::integral_constant<bool, SER>{});
       } else {
 #pragma unroll 1
-        for (int q = 0; q < 7; ++q) point(&s_y[jj][9 + 3 * q], g.wmid[q]);
+        for (int q = 0; q < 7; ++q) point(&s_y[jj][9 + 3 * q], g.wmid[q], std::true_type{});
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -366,7 +374,11 @@ static cudaError_t mf_launch(Context& c, Phys<true> ph, MfArgs m, cudaStream_t s
   dim3 grid((n + 127) / 128, m.nchunk);
   Phys<true> phf = ph;
   phf.fc.sw = kFarSwitch;
-  EWB_NOTE k_mf_farmid<K, USE_U><<<grid, 128, 0, s>>>(c.g, phf, m);
+  // far pairs: r >= 3 d_j >= 2.9 min d (series_free, ewb_assembly.cu)
+  if (c.min_diam > 0.0 && ph.fc.ks_abs * (2.9 * c.min_diam) >= kFarSwitch)
+    EWB_NOTE k_mf_farmid<K, USE_U, false><<<grid, 128, 0, s>>>(c.g, phf, m);
+  else
+    EWB_NOTE k_mf_farmid<K, USE_U, true><<<grid, 128, 0, s>>>(c.g, phf, m);
   if (c.n_near)
     EWB_NOTE k_mf_near<K, USE_U><<<(c.n_near * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m, c.n_near);
   EWB_NOTE k_mf_self<K, USE_U><<<(n * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m);
