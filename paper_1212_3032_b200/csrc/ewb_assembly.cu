@@ -251,13 +251,14 @@ __device__ __forceinline__ void sys_block(const SysArgs& s, long long N, int i, 
     cplx* row = s.A + (size_t)(3 * i + a) * N + 3 * j;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      if (kd[c] == kDirichlet) {
-        row[c] = -U[a][c];
-        bc[a] = bc[a] - T[a][c] * pv[c];
-      } else {
-        row[c] = T[a][c];
-        bc[a] = bc[a] + U[a][c] * pv[c];
-      }
+      // branch-free (selects, no divergent branch per entry): with nu = -U
+      // the stored entry is (Dirichlet ? nu : T) and b -= (Dirichlet ? T : nu) p
+      const bool dir = kd[c] == kDirichlet;
+      const cplx nu = -U[a][c], tv = T[a][c];
+      const cplx st = {dir ? nu.re : tv.re, dir ? nu.im : tv.im};
+      const cplx ml = {dir ? tv.re : nu.re, dir ? tv.im : nu.im};
+      *reinterpret_cast<double2*>(row + c) = make_double2(st.re, st.im);
+      cfma(bc[a], ml, -pv[c]);
     }
   }
 }
@@ -774,10 +775,19 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
       for (int f = 0; f < nf; ++f) {
         cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
         if (far) {
-          // prescribed values of this member, loaded ahead of the quadrature loop
+          // prescribed values of this member (16-byte loads; the next member's
+          // were pulled into L1 one iteration ago, so this is not an L2 wait)
+          const cplx* pcol = o.p + (size_t)f * N + 3 * j;
+          if (f + 1 < nf) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pcol + N));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pcol + N + 2));
+          }
           cplx pv[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) pv[c] = o.p[(size_t)f * N + 3 * j + c];
+          for (int c = 0; c < 3; ++c) {
+            const double2 v2 = *reinterpret_cast<const double2*>(pcol + c);
+            pv[c] = {v2.x, v2.y};
+          }
           Acc<cplx> acc;
           acc_zero(acc);
           const double ratio = fc0.ratio;
@@ -787,7 +797,8 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
             const double dx = SG(2, q), dy = SG(3, q), dz = SG(4, q);
             const double dn2 = SG(5, q), wu = SG(6, q), wt = SG(7, q);
             const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
-            const cplx iks = lds_c(&sfc[f].iks), ikp = lds_c(&sfc[f].ikp);
+            const cplx ts = t_closed(lds_c(&sfc[f].tas), lds_c(&sfc[f].tbs), ir);
+            const cplx tp = t_closed(lds_c(&sfc[f].tap), lds_c(&sfc[f].tbp), ir);
             cplx Es, Ep;
             if (RECUR) {
               Es = SP(0, q);
@@ -812,7 +823,7 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
               const cplx dd = br.f2 - br.f3;
               w.Cw = wt * (ratio * (dd - c_num.two * br.f1) - c_num.two * (dd - br.f1));
             } else {
-              w = weights_phase(ks, kp, iks, ikp, rr, ir, Es, Ep, wu, wt, wb, fb.cr2, fb.c4r);
+              w = weights_phase(ks, kp, ts, tp, rr, Es, Ep, wu, wt, wb, fb.cr2, fb.c4r);
             }
             // sa accumulates (2 d.n) Aw: halved exactly after the loop
             acc_point(acc, w.Phi, w.Psi, w.Aw, w.Bw, w.Cw, dx, dy, dz, dn2);
@@ -821,7 +832,9 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
           // blocks (kernels.py:336-356) entry by entry straight into A and b:
           // U_ac = su d_ac - P_ac, T_ac = B_ac + n_a va_c + vc_a n_c + sa d_ac;
           // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
-          // Dirichlet column A = -U, b -= T p
+          // Dirichlet column A = -U, b -= T p.  Branch-free: with nu = -U the
+          // stored entry is (Dirichlet ? nu : T) and b -= (Dirichlet ? T : nu) p
+          // (selects on the integer pipe instead of a divergent branch per entry)
           const double n[3] = {nx, ny, nz};
           const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
           unsigned ex = 0;
@@ -832,19 +845,17 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
             cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-              const cplx u = a == c ? acc.su - acc.P[sym[a][c]] : -acc.P[sym[a][c]];
+              const cplx nu = a == c ? acc.P[sym[a][c]] - acc.su : acc.P[sym[a][c]];
               cplx tv = acc.B[sym[a][c]];
               madd(tv, n[a], acc.va[c]);
               madd(tv, n[c], acc.vc[a]);
               if (a == c) tv = tv + acc.sa;
-              ex = max(ex, max(expo(u), expo(tv)));
-              if (kbits & (1u << c)) {
-                row[c] = -u;
-                bc[a] = bc[a] - tv * pv[c];
-              } else {
-                row[c] = tv;
-                bc[a] = bc[a] + u * pv[c];
-              }
+              ex = max(ex, max(expo(nu), expo(tv)));
+              const bool dir = kbits & (1u << c);
+              const cplx st = {dir ? nu.re : tv.re, dir ? nu.im : tv.im};
+              const cplx ml = {dir ? tv.re : nu.re, dir ? tv.im : nu.im};
+              *reinterpret_cast<double2*>(row + c) = make_double2(st.re, st.im);
+              cfma(bc[a], ml, -pv[c]);
             }
           }
           if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
@@ -908,7 +919,8 @@ __global__ void __launch_bounds__(128, 3) k_mid_multi(Geo g, FreqBatch fb, SysBa
     const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
     FreqConst fc;
     fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
-    fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+    fc.tas = lds_c(&sfc[f].tas); fc.tbs = lds_c(&sfc[f].tbs);
+    fc.tap = lds_c(&sfc[f].tap); fc.tbp = lds_c(&sfc[f].tbp);
     fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
     fc.ratio = fc0.ratio;
     const double wi = g.wmid[q] * ir;
@@ -1020,7 +1032,8 @@ __global__ void __launch_bounds__(128, 3) k_near_multi(Geo g, FreqBatch fb, SysB
       const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
       FreqConst fc;
       fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
-      fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+      fc.tas = lds_c(&sfc[f].tas); fc.tbs = lds_c(&sfc[f].tbs);
+    fc.tap = lds_c(&sfc[f].tap); fc.tbp = lds_c(&sfc[f].tbp);
       fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
       fc.ratio = fc0.ratio;
       const double wi = wq[q] * ir;
@@ -1083,7 +1096,8 @@ __global__ void __launch_bounds__(128, 3) k_self_multi(Geo g, FreqBatch fb, SysB
       const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
       FreqConst fc;
       fc.ks = lds_c(&sfc[f].ks); fc.kp = lds_c(&sfc[f].kp);
-      fc.iks = lds_c(&sfc[f].iks); fc.ikp = lds_c(&sfc[f].ikp);
+      fc.tas = lds_c(&sfc[f].tas); fc.tbs = lds_c(&sfc[f].tbs);
+    fc.tap = lds_c(&sfc[f].tap); fc.tbp = lds_c(&sfc[f].tbp);
       fc.g2 = lds_c(&sfc[f].g2); fc.ks_abs = lds_d(&sfc[f].ks_abs);
       fc.ratio = fc0.ratio;
       const double wi = y.w * ir;
@@ -1167,8 +1181,11 @@ FreqConst freq_const(const Context& c, double ore, double oim) {
     }
     return r;
   };
-  f.iks = cdiv_h({1.0, 0.0}, f.ks);
-  f.ikp = cdiv_h({1.0, 0.0}, f.kp);
+  const cplx iks = cdiv_h({1.0, 0.0}, f.ks), ikp = cdiv_h({1.0, 0.0}, f.kp);
+  f.tas = {iks.im, -iks.re};                                                    // -i / k_s
+  f.tbs = {-(iks.re * iks.re - iks.im * iks.im), -(2.0 * iks.re * iks.im)};     // -1 / k_s^2
+  f.tap = {ikp.im, -ikp.re};
+  f.tbp = {-(ikp.re * ikp.re - ikp.im * ikp.im), -(2.0 * ikp.re * ikp.im)};
   cplx q = cdiv_h(f.kp, f.ks);
   f.g2 = {q.re * q.re - q.im * q.im, q.re * q.im + q.im * q.re};
   f.ks_abs = hypot(f.ks.re, f.ks.im);

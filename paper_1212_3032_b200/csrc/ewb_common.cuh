@@ -104,11 +104,24 @@ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   }
 }
 
+// t = -i/z - 1/z^2 = ir (ta + tb ir): two FMA + two MUL per wave
+__device__ __forceinline__ cplx t_closed(cplx ta, cplx tb, double ir) {
+  return {fma(tb.re, ir, ta.re) * ir, fma(tb.im, ir, ta.im) * ir};
+}
+// the same with ir2 = ir^2 given: one constant operand per instruction (a
+// DFMA takes a single constant-bank operand), for kernels whose frequency
+// constants are kernel parameters
+__device__ __forceinline__ cplx t_closed2(cplx ta, cplx tb, double ir, double ir2) {
+  return {fma(ta.re, ir, tb.re * ir2), fma(ta.im, ir, tb.im * ir2)};
+}
+
 // Per-frequency constants (host-computed exactly as kernels.py:56-77 and
 // material.py:83-94 do, then passed by value).
 struct FreqConst {
   cplx ks, kp;          // omega / c_s, omega / c_p
-  cplx iks, ikp;        // 1 / ks, 1 / kp
+  // t = -i/z - 1/z^2 of the closed form (kernels.py:105-119) with z = k r:
+  // t = (ta + tb / r) / r,  ta = -i / k,  tb = -1 / k^2  (host constants)
+  cplx tas, tbs, tap, tbp;
   cplx g2;              // (kp / ks)^2   (kernels.py:75)
   double ks_abs;        // |ks| : |z_s| = |ks| r decides the series branch
   double sw;            // series below |z_s| < sw (reference: 0.35, kernels.py:36)
@@ -171,7 +184,7 @@ __device__ __forceinline__ double lds_d(const double* p) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
   return v;
 }
-// (FreqConst is 8-byte aligned with a 120-byte stride: two scalar loads)
+// (FreqConst is 8-byte aligned with a 152-byte stride: two scalar loads)
 __device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), lds_d(&p->im)}; }
 
 // FP64 literals of the hot loops as constant-bank operands: a 64-bit
@@ -207,10 +220,8 @@ __device__ __forceinline__ Brackets brackets_phase(const FreqConst& fc, double r
   double zs_re = fc.ks.re * r, zs_im = fc.ks.im * r;
   double zp_re = fc.kp.re * r, zp_im = fc.kp.im * r;
   cplx Ep = fc.g2 * ep;
-  cplx qs = fc.iks * ir, qp = fc.ikp * ir;      // 1/z
-  cplx qs2 = qs * qs, qp2 = qp * qp;
-  cplx ts = {qs.im - qs2.re, -qs.re - qs2.im};
-  cplx tp = {qp.im - qp2.re, -qp.re - qp2.im};
+  const double ir2 = ir * ir;
+  const cplx ts = t_closed2(fc.tas, fc.tbs, ir, ir2), tp = t_closed2(fc.tap, fc.tbp, ir, ir2);
   cplx Fs = Es * ts, Fp = Ep * tp;
   cplx Gs = Es * cplx{zs_im, -zs_re};
   cplx Gp = Ep * cplx{zp_im, -zp_re};
@@ -305,6 +316,103 @@ __device__ __forceinline__ double fast_exp(double x) {
   return p * __hiloint2double((k2 + 1023) << 20, 0);
 }
 
+// N arguments in lockstep: the same arithmetic as fast_sincos / fast_exp per
+// argument (bit-identical results), written so that each polynomial
+// coefficient feeds N independent FMA chains back to back — one constant
+// fetch instead of N, and N-way instruction-level parallelism on the
+// dependent Horner steps.
+template <int N>
+__device__ __forceinline__ void fast_sincos_n(const double (&x)[N], double (&sp)[N],
+                                              double (&cp)[N]) {
+  bool big = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) big |= !(fabs(x[i]) <= c_math.sincos_big);
+  if (big) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) sincos_large(x[i], &sp[i], &cp[i]);
+    return;
+  }
+  double r[N], z[N], ps[N], pc[N];
+  int q[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double t = fma(x[i], c_math.two_over_pi, c_math.magic);
+    const double kd = t - c_math.magic;
+    q[i] = __double2loint(t);
+    r[i] = fma(-kd, c_math.pio2_1, x[i]);
+    r[i] = fma(-kd, c_math.pio2_2, r[i]);
+    r[i] = fma(-kd, c_math.pio2_3, r[i]);
+    z[i] = r[i] * r[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) ps[i] = fma(z[i], c_math.s[5], c_math.s[4]);
+#pragma unroll
+  for (int m = 3; m >= 0; --m)
+#pragma unroll
+    for (int i = 0; i < N; ++i) ps[i] = fma(z[i], ps[i], c_math.s[m]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) pc[i] = fma(z[i], c_math.c[5], c_math.c[4]);
+#pragma unroll
+  for (int m = 3; m >= 0; --m)
+#pragma unroll
+    for (int i = 0; i < N; ++i) pc[i] = fma(z[i], pc[i], c_math.c[m]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double sn = fma(r[i] * z[i], ps[i], r[i]);
+    const double cs = c_math.e[13] + fma(z[i] * z[i], pc[i], -c_math.half * z[i]);
+    const bool swap = q[i] & 1;
+    sp[i] = flip_sign(swap ? cs : sn, (q[i] >> 1) & 1);
+    cp[i] = flip_sign(swap ? sn : cs, ((q[i] + 1) >> 1) & 1);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void fast_exp_n(const double (&x)[N], double (&e)[N]) {
+  double r[N], p[N];
+  int k[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double xd = x[i] < c_math.exp_lo ? c_math.exp_lo : x[i];   // NaN passes through
+    xd = xd > c_math.exp_hi ? c_math.exp_hi : xd;
+    const double t = fma(xd, c_math.log2e, c_math.magic);
+    const double kd = t - c_math.magic;
+    k[i] = __double2loint(t);
+    r[i] = fma(-kd, c_math.ln2_hi, xd);
+    r[i] = fma(-kd, c_math.ln2_lo, r[i]);
+    p[i] = fma(c_math.e[0], r[i], c_math.e[1]);
+  }
+#pragma unroll
+  for (int m = 2; m < 14; ++m)
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[i] = fma(p[i], r[i], c_math.e[m]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const int k1 = k[i] >> 1, k2 = k[i] - k1;
+    e[i] = (p[i] * __hiloint2double((k1 + 1023) << 20, 0)) * __hiloint2double((k2 + 1023) << 20, 0);
+  }
+}
+
+// The S and P phase factors of NP points: E_s = e^{-i k_s r}, e_p = e^{-i k_p r}.
+template <int NP>
+__device__ __forceinline__ void phase_factors_n(cplx ks, cplx kp, const double (&r)[NP],
+                                                cplx (&Es)[NP], cplx (&ep)[NP]) {
+  double xa[2 * NP], xe[2 * NP], s[2 * NP], c[2 * NP], m[2 * NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    xa[2 * i] = ks.re * r[i];
+    xa[2 * i + 1] = kp.re * r[i];
+    xe[2 * i] = ks.im * r[i];
+    xe[2 * i + 1] = kp.im * r[i];
+  }
+  fast_sincos_n<2 * NP>(xa, s, c);
+  fast_exp_n<2 * NP>(xe, m);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    Es[i] = {m[2 * i] * c[2 * i], -m[2 * i] * s[2 * i]};
+    ep[i] = {m[2 * i + 1] * c[2 * i + 1], -m[2 * i + 1] * s[2 * i + 1]};
+  }
+}
+
 // e^{-i k r} = e^{Im(k) r} (cos(Re(k) r) - i sin(Re(k) r))
 __device__ __forceinline__ cplx phase_factor(cplx k, double r) {
   double s, c;
@@ -314,31 +422,11 @@ __device__ __forceinline__ cplx phase_factor(cplx k, double r) {
 }
 
 __device__ __forceinline__ Brackets brackets_closed(const FreqConst& fc, double r, double ir) {
-  // z = k r ;  -i z = (k.im r) - i (k.re r)
-  double zs_re = fc.ks.re * r, zs_im = fc.ks.im * r;
-  double zp_re = fc.kp.re * r, zp_im = fc.kp.im * r;
-  double ss, cs, sp, cp;
-  fast_sincos(zs_re, &ss, &cs);
-  fast_sincos(zp_re, &sp, &cp);
-  double ms = fast_exp(zs_im), mp = fast_exp(zp_im);
-  cplx Es = {ms * cs, -ms * ss};
-  cplx ep = {mp * cp, -mp * sp};
-  cplx Ep = fc.g2 * ep;
-  cplx qs = fc.iks * ir, qp = fc.ikp * ir;      // 1/z
-  cplx qs2 = qs * qs, qp2 = qp * qp;
-  // t = -i q - q^2
-  cplx ts = {qs.im - qs2.re, -qs.re - qs2.im};
-  cplx tp = {qp.im - qp2.re, -qp.re - qp2.im};
-  cplx Fs = Es * ts, Fp = Ep * tp;
-  // -i z = (z.im, -z.re)
-  cplx Gs = Es * cplx{zs_im, -zs_re};
-  cplx Gp = Ep * cplx{zp_im, -zp_re};
-  Brackets o;
-  o.f0 = Es + Fs - Fp;
-  o.f1 = Es + c_num.three * (Fs - Fp) - Ep;
-  o.f2 = Gs - c_num.two * Es + Ep + c_num.three * (Fp - Fs);
-  o.f3 = Gs - Gp + c_num.four * (Ep - Es) + c_num.nine * (Fp - Fs);
-  return o;
+  // the S and P phases in lockstep (shared coefficient fetches, 2-way ILP)
+  const double rr[1] = {r};
+  cplx Es[1], ep[1];
+  phase_factors_n<1>(fc.ks, fc.kp, rr, Es, ep);
+  return brackets_phase(fc, r, ir, Es[0], ep[0]);
 }
 
 // Horner, real coefficients, complex argument: p(w) = sum_n c_n w^n.
@@ -359,18 +447,21 @@ __device__ __forceinline__ void horner4(cplx w, const double* c0, const double* 
 // Power series (kernels.py:122-138) with the (-i)^n folded into w = -i z:
 //   f0 = A(ws) + g2 B(wp)      f1 = C(ws) - g2 C(wp)
 //   f2 = A'(ws) + g2 B'(wp)    f3 = C'(ws) - g2 C'(wp)
-__device__ __forceinline__ Brackets brackets_series(const FreqConst& fc, double r) {
-  cplx ws = {fc.ks.im * r, -fc.ks.re * r};
-  cplx wp = {fc.kp.im * r, -fc.kp.re * r};
+__device__ __forceinline__ Brackets brackets_series_k(cplx ks, cplx kp, cplx g2, double r) {
+  cplx ws = {ks.im * r, -ks.re * r};
+  cplx wp = {kp.im * r, -kp.re * r};
   cplx s[4], p[4];
   horner4(ws, c_series.a, c_series.da, c_series.c, c_series.dc, s);
   horner4(wp, c_series.b, c_series.db, c_series.c, c_series.dc, p);
   Brackets o;
-  o.f0 = s[0] + fc.g2 * p[0];
-  o.f2 = s[1] + fc.g2 * p[1];
-  o.f1 = s[2] - fc.g2 * p[2];
-  o.f3 = s[3] - fc.g2 * p[3];
+  o.f0 = s[0] + g2 * p[0];
+  o.f2 = s[1] + g2 * p[1];
+  o.f1 = s[2] - g2 * p[2];
+  o.f3 = s[3] - g2 * p[3];
   return o;
+}
+__device__ __forceinline__ Brackets brackets_series(const FreqConst& fc, double r) {
+  return brackets_series_k(fc.ks, fc.kp, fc.g2, r);
 }
 
 // Power-sum form of the same series, NT terms: one complex power per term
@@ -410,8 +501,13 @@ __device__ __forceinline__ Brackets brackets_series_n(const FreqConst& fc, doubl
 // The series branch out of line, for kernels whose series points are rare
 // (far pairs switch at |k_s r| < 0.1): its register peak then does not
 // shape the hot closed-form loop.
-static __device__ __noinline__ Brackets brackets_series_cold(const FreqConst fc, double r) {
-  return brackets_series(fc, r);
+// (only the three constants the series reads travel by value: the whole
+// FreqConst would be passed through local memory)
+static __device__ __noinline__ Brackets brackets_series_cold3(cplx ks, cplx kp, cplx g2, double r) {
+  return brackets_series_k(ks, kp, g2, r);
+}
+__device__ __forceinline__ Brackets brackets_series_cold(const FreqConst& fc, double r) {
+  return brackets_series_cold3(fc.ks, fc.kp, fc.g2, r);
 }
 
 // Strict per-point switch exactly as kernels.py:79-95 (|k_s r| < 0.35).
@@ -522,7 +618,7 @@ __device__ __forceinline__ void point_dynamic(Acc<cplx>& A, const FreqConst& fc,
 
 // The five weighted scalars of one closed-form point straight from the
 // phase factors.  With D = E_s t_s - E_p t_p (t = -i/z - 1/z^2, the 1/z
-// terms of kernels.py:105-119), G_s = -i z_s E_s and G_p = -i z_p E_p, the
+// terms of kernels.py:105-119, from t_closed), G_s = -i z_s E_s and G_p = -i z_p E_p, the
 // brackets are linear in (E_s, E_p, D, G_s, G_p):
 //   f0 = E_s + D,  f1 = E_s - E_p + 3D,  f2 = G_s - 2E_s + E_p - 3D,
 //   f3 = G_s - G_p - 4E_s + 4E_p - 9D,
@@ -539,13 +635,9 @@ __device__ __forceinline__ void point_dynamic(Acc<cplx>& A, const FreqConst& fc,
 struct Weighted5 {
   cplx Phi, Psi, Aw, Bw, Cw;
 };
-__device__ __forceinline__ Weighted5 weights_phase(cplx ks, cplx kp, cplx iks, cplx ikp, double r,
-                                                   double ir, cplx Es, cplx Ep, double wu,
-                                                   double wt, double wb, double cr2, double c4r) {
-  const cplx qs = iks * ir, qp = ikp * ir;
-  const cplx qs2 = qs * qs, qp2 = qp * qp;
-  const cplx ts = {qs.im - qs2.re, -qs.re - qs2.im};
-  const cplx tp = {qp.im - qp2.re, -qp.re - qp2.im};
+__device__ __forceinline__ Weighted5 weights_phase(cplx ks, cplx kp, cplx ts, cplx tp, double r,
+                                                   cplx Es, cplx Ep, double wu, double wt,
+                                                   double wb, double cr2, double c4r) {
   cplx D = Es * ts;
   D.re = fma(-Ep.re, tp.re, fma(Ep.im, tp.im, D.re));
   D.im = fma(-Ep.re, tp.im, fma(-Ep.im, tp.re, D.im));
@@ -569,7 +661,9 @@ __device__ __forceinline__ Weighted5 weights_closed(const FreqConst& fc, double 
                                                    double wu, double wt, double wb) {
   const cplx Es = phase_factor(fc.ks, r);
   const cplx Ep = fc.g2 * phase_factor(fc.kp, r);
-  return weights_phase(fc.ks, fc.kp, fc.iks, fc.ikp, r, ir, Es, Ep, wu, wt, wb,
+  const double ir2 = ir * ir;
+  return weights_phase(fc.ks, fc.kp, t_closed2(fc.tas, fc.tbs, ir, ir2),
+                       t_closed2(fc.tap, fc.tbp, ir, ir2), r, Es, Ep, wu, wt, wb,
                        fc.ratio - c_num.two, c_num.four - fc.ratio);
 }
 
@@ -607,6 +701,30 @@ __device__ __forceinline__ void point_dynamic_scaled(Acc<cplx>& A, const FreqCon
   acc_point(A, Phi, Psi, Aw, Bw, Cw, dx, dy, dz, dn);
 }
 
+// The T product of one point from its four brackets (see point_apply_T).
+__device__ __forceinline__ void point_apply_T_br(cplx y[3], const Brackets& f, double ratio,
+                                                 double dx, double dy, double dz, double dn,
+                                                 double wt, const cplx v[3], cplx nv, double nx,
+                                                 double ny, double nz) {
+  const cplx Aw = wt * (f.f2 - f.f1);
+  const cplx Bw = (c_num.two * wt * dn) * (c_num.two * f.f1 - f.f3);
+  const cplx dd = f.f2 - f.f3;
+  const cplx Cw = wt * (ratio * (dd - c_num.two * f.f1) - c_num.two * (dd - f.f1));
+  cplx sv = dx * v[0];
+  axpy(sv, dy, v[1]);
+  axpy(sv, dz, v[2]);
+  const cplx e = dn * Aw, h = Aw * sv;
+  cplx gg = Bw * sv;
+  cfma(gg, Cw, nv);
+  const double n[3] = {nx, ny, nz}, d[3] = {dx, dy, dz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cfma(y[a], e, v[a]);
+    axpy(y[a], n[a], h);
+    axpy(y[a], d[a], gg);
+  }
+}
+
 // One dynamic point applied straight to a vector (T only, one vector: the
 // matrix-free GMRES product).  With s = d.v and nv = n.v the point's share of
 // T v (kernels.py:345-356) is
@@ -622,23 +740,7 @@ __device__ __forceinline__ void point_apply_T(cplx y[3], const FreqConst& fc, do
   // this product keeps the bracket form)
   const Brackets f =
       SER && fc.ks_abs * r < sw ? brackets_series_cold(fc, r) : brackets_closed(fc, r, ir);
-  const cplx Aw = wt * (f.f2 - f.f1);
-  const cplx Bw = (c_num.two * wt * dn) * (c_num.two * f.f1 - f.f3);
-  const cplx dd = f.f2 - f.f3;
-  const cplx Cw = wt * (fc.ratio * (dd - c_num.two * f.f1) - c_num.two * (dd - f.f1));
-  cplx sv = dx * v[0];
-  axpy(sv, dy, v[1]);
-  axpy(sv, dz, v[2]);
-  const cplx e = dn * Aw, h = Aw * sv;
-  cplx gg = Bw * sv;
-  cfma(gg, Cw, nv);
-  const double n[3] = {nx, ny, nz}, d[3] = {dx, dy, dz};
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    cfma(y[a], e, v[a]);
-    axpy(y[a], n[a], h);
-    axpy(y[a], d[a], gg);
-  }
+  point_apply_T_br(y, f, fc.ratio, dx, dy, dz, dn, wt, v, nv, nx, ny, nz);
 }
 
 // One dynamic point applied straight to one vector for both operators (the

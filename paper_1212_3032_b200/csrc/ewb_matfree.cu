@@ -557,7 +557,8 @@ __global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* 
           const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
           FreqConst fc;
           fc.ks = lds_c(&s_fc.ks); fc.kp = lds_c(&s_fc.kp);
-          fc.iks = lds_c(&s_fc.iks); fc.ikp = lds_c(&s_fc.ikp);
+          fc.tas = lds_c(&s_fc.tas); fc.tbs = lds_c(&s_fc.tbs);
+          fc.tap = lds_c(&s_fc.tap); fc.tbp = lds_c(&s_fc.tbp);
           fc.g2 = lds_c(&s_fc.g2); fc.ks_abs = lds_d(&s_fc.ks_abs);
           fc.ratio = lds_d(&s_fc.ratio);
           const double wi = w7r[q] * ir;
@@ -579,7 +580,8 @@ __global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* 
         const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
         FreqConst fc;
         fc.ks = lds_c(&s_fc.ks); fc.kp = lds_c(&s_fc.kp);
-        fc.iks = lds_c(&s_fc.iks); fc.ikp = lds_c(&s_fc.ikp);
+        fc.tas = lds_c(&s_fc.tas); fc.tbs = lds_c(&s_fc.tbs);
+          fc.tap = lds_c(&s_fc.tap); fc.tbp = lds_c(&s_fc.tbp);
         fc.g2 = lds_c(&s_fc.g2); fc.ks_abs = lds_d(&s_fc.ks_abs);
         fc.ratio = lds_d(&s_fc.ratio);
         const double wi = w7r[q] * ir;
