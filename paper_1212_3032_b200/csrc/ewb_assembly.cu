@@ -688,10 +688,26 @@ constexpr int kFarThreads = EWB_FARMULTI_THREADS;
 #endif
 constexpr int kFarQUnroll = EWB_FAR_QUNROLL;
 constexpr int kFarGeo = 8;
-constexpr int kBredStride = 33;   // padded: the 6 x 8-lane reads hit distinct banks
+// b-reduction scratch: word v of lane l sits at v * kBredStride + bred_pos(l).
+// The reader lane 4v + p sums the 8 lanes 8p..8p+7 of word v; with 64-bit
+// accesses a half-warp must hit 16 distinct bank pairs, so the four 8-lane
+// groups start at 0, 8, 20, 28 (mod 16: 0, 8, 4, 12) and the row stride is
+// 1 mod 16: stores and loads are conflict-free (stride 33 with groups at
+// 0, 8, 16, 24 made every load a 2-way conflict).
+#ifdef EWB_FAR_BRED_OLD
+constexpr int kBredStride = 33;
+__device__ __forceinline__ int bred_pos(int l) { return l; }
+#else
+constexpr int kBredStride = 49;
+__device__ __forceinline__ int bred_pos(int l) { return l + 4 * (l >> 4); }
+#endif
+// per-member constants of the closed-form point, 16-byte aligned so one
+// 128-bit load fetches a complex: ks, kp, tas, tbs, tap, tbp
+constexpr int kFarMc = 6;
+static_assert((sizeof(FreqConst) * kMaxBatch) % 16 == 0, "member table alignment");
 constexpr size_t far_smem(int bd) {
   return sizeof(double) * (kFarGeo * 3 * bd + 4 * 3 * 2 * bd) + sizeof(FreqConst) * kMaxBatch +
-         sizeof(double) * (bd / 32) * 6 * kBredStride;
+         sizeof(cplx) * kFarMc * kMaxBatch + sizeof(double) * (bd / 32) * 6 * kBredStride;
 }
 constexpr size_t kFarMultiSmem = far_smem(kFarThreads);
 
@@ -701,14 +717,62 @@ __device__ __forceinline__ unsigned expo(double v) {
 }
 __device__ __forceinline__ unsigned expo(cplx v) { return max(expo(v.re), expo(v.im)); }
 
+// Blocks of one far pair (kernels.py:336-356) entry by entry straight into A
+// and b:  U_ac = su d_ac - P_ac,  T_ac = B_ac + n_a va_c + vc_a n_c + sa d_ac;
+// BC mix (assembly.py:290-296): Neumann column A = T, b += U p; Dirichlet
+// column A = -U, b -= T p.  With nu = -U the stored entry is
+// (Dirichlet ? nu : T) and b -= (Dirichlet ? T : nu) p — selects on the
+// integer pipe instead of a divergent branch per entry (MIXED), or no
+// selects at all when the whole tile is Neumann.  Returns true when an entry
+// is Inf or NaN (largest exponent field all ones).  Measured neutral or
+// slower and not kept: an OR-of-high-words pre-filter for that test, member-
+// stepped pointers instead of the index arithmetic, and the member constants
+// from the kernel-parameter bank (1.78-1.80 vs 1.78 ms per frequency).
+template <bool MIXED>
+__device__ __forceinline__ bool far_store_block(const Acc<cplx>& acc, double nx, double ny,
+                                                    double nz, unsigned kbits, const cplx (&pv)[3],
+                                                    cplx (&bc)[3], cplx* blk, long long N) {
+  const double n[3] = {nx, ny, nz};
+  const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+  unsigned ex = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cplx* row = blk + (size_t)a * N;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const cplx nu = a == c ? acc.P[sym[a][c]] - acc.su : acc.P[sym[a][c]];
+      cplx tv = acc.B[sym[a][c]];
+      madd(tv, n[a], acc.va[c]);
+      madd(tv, n[c], acc.vc[a]);
+      if (a == c) tv = tv + acc.sa;
+      ex = max(ex, max(expo(nu), expo(tv)));
+      if (MIXED) {
+        const bool dir = kbits & (1u << c);
+        const cplx st = {dir ? nu.re : tv.re, dir ? nu.im : tv.im};
+        const cplx ml = {dir ? tv.re : nu.re, dir ? tv.im : nu.im};
+        *reinterpret_cast<double2*>(row + c) = make_double2(st.re, st.im);
+        cfma(bc[a], ml, -pv[c]);
+      } else {
+        *reinterpret_cast<double2*>(row + c) = make_double2(tv.re, tv.im);
+        cfma(bc[a], nu, -pv[c]);
+      }
+    }
+  }
+  return ex == 0x7ff00000u;
+}
+
 // SER = false: the host proved no far pair of the batch can reach the series
 // branch (min |k_s| x the far-pair distance bound >= the switch, make_batch),
 // so the kernel carries no out-of-line series call (fewer live registers).
 template <bool RECUR, bool SER>
 __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
                                                                       SysBatch o) {
-  extern __shared__ double sm_far[];
+  extern __shared__ __align__(16) double sm_far[];
+#ifdef EWB_FAR_BD_RUNTIME
   const int BD = blockDim.x;
+#else
+  constexpr int BD = kFarThreads;   // always launched with kFarThreads: immediate smem offsets
+#endif
   const int tid = threadIdx.x;
   // [slot][q][thread] with a block-size stride (conflict-free)
   auto SG = [&](int slot, int q) -> double& { return sm_far[(slot * 3 + q) * BD + tid]; };
@@ -717,10 +781,19 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
   FreqConst* sfc = reinterpret_cast<FreqConst*>(sm_far + kFarGeo * 3 * BD + 4 * 3 * 2 * BD);
   for (int k = tid; k < fb.nf * (int)(sizeof(FreqConst) / 8); k += blockDim.x)
     ((double*)sfc)[k] = ((const double*)fb.fc)[k];
+  cplx* smc = reinterpret_cast<cplx*>(sfc + kMaxBatch);   // [member][kFarMc]
+  for (int f = tid; f < fb.nf; f += blockDim.x) {
+    smc[f * kFarMc + 0] = fb.fc[f].ks;
+    smc[f * kFarMc + 1] = fb.fc[f].kp;
+    smc[f * kFarMc + 2] = fb.fc[f].tas;
+    smc[f * kFarMc + 3] = fb.fc[f].tbs;
+    smc[f * kFarMc + 4] = fb.fc[f].tap;
+    smc[f * kFarMc + 5] = fb.fc[f].tbp;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   // this warp's b-reduction scratch [6][kBredStride] (after the member constants)
-  double* sbr = reinterpret_cast<double*>(sfc + kMaxBatch) + (tid >> 5) * 6 * kBredStride;
+  double* sbr = reinterpret_cast<double*>(smc + kFarMc * kMaxBatch) + (tid >> 5) * 6 * kBredStride;
   const int ntile = (g.n_e + 31) >> 5;
   const int ngroups = (g.n_e + kFarRows - 1) / kFarRows;
   const long long nitems = (long long)ngroups * ntile;
@@ -739,6 +812,11 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
     const unsigned kbits = (o.kinds[3 * jj] == kDirichlet ? 1u : 0u) |
                            (o.kinds[3 * jj + 1] == kDirichlet ? 2u : 0u) |
                            (o.kinds[3 * jj + 2] == kDirichlet ? 4u : 0u);
+#ifdef EWB_FAR_ALWAYS_MIXED
+    const bool tile_mixed = true;
+#else
+    const bool tile_mixed = __any_sync(0xffffffffu, kbits != 0);
+#endif
     for (int r = 0; r < kFarRows; ++r) {
       const int i = rg * kFarRows + r;
       if (i >= g.n_e) break;
@@ -773,11 +851,14 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
       }
 #pragma unroll 1
       for (int f = 0; f < nf; ++f) {
+        const cplx* pcol = o.p + (size_t)f * N + 3 * j;
+        cplx* blk = o.A + (size_t)f * N * N + (size_t)(3 * i) * N + 3 * j;
+        double* bp = reinterpret_cast<double*>(o.bpart + ((size_t)f * ntile + t) * N + 3 * i) +
+                     (lane >> 2);
         cplx bc[3] = {{0, 0}, {0, 0}, {0, 0}};
         if (far) {
           // prescribed values of this member (16-byte loads; the next member's
           // were pulled into L1 one iteration ago, so this is not an L2 wait)
-          const cplx* pcol = o.p + (size_t)f * N + 3 * j;
           if (f + 1 < nf) {
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pcol + N));
             asm volatile("prefetch.global.L1 [%0];" ::"l"(pcol + N + 2));
@@ -796,9 +877,16 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
             const double rr = SG(0, q), ir = SG(1, q);
             const double dx = SG(2, q), dy = SG(3, q), dz = SG(4, q);
             const double dn2 = SG(5, q), wu = SG(6, q), wt = SG(7, q);
+#ifndef EWB_FAR_MC64
+            const cplx* mc = smc + f * kFarMc;
+            const cplx ks = lds_c16(mc), kp = lds_c16(mc + 1);
+            const cplx ts = t_closed(lds_c16(mc + 2), lds_c16(mc + 3), ir);
+            const cplx tp = t_closed(lds_c16(mc + 4), lds_c16(mc + 5), ir);
+#else
             const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
             const cplx ts = t_closed(lds_c(&sfc[f].tas), lds_c(&sfc[f].tbs), ir);
             const cplx tp = t_closed(lds_c(&sfc[f].tap), lds_c(&sfc[f].tbp), ir);
+#endif
             cplx Es, Ep;
             if (RECUR) {
               Es = SP(0, q);
@@ -829,36 +917,12 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
             acc_point(acc, w.Phi, w.Psi, w.Aw, w.Bw, w.Cw, dx, dy, dz, dn2);
           }
           acc.sa = c_num.half * acc.sa;
-          // blocks (kernels.py:336-356) entry by entry straight into A and b:
-          // U_ac = su d_ac - P_ac, T_ac = B_ac + n_a va_c + vc_a n_c + sa d_ac;
-          // BC mix (assembly.py:290-296): Neumann column A = T, b += U p;
-          // Dirichlet column A = -U, b -= T p.  Branch-free: with nu = -U the
-          // stored entry is (Dirichlet ? nu : T) and b -= (Dirichlet ? T : nu) p
-          // (selects on the integer pipe instead of a divergent branch per entry)
-          const double n[3] = {nx, ny, nz};
-          const int sym[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
-          unsigned ex = 0;
-          cplx* Af = o.A + (size_t)f * N * N;
           EWB_DCHECK(3LL * i + 2 < N && 3LL * j + 2 < N && f < nf && nf <= kMaxBatch, 201);
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            cplx* row = Af + (size_t)(3 * i + a) * N + 3 * j;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const cplx nu = a == c ? acc.P[sym[a][c]] - acc.su : acc.P[sym[a][c]];
-              cplx tv = acc.B[sym[a][c]];
-              madd(tv, n[a], acc.va[c]);
-              madd(tv, n[c], acc.vc[a]);
-              if (a == c) tv = tv + acc.sa;
-              ex = max(ex, max(expo(nu), expo(tv)));
-              const bool dir = kbits & (1u << c);
-              const cplx st = {dir ? nu.re : tv.re, dir ? nu.im : tv.im};
-              const cplx ml = {dir ? tv.re : nu.re, dir ? tv.im : nu.im};
-              *reinterpret_cast<double2*>(row + c) = make_double2(st.re, st.im);
-              cfma(bc[a], ml, -pv[c]);
-            }
-          }
-          if (ex == 0x7ff00000u) o.flags[4 * f] = 1;
+          // a tile whose 32 columns are all Neumann (warp-uniform) skips the selects
+          const bool bad = tile_mixed
+                               ? far_store_block<true>(acc, nx, ny, nz, kbits, pv, bc, blk, N)
+                               : far_store_block<false>(acc, nx, ny, nz, kbits, pv, bc, blk, N);
+          if (bad) o.flags[4 * f] = 1;
         }
         // b partial of this (row, tile, member): the 32 lanes' 3 complex
         // values, transposed through shared memory — lane 4v + p sums the 8
@@ -867,19 +931,20 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
         // butterfly of 6 doubles in every lane)
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          sbr[(2 * a) * kBredStride + lane] = bc[a].re;
-          sbr[(2 * a + 1) * kBredStride + lane] = bc[a].im;
+          sbr[(2 * a) * kBredStride + bred_pos(lane)] = bc[a].re;
+          sbr[(2 * a + 1) * kBredStride + bred_pos(lane)] = bc[a].im;
         }
         __syncwarp();
         if (lane < 24) {
           const int v = lane >> 2, pp = lane & 3;
-          const double* src = sbr + v * kBredStride + 8 * pp;
+          const double* src = sbr + v * kBredStride + bred_pos(8 * pp);
+          (void)v;
           double sum = ((src[0] + src[1]) + (src[2] + src[3])) + ((src[4] + src[5]) + (src[6] + src[7]));
           sum += __shfl_xor_sync(0x00ffffffu, sum, 1);
           sum += __shfl_xor_sync(0x00ffffffu, sum, 2);
           if (pp == 0) {
             EWB_DCHECK(t < ntile && 3LL * i + 2 < N, 202);
-            reinterpret_cast<double*>(o.bpart + ((size_t)f * ntile + t) * N + 3 * i)[v] = sum;
+            *bp = sum;
           }
         }
         __syncwarp();

@@ -187,6 +187,15 @@ __device__ __forceinline__ double lds_d(const double* p) {
 // (FreqConst is 8-byte aligned with a 152-byte stride: two scalar loads)
 __device__ __forceinline__ cplx lds_c(const cplx* p) { return {lds_d(&p->re), lds_d(&p->im)}; }
 
+// a 16-byte aligned complex in one 128-bit load
+__device__ __forceinline__ cplx lds_c16(const cplx* p) {
+  cplx v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.re), "=d"(v.im)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
 // FP64 literals of the hot loops as constant-bank operands: a 64-bit
 // immediate is not encodable in DFMA/DMUL/DADD, so a literal costs two UMOV
 // per use in an unrolled loop (measured: 5.7 % of k_far_multi's issued

@@ -142,13 +142,16 @@ __device__ __forceinline__ void ring_init(Ring& R, bool evict_first) {
   __syncthreads();
 }
 
+// xk > 0: the same columns of xk input vectors (X + k n) ride in the stage's
+// last xk row slots, so the consumers read x from shared memory.
 __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cplx* A, long long n,
-                                           long long row0, int nrows, long long c0, int tc) {
+                                           long long row0, int nrows, long long c0, int tc,
+                                           const cplx* X = nullptr, int xk = 0) {
   const int b = pos % kNS;
-  EWB_DCHECK(nrows >= 1 && nrows <= kRR && tc >= 1 && tc <= kTC && row0 >= 0 &&
+  EWB_DCHECK(nrows >= 1 && nrows + xk <= kRR && tc >= 1 && tc <= kTC && row0 >= 0 &&
                  row0 + nrows <= n && c0 >= 0 && c0 + tc <= n, 101);
   const uint32_t bar = smem_u32(&R.bar[b]);
-  const uint32_t bytes = (uint32_t)(nrows * tc * 16);
+  const uint32_t bytes = (uint32_t)((nrows + xk) * tc * 16);
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
   // the policy is made here (issuing thread only) instead of living in
@@ -166,6 +169,19 @@ __device__ __forceinline__ void ring_issue(const Ring& R, unsigned pos, const cp
         " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
         "l"(src), "r"(tc * 16), "r"(bar), "l"(pol)
         : "memory");
+  }
+  if (xk > 0) {   // x stays in L2 for every CTA and row block: evict_last
+    uint64_t polx;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(polx));
+    for (int k = 0; k < xk; ++k) {
+      const uint32_t dst = smem_u32(R.buf + (size_t)b * kStageElems + (kRR - xk + k) * kTC);
+      const cplx* src = X + (long long)k * n + c0;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+          "l"(src), "r"(tc * 16), "r"(bar), "l"(polx)
+          : "memory");
+    }
   }
 }
 
@@ -372,20 +388,27 @@ __device__ void matvec_rows(Ring& R, const cplx* __restrict__ A, long long n, co
   R.pos += (unsigned)S;
 }
 
-template <int K, typename Epi>
+// Multi-column matvec (K = 3, 4).  XS = false: kSl = 4 row slices x kRR / 4
+// rows; a slice's 128 threads take kTC / 128 columns of every tile and keep
+// the next stage's x (kCp x K values) in registers, loaded from global memory
+// by every slice.  XS = true (the default for SEM's Y = A X): the stage holds
+// kRA = 8 rows of A plus the K x-chunks of the same columns, all brought in by
+// the same bulk-copy transaction, 2 row slices x 4 rows x 2 columns per
+// thread: x costs no registers, no L2 round trip inside the consumer loop and
+// half the replication (measured, tools/sem_time.py).
+template <int K, bool XS, typename Epi>
 __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long n, const cplx* x,
                             long long r0, long long r1, Epi&& epi) {
-  // 4 row slices x 4 rows; a slice's 128 threads take columns col and
-  // col + 128 of every tile: 4 x K accumulators and 2 x K prefetched x per
-  // thread (K = 3, 4 fit the 128-register budget without spilling).
-  constexpr int kSl = 4, kRw = kRR / kSl, kCols = kSolveThreads / kSl, kCp = kTC / kCols;
-  static_assert(kRR % kSl == 0 && kTC % kCols == 0, "matvec_rows_wide layout");
+  constexpr int kSl = XS ? 2 : 4, kRA = XS ? 8 : kRR, kRw = kRA / kSl;
+  constexpr int kCols = kSolveThreads / kSl, kCp = kTC / kCols;
+  static_assert(kRA % kSl == 0 && kTC % kCols == 0 && kRA + (XS ? K : 0) <= kRR,
+                "matvec_rows_wide layout");
   __shared__ cplx s_red[kSolveWarps][kRw][K];
-  __shared__ cplx s_sum[kRR][K];
+  __shared__ cplx s_sum[kRA][K];
   __shared__ int s_rel[kNS];  // warps done with each ring slot
   const int rows = (int)(r1 - r0);
   if (rows <= 0) return;
-  const int nblk = (rows + kRR - 1) / kRR;
+  const int nblk = (rows + kRA - 1) / kRA;
   const int ntile = (int)((n + kTC - 1) / kTC);
   const int S = nblk * ntile;
   const int last_tc = (int)(n - (long long)(ntile - 1) * kTC);
@@ -398,7 +421,8 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
     const int q = u / ntile, t = u - q * ntile;
     const int rel0 = q * rows / nblk, nr = (q + 1) * rows / nblk - rel0;
     const int tc = t == ntile - 1 ? last_tc : kTC;
-    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc);
+    ring_issue(R, R.pos + (unsigned)u, A, n, r0 + rel0, nr, (long long)t * kTC, tc,
+               XS ? x : nullptr, XS ? K : 0);
   };
   if (threadIdx.x < kNS) s_rel[threadIdx.x] = 0;
   __syncthreads();
@@ -413,14 +437,16 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
   for (int r = 0; r < kRw; ++r)
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[r][k] = {0.0, 0.0};
-  cplx xn[kCp][K];  // x of the stage being consumed (loaded after the previous stage's FMAs)
+  cplx xn[XS ? 1 : kCp][K];  // x of the stage being consumed (XS: one column at a time)
+  if (!XS) {
 #pragma unroll
-  for (int m = 0; m < kCp; ++m)
+    for (int m = 0; m < kCp; ++m)
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int c = col + m * kCols;
-      xn[m][k] = c < n ? ldg(x + k * n + c) : cplx{0.0, 0.0};
-    }
+      for (int k = 0; k < K; ++k) {
+        const int c = col + m * kCols;
+        xn[XS ? 0 : m][k] = c < n ? ldg(x + k * n + c) : cplx{0.0, 0.0};
+      }
+  }
   int q = 0, t = 0;
   long long row0 = r0;
   int nrows = rows / nblk;
@@ -435,6 +461,13 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
       for (int m = 0; m < kCp; ++m) {
         const int c = col + m * kCols;
         if (c < tc) {
+          if (XS) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              double2 x2 = *reinterpret_cast<const double2*>(tile + (kRR - K + k) * kTC + c);
+              xn[0][k] = {x2.x, x2.y};
+            }
+          }
 #pragma unroll
           for (int r = 0; r < kRw; ++r) {
             const int row = slice * kRw + r;
@@ -442,20 +475,20 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
               double2 a2 = *reinterpret_cast<const double2*>(tile + row * kTC + c);
               cplx av = {a2.x, a2.y};
 #pragma unroll
-              for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xn[m][k]);
+              for (int k = 0; k < K; ++k) cfma(acc[r][k], av, xn[XS ? 0 : m][k]);
             }
           }
         }
       }
     }
-    {  // x for the next stage
+    if (!XS) {  // x for the next stage
       const long long cb = (t == ntile - 1 ? 0 : c0 + kTC) + col;
 #pragma unroll
       for (int m = 0; m < kCp; ++m)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const long long cn = cb + m * kCols;
-          xn[m][k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
+          xn[XS ? 0 : m][k] = cn < n ? ldg(x + k * n + cn) : cplx{0.0, 0.0};
         }
     }
     __syncwarp();
@@ -481,7 +514,7 @@ __device__ void matvec_rows_wide(Ring& R, const cplx* __restrict__ A, long long 
           acc[r][k] = {0.0, 0.0};
         }
       __syncthreads();
-      if (threadIdx.x < kRR * K) {
+      if (threadIdx.x < kRA * K) {
         const int row = threadIdx.x / K, k = threadIdx.x % K;
         const int h = row / kRw, r = row % kRw;
         constexpr int wps = kSolveWarps / kSl;  // warps per row slice
@@ -1190,8 +1223,13 @@ __global__ void __launch_bounds__(kSolveThreads, kSolveMinBlocks) k_multi_gemv(c
       Y[k * n + row0 + row] = sum[row][k];
     }
   };
+#ifdef EWB_SEM_X_GLOBAL
+  constexpr bool kXs = false;
+#else
+  constexpr bool kXs = kRR >= 8 + K && kTC % (kSolveThreads / 2) == 0;   // x staged in the ring
+#endif
   if constexpr (K <= 2) matvec_rows<K>(ring, A, n, X, r0, r1, store);
-  else matvec_rows_wide<K>(ring, A, n, X, r0, r1, store);
+  else matvec_rows_wide<K, kXs>(ring, A, n, X, r0, r1, store);
 }
 
 template <int K>
