@@ -172,6 +172,32 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
                                               wq * ir * ir * ct, v, nv, nx, ny, nz);
         };
         if (tier == 0) {
+#ifndef EWB_MF_NO_DELTA
+          // damping factors of points 1, 2 from point 0's (column-uniform test)
+          if (fabs(ph.fc.ks.im) * s_geo[jj][3] <= c_math.delta_max) {
+            double r0 = 0, ms0 = 0, mp0 = 0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const double* yq = &s_y[jj][3 * q];
+              double dx = yq[0] - xi, dy = yq[1] - yi, dz = yq[2] - zi;
+              const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+              const double ir = rsqrt(r2);
+              const double r = r2 * ir;
+              dx *= ir; dy *= ir; dz *= ir;
+              const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+              double ms, mp;
+              if (q == 0) {
+                damping_factors<false>(ph.fc, r, 0.0, 0.0, 0.0, ms, mp);
+                r0 = r; ms0 = ms; mp0 = mp;
+              } else {
+                damping_factors<true>(ph.fc, r, r0, ms0, mp0, ms, mp);
+              }
+              point_apply_T_m<SER>(y[0], ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn,
+                                   g.wfar[q] * ir * ir * ct, v, nv, nx, ny, nz, ms, mp);
+            }
+            continue;
+          }
+#endif
 #pragma unroll kMfQUnroll
           for (int q = 0; q < 3; ++q)
             point1(&s_y[jj][3 * q], g.wfar[q], std::integral_constant<bool, SER>{});
@@ -196,9 +222,36 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
                                                    wi * cu, wi * ir * ct);
       };
       if (tier == 0) {
+#ifndef EWB_MF_NO_DELTA
+        if (fabs(ph.fc.ks.im) * s_geo[jj][3] <= c_math.delta_max) {
+          double r0 = 0, ms0 = 0, mp0 = 0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const double* yq = &s_y[jj][3 * q];
+            double dx = yq[0] - xi, dy = yq[1] - yi, dz = yq[2] - zi;
+            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            const double ir = rsqrt(r2);
+            const double r = r2 * ir;
+            dx *= ir; dy *= ir; dz *= ir;
+            const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
+            const double wi = g.wfar[q] * ir;
+            double ms, mp;
+            if (q == 0) {
+              damping_factors<false>(ph.fc, r, 0.0, 0.0, 0.0, ms, mp);
+              r0 = r; ms0 = ms; mp0 = mp;
+            } else {
+              damping_factors<true>(ph.fc, r, r0, ms0, mp0, ms, mp);
+            }
+            point_dynamic_scaled_m<SER>(acc, ph.fc, c_num.far_sw, r, ir, dx, dy, dz, dn, wi * cu,
+                                        wi * ir * ct, ms, mp);
+          }
+        } else
+#endif
+        {
 #pragma unroll kMfQUnroll
-        for (int q = 0; q < 3; ++q)
-          point(&s_y[jj][3 * q], g.wfar[q], std::integral_constant<bool, SER>{});
+          for (int q = 0; q < 3; ++q)
+            point(&s_y[jj][3 * q], g.wfar[q], std::integral_constant<bool, SER>{});
+        }
       } else {
 #pragma unroll 1
         for (int q = 0; q < 7; ++q) point(&s_y[jj][9 + 3 * q], g.wmid[q], std::true_type{});
