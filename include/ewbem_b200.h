@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EWB_ABI_VERSION 5
+#define EWB_ABI_VERSION 6
 
 enum ewb_status {
   EWB_OK = 0,
@@ -294,6 +294,12 @@ int ewb_fp64_peak_probe(int64_t iters, int32_t blocks_per_sm, double* tflops_hos
  * check against libm (tests).  Synchronises. */
 int ewb_math_selftest(const double* x_host, int64_t n, double* sin_host, double* cos_host,
                       double* exp_host, void* stream);
+
+/* The small-argument exponential (ewb_common.cuh exp_small) that steps the
+ * damping factor e^{Im(k) r} from the first quadrature point of a far pair
+ * to the other two in the matrix-free kernels, on n HOST arguments
+ * |t| <= 2^-4 (EWB_ERR_INVALID beyond).  Synchronises. */
+int ewb_math_selftest_delta(const double* t_host, int64_t n, double* exp_host, void* stream);
 
 /* Debug-build self checks (library built with -DEWB_DEBUG_CHECKS; the
  * stand-in for compute-sanitizer): *failures = device-side

@@ -29,11 +29,11 @@ EXPORTS = (
     "ewb_matfree_workspace_bytes", "ewb_matfree_apply", "ewb_matfree_apply_masked",
     "ewb_pair_kernels_blocks", "ewb_pair_kernels_workspace_bytes",
     "ewb_pair_kernels_reduce", "ewb_fp64_peak_probe", "ewb_debug_checks",
-    "ewb_math_selftest",
+    "ewb_math_selftest", "ewb_math_selftest_delta",
 )
 
 EWB_OK, EWB_ERR_INVALID, EWB_ERR_CUDA, EWB_ERR_NONFINITE = 0, 1, 2, 3
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 class NativeUnavailable(RuntimeError):
@@ -98,6 +98,7 @@ _SIGS = {
     "ewb_fp64_peak_probe": (I32, [I64, I32, P, P, P]),
     "ewb_debug_checks": (I32, [P, P, I32]),
     "ewb_math_selftest": (I32, [P, I64, P, P, P, P]),
+    "ewb_math_selftest_delta": (I32, [P, I64, P, P]),
 }
 
 

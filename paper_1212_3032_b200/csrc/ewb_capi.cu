@@ -524,6 +524,7 @@ int ewb_window_idft(const void* half, int64_t n_half, int64_t D, int32_t window,
 namespace ewb {
 cudaError_t launch_math_selftest(const double* x, long long n, double* s, double* c, double* e,
                                  cudaStream_t st);
+cudaError_t launch_math_selftest_delta(const double* t, long long n, double* e, cudaStream_t st);
 }
 
 // ---------------------------------------------------------------------
@@ -701,6 +702,24 @@ int ewb_math_selftest(const double* x, int64_t n, double* sin_out, double* cos_o
   if (!e) e = cudaStreamSynchronize(s);
   cudaFree(d);
   EWB_CUDA(e, "ewb_math_selftest");
+  return EWB_OK;
+}
+
+int ewb_math_selftest_delta(const double* t, int64_t n, double* exp_out, void* stream) {
+  if (!t || !exp_out || n < 0) return fail(EWB_ERR_INVALID, "ewb_math_selftest_delta: bad argument");
+  for (int64_t i = 0; i < n; ++i)
+    if (!(t[i] >= -0.0625 && t[i] <= 0.0625))
+      return fail(EWB_ERR_INVALID, "ewb_math_selftest_delta: |t| > 2^-4");
+  if (n == 0) return EWB_OK;
+  double* d = nullptr;
+  EWB_CUDA(cudaMalloc(&d, sizeof(double) * 2 * n), "ewb_math_selftest_delta");
+  cudaStream_t s = S(stream);
+  cudaError_t e = cudaMemcpyAsync(d, t, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (!e) e = ewb::launch_math_selftest_delta(d, n, d + n, s);
+  if (!e) e = cudaMemcpyAsync(exp_out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  EWB_CUDA(e, "ewb_math_selftest_delta");
   return EWB_OK;
 }
 

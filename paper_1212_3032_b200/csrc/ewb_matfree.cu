@@ -545,29 +545,39 @@ __global__ void k_pair_blocks(const double* x, long long P, const double* tri, l
 
 // fused reduction: y_U[f][p] = sum_m U(p,m) x_m, y_T likewise.  Thread per
 // point, CTA stages 32 triangles (field points, normal, weight*area, x_m)
-// in shared memory; blockIdx.y = frequency, blockIdx.z = triangle chunk.
+// in shared memory; blockIdx.y = frequency group, blockIdx.z = triangle chunk.
 constexpr int kPkTile = 32;
 #ifndef EWB_PK_MINB
 #define EWB_PK_MINB 3
 #endif
+// FC frequencies per thread (blockIdx.y = frequency group): the pair
+// geometry of a point (r, 1/r, d, d.n: rsqrt + ~20 FP64 instructions) is
+// computed once for the group instead of once per frequency.
+template <int FC>
 __global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* x, long long P,
                                                      const double* tri, long long M,
-                                                     const cplx* xv, const FreqConst* fcs,
+                                                     const cplx* xv, const FreqConst* fcs, int F,
                                                      const double* b7, const double* w7,
                                                      long long chunk, cplx* part) {
   __shared__ double s_y[kPkTile][21];
   __shared__ double s_n[kPkTile][4];   // nx ny nz area
   __shared__ cplx s_x[kPkTile][3];
-  __shared__ FreqConst s_fc;
+  __shared__ FreqConst s_fcs[FC];
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int f = blockIdx.y;
-  if (threadIdx.x < sizeof(FreqConst) / 8)
-    ((double*)&s_fc)[threadIdx.x] = ((const double*)(fcs + f))[threadIdx.x];
+  const int f0 = blockIdx.y * FC;
+  for (int k = threadIdx.x; k < FC * (int)(sizeof(FreqConst) / 8); k += blockDim.x) {
+    const int c = k / (int)(sizeof(FreqConst) / 8), w = k % (int)(sizeof(FreqConst) / 8);
+    ((double*)&s_fcs[c])[w] = ((const double*)(fcs + min(f0 + c, F - 1)))[w];
+  }
   __syncthreads();
   const long long m0 = (long long)blockIdx.z * chunk, m1 = min(M, m0 + chunk);
   const bool ok = p < P;
   const double xi = ok ? x[3 * p] : 0.0, yi = ok ? x[3 * p + 1] : 0.0, zi = ok ? x[3 * p + 2] : 0.0;
-  cplx yu[3] = {{0, 0}, {0, 0}, {0, 0}}, yt[3] = {{0, 0}, {0, 0}, {0, 0}};
+  cplx yu[FC][3], yt[FC][3];
+#pragma unroll
+  for (int c = 0; c < FC; ++c)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { yu[c][a] = {0.0, 0.0}; yt[c][a] = {0.0, 0.0}; }
   double w7r[7];
 #pragma unroll
   for (int q = 0; q < 7; ++q) w7r[q] = w7[q];
@@ -590,39 +600,15 @@ __global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* 
     if (!ok) continue;
     for (int jj = 0; jj < tc; ++jj) {
       const double nx = s_n[jj][0], ny = s_n[jj][1], nz = s_n[jj][2], ar = s_n[jj][3];
-      // 1/(4 pi mu), 1/(4 pi) folded into the weights; per-frequency
-      // constants read from shared memory where used (not held in registers)
-      const double cu = ar * s_fc.inv4pimu, ct = ar * s_fc.inv4pi;
-#ifndef EWB_PK_ACC
-      // points applied straight to x_m (no 20-word accumulator)
-      {
-        const cplx v[3] = {s_x[jj][0], s_x[jj][1], s_x[jj][2]};
-        cplx nv = nx * v[0];
-        axpy(nv, ny, v[1]);
-        axpy(nv, nz, v[2]);
-#pragma unroll 1
-        for (int q = 0; q < 7; ++q) {
-          double dx = s_y[jj][3 * q] - xi, dy = s_y[jj][3 * q + 1] - yi, dz = s_y[jj][3 * q + 2] - zi;
-          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-          const double ir = rsqrt(r2);
-          const double r = r2 * ir;
-          dx *= ir; dy *= ir; dz *= ir;
-          const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-          FreqConst fc;
-          fc.ks = lds_c(&s_fc.ks); fc.kp = lds_c(&s_fc.kp);
-          fc.tas = lds_c(&s_fc.tas); fc.tbs = lds_c(&s_fc.tbs);
-          fc.tap = lds_c(&s_fc.tap); fc.tbp = lds_c(&s_fc.tbp);
-          fc.g2 = lds_c(&s_fc.g2); fc.ks_abs = lds_d(&s_fc.ks_abs);
-          fc.ratio = lds_d(&s_fc.ratio);
-          const double wi = w7r[q] * ir;
-          point_apply_UT(yu, yt, fc, lds_d(&s_fc.sw), r, ir, dx, dy, dz, dn, wi * cu,
-                         wi * ir * ct, v, nv, nx, ny, nz);
-        }
-        continue;
-      }
-#endif
-      Acc<cplx> acc;
-      acc_zero(acc);
+      // points applied straight to x_m (no 20-word accumulator); 1/(4 pi mu),
+      // 1/(4 pi) folded into the weights; per-frequency constants read from
+      // shared memory where used (not held in registers)
+      // (material constants: the same in every member of the group)
+      const double cu = ar * s_fcs[0].inv4pimu, ct = ar * s_fcs[0].inv4pi;
+      const cplx v[3] = {s_x[jj][0], s_x[jj][1], s_x[jj][2]};
+      cplx nv = nx * v[0];
+      axpy(nv, ny, v[1]);
+      axpy(nv, nz, v[2]);
 #pragma unroll 1
       for (int q = 0; q < 7; ++q) {
         double dx = s_y[jj][3 * q] - xi, dy = s_y[jj][3 * q + 1] - yi, dz = s_y[jj][3 * q + 2] - zi;
@@ -631,23 +617,30 @@ __global__ void __launch_bounds__(128, EWB_PK_MINB) k_pair_reduce(const double* 
         const double r = r2 * ir;
         dx *= ir; dy *= ir; dz *= ir;
         const double dn = fma(dz, nz, fma(dy, ny, dx * nx));
-        FreqConst fc;
-        fc.ks = lds_c(&s_fc.ks); fc.kp = lds_c(&s_fc.kp);
-        fc.tas = lds_c(&s_fc.tas); fc.tbs = lds_c(&s_fc.tbs);
-          fc.tap = lds_c(&s_fc.tap); fc.tbp = lds_c(&s_fc.tbp);
-        fc.g2 = lds_c(&s_fc.g2); fc.ks_abs = lds_d(&s_fc.ks_abs);
-        fc.ratio = lds_d(&s_fc.ratio);
         const double wi = w7r[q] * ir;
-        point_dynamic_scaled(acc, fc, lds_d(&s_fc.sw), r, ir, dx, dy, dz, dn, wi * cu,
-                             wi * ir * ct);
+        const double wu = wi * cu, wt = wi * ir * ct;
+#pragma unroll
+        for (int c = 0; c < FC; ++c) {
+          const FreqConst& sf = s_fcs[c];
+          FreqConst fc;
+          fc.ks = lds_c(&sf.ks); fc.kp = lds_c(&sf.kp);
+          fc.tas = lds_c(&sf.tas); fc.tbs = lds_c(&sf.tbs);
+          fc.tap = lds_c(&sf.tap); fc.tbp = lds_c(&sf.tbp);
+          fc.g2 = lds_c(&sf.g2); fc.ks_abs = lds_d(&sf.ks_abs);
+          fc.ratio = lds_d(&sf.ratio);
+          point_apply_UT(yu[c], yt[c], fc, lds_d(&sf.sw), r, ir, dx, dy, dz, dn, wu, wt, v, nv,
+                         nx, ny, nz);
+        }
       }
-      acc_apply_U(acc, 1.0, s_x[jj], yu);
-      acc_apply_T(acc, nx, ny, nz, 1.0, s_x[jj], yt);
     }
   }
   if (!ok) return;
-  cplx* o = part + (((size_t)blockIdx.z * gridDim.y + f) * P + p) * 6;
-  for (int a = 0; a < 3; ++a) { o[a] = yu[a]; o[3 + a] = yt[a]; }
+#pragma unroll
+  for (int c = 0; c < FC; ++c) {
+    if (f0 + c >= F) break;
+    cplx* o = part + (((size_t)blockIdx.z * F + f0 + c) * P + p) * 6;
+    for (int a = 0; a < 3; ++a) { o[a] = yu[c][a]; o[3 + a] = yt[c][a]; }
+  }
 }
 
 __global__ void k_pair_reduce_final(const cplx* part, int nchunk, int F, long long P, cplx* yu,
@@ -679,8 +672,16 @@ cudaError_t launch_pair_reduce(const double* x, long long P, const double* tri, 
   cudaError_t e = upload_series(s);
   if (e) return e;
   long long chunk = (M + nchunk - 1) / nchunk;
-  dim3 grid((unsigned)((P + 127) / 128), F, nchunk);
-  EWB_NOTE k_pair_reduce<<<grid, 128, 0, s>>>(x, P, tri, M, xv, fcs_dev, b7, w7, chunk, part);
+  // frequencies per thread: 2 shares the pair geometry but measured 2.5 %
+  // slower on cfg3 (7.41e9 vs 7.60e9 pair-evals/s: 96 bytes of spills and
+  // two interleaved phase evaluations at 168 registers), so 1
+#ifndef EWB_PK_FC
+#define EWB_PK_FC 1
+#endif
+  constexpr int kFc = EWB_PK_FC;
+  dim3 grid((unsigned)((P + 127) / 128), (unsigned)((F + kFc - 1) / kFc), nchunk);
+  EWB_NOTE k_pair_reduce<kFc><<<grid, 128, 0, s>>>(x, P, tri, M, xv, fcs_dev, F, b7, w7, chunk,
+                                                   part);
   long long tot = (long long)F * P * 6;
   EWB_NOTE k_pair_reduce_final<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, nchunk, F, P, yu, yt);
   return cudaGetLastError();

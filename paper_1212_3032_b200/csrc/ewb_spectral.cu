@@ -80,6 +80,19 @@ __global__ void k_math_selftest(const double* x, long long n, double* s, double*
   e[i] = fast_exp(x[i]);
 }
 
+// exp_small (the damping-factor update between the quadrature points of a
+// far pair) on host arguments |t| <= 2^-4
+__global__ void k_math_selftest_delta(const double* t, long long n, double* e) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) e[i] = exp_small(t[i]);
+}
+
+cudaError_t launch_math_selftest_delta(const double* t, long long n, double* e, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  EWB_NOTE k_math_selftest_delta<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(t, n, e);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_math_selftest(const double* x, long long n, double* s, double* c, double* e,
                                  cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

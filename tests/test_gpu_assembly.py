@@ -342,3 +342,13 @@ def test_device_sincos_exp_vs_libm(cuda):
     assert np.isnan(e[np.isnan(x)]).all() and e[x == np.inf][0] == np.inf
     assert e[x == -np.inf][0] == 0.0 and e[x == -800.0][0] == 0.0 and e[x == 710.0][0] == np.inf
     assert e[x == -745.0][0] <= 1e-323
+    # exp_small: the damping-factor step between a far pair's quadrature points
+    t = np.concatenate([rng.uniform(-0.0625, 0.0625, 300_000), rng.uniform(-1e-3, 1e-3, 100_000),
+                        10.0 ** rng.uniform(-300, -3, 50_000), [0.0, -0.0, 0.0625, -0.0625]])
+    es = np.empty(len(t))
+    _lib.check(lib.ewb_math_selftest_delta(t.ctypes.data, len(t), es.ctypes.data,
+                                           _lib.stream_handle()))
+    ulp = np.abs(es - np.exp(t)) / np.spacing(np.exp(t))
+    assert ulp.max() <= 1.0, ulp.max()
+    assert lib.ewb_math_selftest_delta(np.array([0.07]).ctypes.data, 1, es.ctypes.data,
+                                       _lib.stream_handle()) != 0

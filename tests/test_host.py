@@ -109,7 +109,7 @@ def test_library_exports_every_declared_symbol():
     assert sorted(_lib.EXPORTS) == declared
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.ewb_abi_version() == _lib.ABI_VERSION == 5
+    assert lib.ewb_abi_version() == _lib.ABI_VERSION == 6
     out = subprocess.run(["nm", "-D", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     for name in declared:
         assert re.search(rf" T {name}$", out, re.M), name
