@@ -719,6 +719,36 @@ def _unit():
     return Material.from_young_poisson(1.0, 0.25, 1.0)
 
 
+@pytest.mark.parametrize("K,n", [(3, 1111), (4, 1111), (4, 513), (3, 40), (4, 2304)])
+def test_sem_ring_staged_x_ragged_sizes(cuda, K, n):
+    """SEM's Y = A X for K = 3, 4 stages the x chunks in the TMA ring next to 8
+    rows of A (matvec_rows_wide<K, XS>): sizes with a ragged last column tile,
+    a one-column second tile, fewer columns than one tile and the cfg1 size,
+    against the oracle's least squares (linsolve.py:213-242) and, through the
+    returned A x0, against numpy's product."""
+    torch = cuda
+    from oracle import ewbem_oracle as O
+    from paper_1212_3032_b200.linsolve import sem_device
+
+    rng = np.random.default_rng(100 * K + n)
+    A = rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n)) + 3 * np.sqrt(n) * np.eye(n)
+    base = rng.normal(size=n) + 1j * rng.normal(size=n)
+    X = np.stack([base * (1 + 0.1 * i) + 1e-2 * (rng.normal(size=n) + 1j * rng.normal(size=n))
+                  for i in range(K)])
+    b = A @ (base * 1.07) + 1e-3 * rng.normal(size=n)
+    oh = O.History(K)
+    for i in range(K - 1, -1, -1):
+        oh.push(X[i])
+    ref = O.sem_guess(oh, A, b)
+    Ad = torch.from_numpy(A).cuda()
+    x0 = torch.empty(n, dtype=torch.complex128, device="cuda")
+    ax0 = torch.empty_like(x0)
+    sem_device(Ad, torch.from_numpy(b).cuda(), torch.from_numpy(X).cuda(), 1e-10, x0, ax0_out=ax0)
+    got = x0.cpu().numpy()
+    assert rel_max(got, ref) <= 1e-9
+    assert rel_max(ax0.cpu().numpy(), A @ got) <= 1e-12
+
+
 @pytest.mark.parametrize("K", [5, 6, 8])
 def test_sem_deep_history_vs_oracle(cuda, K):
     """SEM with K > 4 history columns (Y = A X in passes of 4; linsolve.py:213-242)
