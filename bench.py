@@ -425,8 +425,10 @@ def run_ours_sweep(args, rank, world, local_rank):
         "pipe_frac_standalone": round(counts["far"] * far_instr / (sa_per_freq * 1e-3) / dfma_rate, 4),
         "pipe_frac_in_sweep": round(counts["far"] * far_instr / (asm_per_freq_ms * 1e-3) / dfma_rate, 4),
         "flop_frac_standalone": round(counts["far"] * far_flops / (sa_per_freq * 1e-3) / 1e12 / peak64, 4),
-        "note": "upper bounds: the whole assembly time is charged to the far pairs; the "
-                "phase recurrence removed the transcendentals the algorithmic count credits",
+        "note": "far-pair instructions over the WHOLE assembly time (mid / near / self kernels "
+                "included in the time, not in the instructions): a lower bound on k_far_multi's "
+                "own FP64 pipe fraction (ncu: 57.5 % active); the phase recurrence removed the "
+                "transcendentals the algorithmic count credits",
         "source": "static SASS count of the member loop (tools/sass_loops.py), "
                   "profiles/r02/SUMMARY.md"}
     rl_asm["note"] = ("in-sweep figure: assembly runs between power-capped GMRES phases "

@@ -100,10 +100,21 @@ constexpr int kMfQUnroll = EWB_MF_QUNROLL;
 // SER = false: no far pair of this application can reach the series branch
 // (mf_launch checks |k_s| x the far-pair distance bound, as series_free in
 // ewb_assembly.cu); mid pairs always keep the check.
+// K >= kMfYsMin: the K x 3 row outputs live in shared memory ([k][a][thread],
+// conflict-free 128-bit accesses) instead of 6 K registers per thread: they
+// are touched once per PAIR, and beside the 40-word accumulator they made the
+// K = 5 pass spill (804 bytes of spill stores in the <5, U> instance).
+#ifndef EWB_MF_YS_MIN
+#define EWB_MF_YS_MIN 3
+#endif
+constexpr int kMfYsMin = EWB_MF_YS_MIN;
 template <int K, bool USE_U, bool SER>
 __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_MF_MINB)
     k_mf_farmid(Geo g, Phys<true> ph, MfArgs m) {
   EWB_MF_GATE
+  constexpr bool YS = K >= kMfYsMin;
+  extern __shared__ __align__(16) unsigned char mf_dyn[];   // YS: K x 3 x 128 complex
+  cplx* s_yacc = reinterpret_cast<cplx*>(mf_dyn);
   __shared__ double s_geo[kMfTile][8];        // cx cy cz diam nx ny nz area
   __shared__ double s_y[kMfTile][30];         // 3 far + 7 mid points
   __shared__ cplx s_vt[kMfTile][K][3];
@@ -116,11 +127,14 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
   const bool row_ok = i < n;
   double xi = 0, yi = 0, zi = 0;
   if (row_ok) { xi = g.cx[i]; yi = g.cy[i]; zi = g.cz[i]; }
-  cplx y[K][3];
+  cplx y[YS ? 1 : K][3];
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int a = 0; a < 3; ++a) y[k][a] = {0.0, 0.0};
+    for (int a = 0; a < 3; ++a) {
+      if (YS) s_yacc[(k * 3 + a) * 128 + threadIdx.x] = {0.0, 0.0};
+      else y[YS ? 0 : k][a] = {0.0, 0.0};
+    }
   for (int t0 = j_begin; t0 < j_end; t0 += kMfTile) {
     const int tc = min(kMfTile, j_end - t0);
     __syncthreads();
@@ -258,8 +272,26 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        if ((m.t_mask >> k) & 1u) acc_apply_T(acc, nx, ny, nz, 1.0, s_vt[jj][k], y[k]);
-        if (USE_U && ((m.u_mask >> k) & 1u)) acc_apply_U(acc, 1.0, s_vu[jj][k], y[k]);
+        const bool dt = (m.t_mask >> k) & 1u, du = USE_U && ((m.u_mask >> k) & 1u);
+        if (YS) {
+          if (!dt && !du) continue;
+          cplx yk[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const double2 v2 = *reinterpret_cast<const double2*>(
+                &s_yacc[(k * 3 + a) * 128 + threadIdx.x]);
+            yk[a] = {v2.x, v2.y};
+          }
+          if (dt) acc_apply_T(acc, nx, ny, nz, 1.0, s_vt[jj][k], yk);
+          if (du) acc_apply_U(acc, 1.0, s_vu[jj][k], yk);
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            *reinterpret_cast<double2*>(&s_yacc[(k * 3 + a) * 128 + threadIdx.x]) =
+                make_double2(yk[a].re, yk[a].im);
+        } else {
+          if (dt) acc_apply_T(acc, nx, ny, nz, 1.0, s_vt[jj][k], y[YS ? 0 : k]);
+          if (du) acc_apply_U(acc, 1.0, s_vu[jj][k], y[YS ? 0 : k]);
+        }
       }
     }
   }
@@ -268,7 +300,9 @@ __global__ void __launch_bounds__(128, (K == 1 && !USE_U) ? EWB_MF1_MINB : EWB_M
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int a = 0; a < 3; ++a) out[(size_t)k * N + 3 * i + a] = y[k][a];
+    for (int a = 0; a < 3; ++a)
+      out[(size_t)k * N + 3 * i + a] =
+          YS ? s_yacc[(k * 3 + a) * 128 + threadIdx.x] : y[YS ? 0 : k][a];
 }
 
 template <int K, bool USE_U>
@@ -428,10 +462,19 @@ static cudaError_t mf_launch(Context& c, Phys<true> ph, MfArgs m, cudaStream_t s
   Phys<true> phf = ph;
   phf.fc.sw = kFarSwitch;
   // far pairs: r >= 3 d_j >= 2.9 min d (series_free, ewb_assembly.cu)
+  constexpr size_t ys_bytes = K >= kMfYsMin ? sizeof(cplx) * K * 3 * 128 : 0;
+  static bool attr = false;
+  if (!attr && ys_bytes) {   // static + dynamic shared memory exceeds the 48 KB default
+    cudaFuncSetAttribute(k_mf_farmid<K, USE_U, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ys_bytes);
+    cudaFuncSetAttribute(k_mf_farmid<K, USE_U, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ys_bytes);
+    attr = true;
+  }
   if (c.min_diam > 0.0 && ph.fc.ks_abs * (2.9 * c.min_diam) >= kFarSwitch)
-    EWB_NOTE k_mf_farmid<K, USE_U, false><<<grid, 128, 0, s>>>(c.g, phf, m);
+    EWB_NOTE k_mf_farmid<K, USE_U, false><<<grid, 128, ys_bytes, s>>>(c.g, phf, m);
   else
-    EWB_NOTE k_mf_farmid<K, USE_U, true><<<grid, 128, 0, s>>>(c.g, phf, m);
+    EWB_NOTE k_mf_farmid<K, USE_U, true><<<grid, 128, ys_bytes, s>>>(c.g, phf, m);
   if (c.n_near)
     EWB_NOTE k_mf_near<K, USE_U><<<(c.n_near * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m, c.n_near);
   EWB_NOTE k_mf_self<K, USE_U><<<(n * 32 + 127) / 128, 128, 0, s>>>(c.g, ph, m);
