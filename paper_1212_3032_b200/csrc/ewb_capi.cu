@@ -546,10 +546,13 @@ cudaError_t fp64_peak_probe(long long iters, int blocks_per_sm, double* tflops, 
                             cudaStream_t s);
 }  // namespace ewb
 
+#ifndef EWB_PK_CTAS_PER_SM
+#define EWB_PK_CTAS_PER_SM 4
+#endif
 static int pair_chunks(int64_t P, int64_t M) {
   (void)M;
   int64_t pblocks = (P + 127) / 128;
-  int64_t want = (148 * 4 + pblocks - 1) / pblocks;
+  int64_t want = (148 * EWB_PK_CTAS_PER_SM + pblocks - 1) / pblocks;
   if (want < 1) want = 1;
   if (want > 16) want = 16;
   return (int)want;

@@ -481,14 +481,22 @@ static cudaError_t mf_launch(Context& c, Phys<true> ph, MfArgs m, cudaStream_t s
   return cudaGetLastError();
 }
 
+// CTAs the far/mid grid should have, in units of the SM count.  The K = 1
+// product runs at 4 CTAs/SM, so the old 148 x 8 CTAs were two waves and a
+// 16 %-full third one; measured on the cfg5 application (K = 1 / K = 5, ms,
+// A/B in one job): 8 -> 381 / 615, 16 -> 368 / 600, 32 -> 355 / 580,
+// 64 -> 349 / 571, 128 -> 348 / 568, 256 -> 346 / 566.
+#ifndef EWB_MF_CTAS_PER_SM
+#define EWB_MF_CTAS_PER_SM 256
+#endif
 int mf_chunks(const Context& c) {
-  // enough CTAs for >= 8 waves on 148 SMs, chunks of >= 256 columns
+  // chunks of >= 256 columns
   int row_blocks = (c.n_e + 127) / 128;
-  int want = (148 * 8 + row_blocks - 1) / row_blocks;
+  int want = (148 * EWB_MF_CTAS_PER_SM + row_blocks - 1) / row_blocks;
   int max_chunks = (c.n_e + 255) / 256;
   if (want > max_chunks) want = max_chunks;
   if (want < 1) want = 1;
-  if (want > 64) want = 64;
+  if (want > 128) want = 128;
   return want;
 }
 
