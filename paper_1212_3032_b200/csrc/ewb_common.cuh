@@ -800,6 +800,26 @@ __device__ __forceinline__ void point_apply_T(cplx y[3], const FreqConst& fc, do
   point_apply_T_br(y, f, fc.ratio, dx, dy, dz, dn, wt, v, nv, nx, ny, nz);
 }
 
+// The T product of one point from its weighted scalars Aw, Bw (2 dn folded
+// in), Cw (see point_apply_T).
+__device__ __forceinline__ void point_apply_T_w(cplx y[3], cplx Aw, cplx Bw, cplx Cw, double dx,
+                                                double dy, double dz, double dn, const cplx v[3],
+                                                cplx nv, double nx, double ny, double nz) {
+  cplx sv = dx * v[0];
+  axpy(sv, dy, v[1]);
+  axpy(sv, dz, v[2]);
+  const cplx e = dn * Aw, h = Aw * sv;
+  cplx gg = Bw * sv;
+  cfma(gg, Cw, nv);
+  const double n[3] = {nx, ny, nz}, d[3] = {dx, dy, dz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cfma(y[a], e, v[a]);
+    axpy(y[a], n[a], h);
+    axpy(y[a], d[a], gg);
+  }
+}
+
 // The same with the point's damping factors supplied by the caller.
 template <bool SER = true>
 __device__ __forceinline__ void point_apply_T_m(cplx y[3], const FreqConst& fc, double sw, double r,
@@ -807,6 +827,25 @@ __device__ __forceinline__ void point_apply_T_m(cplx y[3], const FreqConst& fc, 
                                                 double dn, double wt, const cplx v[3], cplx nv,
                                                 double nx, double ny, double nz, double ms,
                                                 double mp) {
+#ifndef EWB_MF_BRACKETS
+  if (!(SER && fc.ks_abs * r < sw)) {
+    // weighted scalars straight from the linear basis (weights_phase): with
+    // the damping factors supplied, measured 1.6 % (low frequency) to 3.6 %
+    // (omega = 8) faster on the cfg5 application than the bracket form below
+    const double xa[2] = {fc.ks.re * r, fc.kp.re * r};
+    double s[2], c[2];
+    fast_sincos_n<2>(xa, s, c);
+    const cplx Es = {ms * c[0], -ms * s[0]};
+    const cplx Ep = fc.g2 * cplx{mp * c[1], -mp * s[1]};
+    const double ir2 = ir * ir;
+    const Weighted5 w = weights_phase(fc.ks, fc.kp, t_closed2(fc.tas, fc.tbs, ir, ir2),
+                                      t_closed2(fc.tap, fc.tbp, ir, ir2), r, Es, Ep, 0.0, wt,
+                                      c_num.two * wt * dn, fc.ratio - c_num.two,
+                                      c_num.four - fc.ratio);
+    point_apply_T_w(y, w.Aw, w.Bw, w.Cw, dx, dy, dz, dn, v, nv, nx, ny, nz);
+    return;
+  }
+#endif
   const Brackets f = SER && fc.ks_abs * r < sw ? brackets_series_cold(fc, r)
                                                : brackets_closed_m(fc, r, ir, ms, mp);
   point_apply_T_br(y, f, fc.ratio, dx, dy, dz, dn, wt, v, nv, nx, ny, nz);
