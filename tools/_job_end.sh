@@ -15,4 +15,4 @@ python tools/prof_mf.py > gpurun_out/end_plain_mf.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_mf_farmid -c 1 -o gpurun_out/end_mf python tools/prof_mf.py > gpurun_out/end_ncu_mf.log 2>&1; echo mf_rc=$?
 python tools/sem_time.py > gpurun_out/end_sem_time.log 2>&1; echo sem_rc=$?
 timeout 600 python tools/cfg5_probe.py 33 > gpurun_out/end_cfg5_sweep.log 2>&1; echo cfg5_rc=$?
-for w in cfg1 cfg4; do timeout 600 python bench.py --workload $w --steps 5 --warmup 3 > gpurun_out/end_bench_$w.log 2>&1; done
+for w in cfg1 cfg3 cfg4; do timeout 600 python bench.py --workload $w --steps 5 --warmup 3 > gpurun_out/end_bench_$w.log 2>&1; done
