@@ -856,6 +856,26 @@ __device__ __forceinline__ void point_dynamic_scaled_m(Acc<cplx>& A, const FreqC
                                                        double sw, double r, double ir, double dx,
                                                        double dy, double dz, double dn, double wu,
                                                        double wt, double ms, double mp) {
+#ifndef EWB_MF_ACC_BRACKETS
+  // linear-basis weights as in point_apply_T_m, in the series-free instances
+  // only: measured on the masked K = 5 cfg5 pass, 567 -> 556 ms at omega = 8
+  // (SER = false) but 601 -> 659 ms at low frequency, where the kernel also
+  // carries the series call (register pressure)
+  if (!SER) {
+    const double xa[2] = {fc.ks.re * r, fc.kp.re * r};
+    double s[2], c[2];
+    fast_sincos_n<2>(xa, s, c);
+    const cplx Es = {ms * c[0], -ms * s[0]};
+    const cplx Ep = fc.g2 * cplx{mp * c[1], -mp * s[1]};
+    const double ir2 = ir * ir;
+    const Weighted5 w = weights_phase(fc.ks, fc.kp, t_closed2(fc.tas, fc.tbs, ir, ir2),
+                                      t_closed2(fc.tap, fc.tbp, ir, ir2), r, Es, Ep, wu, wt,
+                                      c_num.two * wt * dn, fc.ratio - c_num.two,
+                                      c_num.four - fc.ratio);
+    acc_point(A, w.Phi, w.Psi, w.Aw, w.Bw, w.Cw, dx, dy, dz, dn);
+    return;
+  }
+#endif
   const Brackets f = SER && fc.ks_abs * r < sw ? brackets_series_cold(fc, r)
                                                : brackets_closed_m(fc, r, ir, ms, mp);
   const cplx Phi = wu * f.f0;
