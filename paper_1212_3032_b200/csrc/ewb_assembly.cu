@@ -694,13 +694,8 @@ constexpr int kFarGeo = 8;
 // groups start at 0, 8, 20, 28 (mod 16: 0, 8, 4, 12) and the row stride is
 // 1 mod 16: stores and loads are conflict-free (stride 33 with groups at
 // 0, 8, 16, 24 made every load a 2-way conflict).
-#ifdef EWB_FAR_BRED_OLD
-constexpr int kBredStride = 33;
-__device__ __forceinline__ int bred_pos(int l) { return l; }
-#else
 constexpr int kBredStride = 49;
 __device__ __forceinline__ int bred_pos(int l) { return l + 4 * (l >> 4); }
-#endif
 // per-member constants of the closed-form point, 16-byte aligned so one
 // 128-bit load fetches a complex: ks, kp, tas, tbs, tap, tbp
 constexpr int kFarMc = 6;
@@ -768,11 +763,7 @@ template <bool RECUR, bool SER>
 __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Geo g, FreqBatch fb,
                                                                       SysBatch o) {
   extern __shared__ __align__(16) double sm_far[];
-#ifdef EWB_FAR_BD_RUNTIME
-  const int BD = blockDim.x;
-#else
   constexpr int BD = kFarThreads;   // always launched with kFarThreads: immediate smem offsets
-#endif
   const int tid = threadIdx.x;
   // [slot][q][thread] with a block-size stride (conflict-free)
   auto SG = [&](int slot, int q) -> double& { return sm_far[(slot * 3 + q) * BD + tid]; };
@@ -812,11 +803,7 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
     const unsigned kbits = (o.kinds[3 * jj] == kDirichlet ? 1u : 0u) |
                            (o.kinds[3 * jj + 1] == kDirichlet ? 2u : 0u) |
                            (o.kinds[3 * jj + 2] == kDirichlet ? 4u : 0u);
-#ifdef EWB_FAR_ALWAYS_MIXED
-    const bool tile_mixed = true;
-#else
     const bool tile_mixed = __any_sync(0xffffffffu, kbits != 0);
-#endif
     for (int r = 0; r < kFarRows; ++r) {
       const int i = rg * kFarRows + r;
       if (i >= g.n_e) break;
@@ -877,16 +864,10 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
             const double rr = SG(0, q), ir = SG(1, q);
             const double dx = SG(2, q), dy = SG(3, q), dz = SG(4, q);
             const double dn2 = SG(5, q), wu = SG(6, q), wt = SG(7, q);
-#ifndef EWB_FAR_MC64
             const cplx* mc = smc + f * kFarMc;
             const cplx ks = lds_c16(mc), kp = lds_c16(mc + 1);
             const cplx ts = t_closed(lds_c16(mc + 2), lds_c16(mc + 3), ir);
             const cplx tp = t_closed(lds_c16(mc + 4), lds_c16(mc + 5), ir);
-#else
-            const cplx ks = lds_c(&sfc[f].ks), kp = lds_c(&sfc[f].kp);
-            const cplx ts = t_closed(lds_c(&sfc[f].tas), lds_c(&sfc[f].tbs), ir);
-            const cplx tp = t_closed(lds_c(&sfc[f].tap), lds_c(&sfc[f].tbp), ir);
-#endif
             cplx Es, Ep;
             if (RECUR) {
               Es = SP(0, q);
@@ -938,7 +919,6 @@ __global__ void __launch_bounds__(kFarThreads, EWB_FARMULTI_MINB) k_far_multi(Ge
         if (lane < 24) {
           const int v = lane >> 2, pp = lane & 3;
           const double* src = sbr + v * kBredStride + bred_pos(8 * pp);
-          (void)v;
           double sum = ((src[0] + src[1]) + (src[2] + src[3])) + ((src[4] + src[5]) + (src[6] + src[7]));
           sum += __shfl_xor_sync(0x00ffffffu, sum, 1);
           sum += __shfl_xor_sync(0x00ffffffu, sum, 2);
