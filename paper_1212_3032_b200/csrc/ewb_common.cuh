@@ -836,7 +836,15 @@ __device__ __forceinline__ void point_apply_T_m(cplx y[3], const FreqConst& fc, 
     double s[2], c[2];
     fast_sincos_n<2>(xa, s, c);
     const cplx Es = {ms * c[0], -ms * s[0]};
+#ifdef EWB_MF_G2_COMPLEX
     const cplx Ep = fc.g2 * cplx{mp * c[1], -mp * s[1]};
+#else
+    // g2 = (k_p / k_s)^2 = (c_s / c_p)^2 is real for the real materials of
+    // the reference (its complex value carries ~1e-17 of rounding in the
+    // imaginary part): folded into the damping factor as a real scalar
+    const double mpg = mp * fc.g2.re;
+    const cplx Ep = {mpg * c[1], -mpg * s[1]};
+#endif
     const double ir2 = ir * ir;
     const Weighted5 w = weights_phase(fc.ks, fc.kp, t_closed2(fc.tas, fc.tbs, ir, ir2),
                                       t_closed2(fc.tap, fc.tbp, ir, ir2), r, Es, Ep, 0.0, wt,
@@ -866,7 +874,15 @@ __device__ __forceinline__ void point_dynamic_scaled_m(Acc<cplx>& A, const FreqC
     double s[2], c[2];
     fast_sincos_n<2>(xa, s, c);
     const cplx Es = {ms * c[0], -ms * s[0]};
+#ifdef EWB_MF_G2_COMPLEX
     const cplx Ep = fc.g2 * cplx{mp * c[1], -mp * s[1]};
+#else
+    // g2 = (k_p / k_s)^2 = (c_s / c_p)^2 is real for the real materials of
+    // the reference (its complex value carries ~1e-17 of rounding in the
+    // imaginary part): folded into the damping factor as a real scalar
+    const double mpg = mp * fc.g2.re;
+    const cplx Ep = {mpg * c[1], -mpg * s[1]};
+#endif
     const double ir2 = ir * ir;
     const Weighted5 w = weights_phase(fc.ks, fc.kp, t_closed2(fc.tas, fc.tbs, ir, ir2),
                                       t_closed2(fc.tap, fc.tbp, ir, ir2), r, Es, Ep, wu, wt,
